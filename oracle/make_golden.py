@@ -1,0 +1,285 @@
+"""Generate tests/golden/ fixtures by running the REFERENCE implementation.
+
+Run in the build container only (it needs /root/reference):
+
+    python oracle/make_golden.py
+
+It copies /root/reference/pkg/src to a scratch dir (so nothing is written
+into the read-only reference tree), imports `skiff` from there, and records
+on seeded inputs:
+
+  * kernels.npz   — matmul / layer_norm / softmax / log_softmax / sigmoid /
+                    multi-head attention outputs (kernels.py:167-547)
+  * params.json   — per-parameter float64 checksums of init_params for every
+                    fixture config (model.py:244-265)
+  * steps_<cfg>.npz — teacher-forced decode_step logits along a fixed token
+                    path, plus select_rows reorders (model.py:521-585, 316-330)
+  * search.json   — translate() records for greedy / beam / alpha / shortlist /
+                    NVS / prefix / strip / chunking / error cases
+                    (search.py:275-468)
+  * beam_trace_<cfg>.npz — per-step lp, alive scores and picks of a beam run,
+                    captured by wrapping Model.decode_step and
+                    DecodeState.select_rows (never editing the reference)
+
+The oracle (oracle/skiff_oracle.py) is then checked against these files by
+tests/test_oracle_golden.py; the CUDA path is checked against the oracle and
+against these files by the -m gpu tests.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import shutil
+import sys
+import tempfile
+from pathlib import Path
+from types import SimpleNamespace
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+sys.path.insert(0, str(ROOT))
+from oracle.fixture_configs import CONFIGS, SEARCH_CASES, make_words  # noqa: E402
+
+
+def import_reference():
+    src = Path("/root/reference/pkg/src")
+    if not src.is_dir():
+        raise SystemExit("make_golden.py needs /root/reference (build container only)")
+    tmp = Path(tempfile.mkdtemp(prefix="skiff_ref_"))
+    shutil.copytree(src, tmp / "src")
+    os.environ["PYTHONDONTWRITEBYTECODE"] = "1"
+    os.environ.setdefault("NUMBA_CACHE_DIR", str(tmp / "numba"))
+    sys.path.insert(0, str(tmp / "src"))
+    import skiff  # noqa: F401
+    return tmp
+
+
+def ref_model(name):
+    from skiff.model import Model, ModelConfig, SourceFactorSpec, TargetFactorSpec
+    spec = CONFIGS[name]
+    cfg = dict(spec["config"])
+    cfg["source_factor_specs"] = [SourceFactorSpec(*s) for s in cfg.get("source_factor_specs", [])]
+    cfg["target_factor_specs"] = [TargetFactorSpec(v) for v in cfg.get("target_factor_specs", [])]
+    return Model(ModelConfig(**cfg), seed=spec["seed"])
+
+
+def ref_vocabs(name):
+    from skiff.vocab import FACTOR_SPECIALS, SPECIALS, Vocabulary
+    spec = CONFIGS[name]
+    cfg = spec["config"]
+    src = Vocabulary(SPECIALS + make_words(cfg["src_vocab_size"] - 4))
+    trg = Vocabulary(SPECIALS + make_words(cfg["trg_vocab_size"] - 4))
+    sfv = [Vocabulary(SPECIALS + [f"s{i}_{j}" for j in range(v - 4)])
+           for i, (v, _, _) in enumerate(cfg.get("source_factor_specs", []))]
+    tfv = [Vocabulary(FACTOR_SPECIALS + [f"F{i}_{j}" for j in range(v - 5)])
+           for i, v in enumerate(cfg.get("target_factor_specs", []))]
+    return SimpleNamespace(src_vocab=src, trg_vocab=trg, src_factor_vocabs=sfv,
+                           trg_factor_vocabs=tfv)
+
+
+def gen_kernels():
+    import skiff.kernels as K
+    from skiff.kernels import Tensor
+    rng = np.random.default_rng(1234)
+    out = {}
+    a = rng.normal(size=(5, 37)).astype(np.float32)
+    b = rng.normal(size=(37, 11)).astype(np.float32)
+    out["mm_a"], out["mm_b"] = a, b
+    out["mm_out"] = K.matmul(Tensor(a), Tensor(b)).data
+    x = rng.normal(size=(4, 3, 24)).astype(np.float32) * 3 + 1
+    g = rng.normal(size=(24,)).astype(np.float32)
+    bb = rng.normal(size=(24,)).astype(np.float32)
+    out["ln_x"], out["ln_g"], out["ln_b"] = x, g, bb
+    out["ln_out"] = K.layer_norm(Tensor(x), Tensor(g), Tensor(bb)).data
+    s = (rng.normal(size=(6, 50)) * 5).astype(np.float32)
+    out["sm_x"] = s
+    out["sm_out"] = K.softmax(Tensor(s)).data
+    out["lsm_out"] = K.log_softmax(Tensor(s)).data
+    out["sig_out"] = K.sigmoid(Tensor(s)).data
+    q = rng.normal(size=(2, 5, 16)).astype(np.float32)
+    kv = rng.normal(size=(2, 7, 16)).astype(np.float32)
+    ws = [rng.normal(size=(16, 16)).astype(np.float32) * 0.3 for _ in range(4)]
+    mask = np.where(np.arange(7)[None, :] >= np.array([5, 7])[:, None], -1e9, 0.0
+                    ).astype(np.float32)[:, None, None, :]
+    out["mha_q"], out["mha_kv"], out["mha_mask"] = q, kv, mask
+    for i, n in enumerate(("wq", "wk", "wv", "wo")):
+        out["mha_" + n] = ws[i]
+    out["mha_out"] = K.multi_head_attention(Tensor(q), Tensor(kv), Tensor(kv), 4,
+                                            *[Tensor(w) for w in ws], mask=mask).data
+    np.savez_compressed(GOLDEN / "kernels.npz", **out)
+
+
+def gen_params():
+    out = {}
+    for name in CONFIGS:
+        m = ref_model(name)
+        out[name] = {n: [float(t.data.astype(np.float64).sum()),
+                         float(np.abs(t.data.astype(np.float64)).sum()),
+                         float(t.data.ravel()[0]), float(t.data.ravel()[-1])]
+                     for n, t in m.params.items()}
+    (GOLDEN / "params.json").write_text(json.dumps(out, indent=0, sort_keys=True))
+
+
+def gen_steps():
+    """Teacher-forced decode along fixed paths, with a beam-style reorder."""
+    for name, spec in CONFIGS.items():
+        if not spec.get("steps"):
+            continue
+        m = ref_model(name)
+        cfg = m.config
+        rng = np.random.default_rng(99)
+        B, L, T = 3, spec["steps"]["L"], spec["steps"]["T"]
+        lens = np.array([L, max(1, L - 2), max(1, L // 2)])
+        src = rng.integers(4, cfg.src_vocab_size, size=(B, L))
+        for i, n in enumerate(lens):
+            src[i, n:] = 0
+        sf = [rng.integers(4, v.vocab_size, size=(B, L)) for v in cfg.source_factor_specs]
+        fed = rng.integers(4, cfg.trg_vocab_size, size=(T, B))
+        fed[0] = 2
+        fedf = [rng.integers(4, v.vocab_size, size=(T, B)) for v in cfg.target_factor_specs]
+        for f in fedf:
+            f[0] = 4
+        reorders = rng.integers(0, B, size=(T, B))
+        st = m.decode_init(src, sf, lens)
+        logits, facs = [], []
+        for t in range(T):
+            o = m.decode_step(st, fed[t], [f[t] for f in fedf])
+            logits.append(o.surface.data)
+            facs.append([f.data for f in o.factors])
+            st.select_rows(reorders[t])
+        out = dict(src=src, lens=lens, fed=fed, reorders=reorders,
+                   logits=np.stack(logits).astype(np.float32))
+        for i, s in enumerate(sf):
+            out[f"src_factor{i}"] = s
+        for k, f in enumerate(fedf):
+            out[f"fed_factor{k}"] = f
+            out[f"factor_logits{k}"] = np.stack([x[k] for x in facs]).astype(np.float32)
+        if spec["steps"].get("teacher"):
+            trg_in = fed.T[:1].repeat(1, 0)
+            full = m.forward_sequence(src[:1], [s[:1] for s in sf], lens[:1],
+                                      fed.T[:1], [f.T[:1] for f in fedf]).surface.data
+            out["teacher_logits"] = full.astype(np.float32)
+            del trg_in
+        if len(cfg.source_factor_specs) == 0 and cfg.nvs_enabled:
+            nvs = m.nvs_select(m.encode(src, sf, lens)[0], lens, 0.5, [0, 1, 3])
+            out["nvs_ids"] = np.concatenate(nvs)
+            out["nvs_counts"] = np.array([len(x) for x in nvs])
+        np.savez_compressed(GOLDEN / f"steps_{name}.npz", **out)
+
+
+def _records_to_json(records):
+    return [dict(text=r.text, score=r.score, factors=r.factors, chunks=r.chunks,
+                 forced_eos=r.forced_eos, error=r.error) for r in records]
+
+
+def gen_search():
+    from skiff.model import Model, ModelConfig
+    from skiff.search import (NvsRestriction, SearchSettings, SentenceInput,
+                              ShortlistRestriction, translate, chunk_input,
+                              parse_input_line)
+    from skiff.shortlist import Shortlist
+    results = []
+    for case in SEARCH_CASES:
+        m = ref_model(case["config"])
+        vocabs = ref_vocabs(case["config"])
+        if case.get("max_seq_len"):
+            cfg = ModelConfig(**{**vars(m.config), "max_seq_len": case["max_seq_len"]})
+            m = Model(cfg, params=m.params)
+        restriction = None
+        if case.get("shortlist"):
+            rows = {int(k): np.asarray(v, dtype=np.int64) for k, v in case["shortlist"].items()}
+            restriction = ShortlistRestriction(Shortlist(rows))
+        elif case.get("nvs") is not None:
+            restriction = NvsRestriction(case["nvs"])
+        settings = SearchSettings(beam=case.get("beam", 1), length_alpha=case.get("alpha", 1.0),
+                                  restriction=restriction, use_greedy=case.get("use_greedy"))
+        inputs = [SentenceInput(**inp) for inp in case["inputs"]]
+        records = translate(m, vocabs, inputs, settings)
+        results.append(dict(name=case["name"], records=_records_to_json(records)))
+    # host-logic goldens: parsing and chunking
+    lines = ['a b   c', '{"text": "a b", "source_prefix": "<t>", "target_prefix": "x y", '
+             '"target_prefix_factors": ["O O B"], "source_factors": ["P Q"]}',
+             '{"text": "a", "extra": 1}', '{bad json', '{"text": 3}']
+    parsed = []
+    for ln in lines:
+        try:
+            s = parse_input_line(ln)
+            parsed.append(dict(ok=True, tokens=s.tokens, source_factors=s.source_factors,
+                               source_prefix=s.source_prefix, target_prefix=s.target_prefix,
+                               target_prefix_factors=s.target_prefix_factors))
+        except Exception as e:  # noqa: BLE001
+            parsed.append(dict(ok=False, error=type(e).__name__))
+    chunks = [[c.tokens for c in chunk_input(SentenceInput(tokens=list("abcdefghij"),
+                                                           source_prefix=["<p>"]), 4)]]
+    (GOLDEN / "search.json").write_text(json.dumps(
+        dict(cases=results, parsed=parsed, chunks=chunks), indent=0))
+
+
+def gen_beam_traces():
+    """Wrap decode_step/select_rows to record what beam_search saw and chose."""
+    import skiff.kernels as K
+    from skiff.model import DecodeState, Model
+    from skiff.search import SentenceInput, beam_search
+    for name, spec in CONFIGS.items():
+        bt = spec.get("beam_trace")
+        if not bt:
+            continue
+        m = ref_model(name)
+        vocabs = ref_vocabs(name)
+        rng = np.random.default_rng(5)
+        words = vocabs.src_vocab.tokens[4:]
+        rec = {"lp": [], "parents": [], "fed": []}
+        orig_step, orig_sel = Model.decode_step, DecodeState.select_rows
+
+        def step(self, state, prev_ids, prev_factor_ids):
+            out = orig_step(self, state, prev_ids, prev_factor_ids)
+            rec["lp"].append(K.log_softmax(out.surface).data.copy())
+            rec["fed"].append(np.asarray(prev_ids).copy())
+            return out
+
+        def sel(self, idx):
+            rec["parents"].append(np.asarray(idx).copy())
+            return orig_sel(self, idx)
+
+        Model.decode_step, DecodeState.select_rows = step, sel
+        try:
+            toks = list(rng.choice(words, size=bt["L"]))
+            hyp = beam_search(m, vocabs, SentenceInput(tokens=toks), bt["beam"],
+                              length_alpha=bt.get("alpha", 1.0))
+        finally:
+            Model.decode_step, DecodeState.select_rows = orig_step, orig_sel
+        keep = bt.get("keep_lp_steps")
+        out = dict(src=np.array(vocabs.src_vocab.encode(toks)),
+                   hyp_tokens=np.array(hyp.tokens, dtype=np.int64),
+                   hyp_logprob=np.array(hyp.logprob), hyp_steps=np.array(hyp.steps),
+                   hyp_forced=np.array(hyp.forced_eos),
+                   n_steps=np.array(len(rec["lp"])))
+        for t, (lp, fed) in enumerate(zip(rec["lp"], rec["fed"])):
+            out[f"fed{t}"] = fed
+            if keep is None or t in keep or t == len(rec["lp"]) - 1:
+                out[f"lp{t}"] = lp
+        for t, p in enumerate(rec["parents"]):
+            out[f"parents{t}"] = p
+        np.savez_compressed(GOLDEN / f"beam_trace_{name}.npz", **out)
+
+
+def main():
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    tmp = import_reference()
+    try:
+        gen_kernels()
+        gen_params()
+        gen_steps()
+        gen_search()
+        gen_beam_traces()
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    for p in sorted(GOLDEN.iterdir()):
+        print(f"{p.name:32s} {p.stat().st_size:>9d} B")
+
+
+if __name__ == "__main__":
+    main()
