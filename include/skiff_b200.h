@@ -1,0 +1,233 @@
+/*
+ * skiff_b200.h — C ABI of the B200-native translation hot path.
+ *
+ * The reference (skiff, /root/reference/pkg/src/skiff) is pure Python/numpy:
+ * it has no FFI.  Each entry point below replaces one numpy "kernel" or one
+ * piece of search bookkeeping on the decode path; the citation names the
+ * reference function it replaces (file:line).  The Python host package
+ * (paper_2207_05851_b200) binds these with ctypes and mirrors the reference's
+ * translate / Model.decode_init / decode_step interface on top.
+ *
+ * Conventions:
+ *   - plain device pointers + int sizes; no torch types; every call is
+ *     stream-ordered on the caller's cudaStream_t (passed as void*);
+ *   - nothing here allocates or frees device memory; caller owns all buffers;
+ *   - every function returns an int status (SKB_OK = 0).  The matching
+ *     message is available from skb_last_error() (thread-local).  The host
+ *     maps SKB_ERR_SHAPE -> ShapeError, SKB_ERR_CONFIG -> ConfigError,
+ *     SKB_ERR_NUMERIC -> NumericError, others -> RuntimeError;
+ *   - "step" arguments are device pointers so a whole decode step can be
+ *     captured once into a CUDA graph and replayed.
+ */
+#ifndef SKIFF_B200_H
+#define SKIFF_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SKB_OK 0
+#define SKB_ERR_SHAPE 1
+#define SKB_ERR_CONFIG 2
+#define SKB_ERR_LAUNCH 3
+#define SKB_ERR_NUMERIC 4
+#define SKB_ERR_UNSUPPORTED 5
+
+/* element types */
+#define SKB_F32 0
+#define SKB_BF16 1
+
+/* GEMM epilogues */
+#define SKB_EPI_STORE 0  /* out = acc (+bias)                                 */
+#define SKB_EPI_RELU 1   /* out = relu(acc + bias)        (kernels.py:243-250) */
+#define SKB_EPI_RESID 2  /* x  += acc (+bias), x fp32     (model.py:565-574)   */
+#define SKB_EPI_SSRU 3   /* SSRU cell, columns interleaved (f_j, Wx_j)         */
+                         /*                               (model.py:268-272)   */
+
+/* GEMM epilogue parameters (plain C struct, passed by pointer). */
+typedef struct skb_epilogue {
+  int kind;              /* SKB_EPI_*                                          */
+  const float *bias;     /* [N] or NULL                                        */
+  void *out;             /* STORE/RELU: [M, ldo] of out_dtype; RESID/SSRU: x   */
+  int ldo;               /* leading dim of out (elements)                      */
+  int out_dtype;         /* SKB_F32 / SKB_BF16 (RESID/SSRU: must be F32)       */
+  /* SSRU only: cell state, fp32 [M, ld_state]; c_prev row = src_row[m]       */
+  const float *c_prev;   /* NULL => zero previous cell (first step)            */
+  float *c_next;
+  const int *src_row;    /* NULL => identity                                   */
+  int ld_state;
+} skb_epilogue;
+
+/* Library identity / diagnostics */
+const char *skb_version(void);
+const char *skb_last_error(void);
+/* 1 if the tcgen05 GEMM path is usable on the current device (sm_100). */
+int skb_tc_available(void);
+
+/*
+ * C[M,N] = A[M,K] . W[N,K]^T with a fused epilogue.
+ * Replaces kernels.py:479-484 (linear) / 167-195 (matmul, fp64-accumulated):
+ * fp32 inputs use a SIMT FFMA kernel (fp32 accumulate); bf16 inputs use the
+ * tcgen05/TMEM/TMA kernel (fp32 accumulate in TMEM).  A and W are K-major
+ * (row-major), exactly the reference's (out, in) weight layout.
+ */
+int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
+             int ldw, const skb_epilogue *epi, void *stream);
+
+/* Same, forcing the SIMT path (for parity tests of the tcgen05 path). */
+int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
+                  int ldw, const skb_epilogue *epi, void *stream);
+
+/*
+ * Pre-norm layer norm over rows of width d, population variance, eps.
+ * Replaces kernels.py:298-324.  x fp32 [rows, ldx]; out [rows, ldo] out_dtype.
+ */
+int skb_layernorm(int rows, int d, const float *x, int ldx, const float *gain,
+                  const float *bias, float eps, void *out, int ldo, int out_dtype,
+                  void *stream);
+
+/*
+ * Target-side step embedding (model.py:399-410, 545-547):
+ * x[r] = E[tok[r]] + PE[*step] + sum_k F_k[ftok[k*rows + r]].
+ * pe: [max_steps, d] fp32 position table (float64 sin/cos cast to fp32).
+ * ftables: array (device) of n_factors device pointers to [V_k, d] fp32.
+ */
+int skb_embed_target(int rows, int d, const int *tok, const float *E, const float *pe,
+                     const int *step, int n_factors, const int *ftok,
+                     const float *const *ftables, float *x, void *stream);
+
+/*
+ * Source embedding (model.py:370-397) for B x L padded ids:
+ * surface E_src[id] + PE over the first ds = d - sum(concat dims) columns,
+ * concat factor embeddings after it, then sum-combined factors added.
+ * fdims[i] = factor dim, fcombine[i] = 0 sum / 1 concat (host arrays),
+ * fids: device [n_factors, B*L]; ftables: device array of device pointers.
+ */
+int skb_embed_source(int B, int L, int d, int ds, const int *ids, const float *E,
+                     const float *pe, int n_factors, const int *fdims_host,
+                     const int *fcombine_host, const int *fids,
+                     const float *const *ftables, float *x, void *stream);
+
+/*
+ * Encoder self-attention (kernels.py:510-547 with the pad bias of
+ * model.py:174-179): qkv [B*L, ld_qkv] holds q | k | v (each d wide, dtype
+ * qkv_dtype); lengths [B] int; ctx [B*L, ldc] in ctx_dtype.
+ */
+int skb_encoder_attention(int B, int L, int H, int dh, const void *qkv, int ld_qkv,
+                          int qkv_dtype, const int *lengths, void *ctx, int ldc,
+                          int ctx_dtype, void *stream);
+
+/*
+ * Incremental decoder self-attention for one step (model.py:559-567):
+ * row r attends over positions 0..t (t = *step) of its hypothesis.  New k,v
+ * (from qkv) are stored at cache slot (r, t); earlier positions p < t are
+ * read from slot anc[(t&1)][r][p] (ancestor table) — the beam
+ * reorder never moves cache bytes.  kc/vc: [R_cap, S_max, H*dh] cache_dtype.
+ */
+int skb_self_attention_step(int R, int H, int dh, const void *qkv, int ld_qkv, int qkv_dtype,
+                            void *kc, void *vc, int cache_dtype, int S_max, const int *anc,
+                            const int *step, void *ctx, int ldc, int ctx_dtype, void *stream);
+
+/*
+ * Cross-attention for one step (model.py:568-573): q [R, ldq]; row r reads
+ * sentence row_sent[r] of the per-sentence encoder K/V memory
+ * kv [B*L, ld_kv] (K at column offset koff, V at voff), masked past
+ * lengths[sentence].
+ */
+int skb_cross_attention_step(int R, int H, int dh, const void *q, int ldq, int q_dtype,
+                             const void *kv, int ld_kv, int kv_dtype, int koff, int voff,
+                             int L, const int *row_sent, const int *lengths, void *ctx,
+                             int ldc, int ctx_dtype, void *stream);
+
+/* Gather rows of a table: out[i] = table[idx[i]] (row width w, dtype). Used to
+ * build the restricted output-projection operand E[active] (model.py:577-581). */
+int skb_gather_rows(int n, int w, const void *table, int ld_table, const int *idx,
+                    void *out, int ld_out, int dtype, void *stream);
+
+/*
+ * Beam search step state (all device memory, sized by the caller).
+ * Rows are slots r = b*K + i (sentence b, beam position i).
+ * Replaces the per-step body of search.py:345-393 (and greedy 292-312,
+ * which is its beam = 1 special case, bit-identical per test_search.py:170).
+ */
+typedef struct skb_beam_state {
+  int B, K, U;            /* sentences, beam, columns of the logits          */
+  int S_max;              /* history capacity (steps)                        */
+  int n_factors;          /* target factor streams                           */
+  double alpha;           /* length penalty exponent (search.py:74-75)       */
+  const int *step;        /* device: current step t                          */
+  const int *col_token;   /* [U] token id of column (NULL: identity)         */
+  const unsigned *mask;   /* [B, ceil(U/32)] active-column bits (NULL: all)  */
+  int eos_col;            /* column of EOS                                    */
+  const int *max_len;     /* [B] 2*L+10 per sentence (search.py:231)          */
+  const int *prefix_len;  /* [B]                                              */
+  const int *prefix_col;  /* [B, P] forced column per step (search.py:296)   */
+  int P;
+  const int *prefix_fac;  /* [B, n_factors, P] prefix factor ids or -1        */
+  int *n_alive;           /* [B] alive rows (starts at 1)                     */
+  int *done;              /* [B] sentence finished flag                       */
+  double *score;          /* [R] alive hypothesis log-prob (float64)         */
+  double *score_next;     /* [R]                                              */
+  int *tok_next;          /* [R] token fed at the next step                   */
+  int *ftok_next;         /* [n_factors, R] factor ids fed next step          */
+  int *parent;            /* [R] parent slot of each new row                   */
+  int *tok_hist;          /* [S_max, R] token appended at step t              */
+  int *par_hist;          /* [S_max, R] parent beam index at step t           */
+  int *fac_hist;          /* [S_max, n_factors, R] factor of the new row       */
+  const float *fac_logits;/* [n_factors] x [R, fac_ld] concatenated, or NULL  */
+  int fac_ld;             /* row stride of fac_logits                          */
+  const int *fac_off;     /* [n_factors+1] column offsets into fac_logits     */
+  /* scratch */
+  double *cand_score;     /* [R, K] */
+  float *cand_lp;         /* [R, K] */
+  int *cand_col;          /* [R, K] */
+  int *cand_cnt;          /* [R]    */
+  int *row_argmax;        /* [R]    */
+  int *fac_choice;        /* [R, n_factors] */
+  unsigned *counter;      /* [B] zero-initialised arrival counters            */
+  /* best finished hypothesis per sentence (search.py:394) */
+  double *best_norm;      /* [B] */
+  double *best_logprob;   /* [B] */
+  int *best_steps;        /* [B] 0 = none yet */
+  int *best_forced;       /* [B] */
+  int *best_parent;       /* [B] beam index of the parent row at best_t */
+  int *best_fac;          /* [B, n_factors] factor entry of the EOS step */
+  int *n_done;            /* [1] sentences finished (for host polling)      */
+} skb_beam_state;
+
+/*
+ * One beam step over fp32 logits [R, ld_logits]: per row masked
+ * log-softmax (kernels.py:287-295), float64 candidate scores, exact
+ * (score desc, token asc, parent asc) top-K per sentence (search.py:363),
+ * EOS routing, forced prefix/EOS steps, finished-hypothesis tracking.
+ * If lp_in is non-zero the logits are taken as already-normalised fp32
+ * log-probs (bit-exact parity harness: "given identical scores").
+ */
+int skb_beam_step(const float *logits, int ld_logits, int lp_in, const skb_beam_state *st,
+                  void *stream);
+
+/*
+ * Beam reorder (model.py:316-330 select_rows): ancestor table
+ * anc[(t+1)&1][r][p] = anc[t&1][parent[r]][p] for p < t and = parent[r] at
+ * p = t.  Also advances *step.  SSRU cells are gathered inside the SSRU GEMM
+ * epilogue via src_row = parent.
+ */
+int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, int *step, void *stream);
+
+/*
+ * Backtrack the best finished hypothesis of every sentence through the
+ * per-step history: tokens_out [B, S_max] (EOS excluded), factors_out
+ * [B, n_factors, S_max] (one entry per step incl. the EOS step).
+ */
+int skb_beam_finalize(const skb_beam_state *st, int best_t_from_steps, int *tokens_out,
+                      int *factors_out, void *stream);
+
+/* out[r] = max over positions l < len[b] of enc[b, l, :] (model.py:496-500). */
+int skb_masked_maxpool(int B, int L, int d, const float *enc, const int *lengths, float *out,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKIFF_B200_H */

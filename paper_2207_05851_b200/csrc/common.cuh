@@ -1,0 +1,66 @@
+// Shared helpers for the sm_100a kernels of the translation hot path.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/skiff_b200.h"
+
+namespace skb {
+
+// ------------------------------------------------------------- error state
+void set_error(const char *fmt, ...);
+int fail(int code, const char *fmt, ...);
+
+#define SKB_CHECK_LAUNCH(what)                                                        \
+  do {                                                                                \
+    cudaError_t _e = cudaGetLastError();                                              \
+    if (_e != cudaSuccess)                                                            \
+      return ::skb::fail(SKB_ERR_LAUNCH, "%s: %s", what, cudaGetErrorString(_e));     \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------- element access
+__device__ __forceinline__ float load_f(const void *p, int dtype, size_t i) {
+  return dtype == SKB_F32 ? reinterpret_cast<const float *>(p)[i]
+                          : __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i]);
+}
+__device__ __forceinline__ void store_f(void *p, int dtype, size_t i, float v) {
+  if (dtype == SKB_F32)
+    reinterpret_cast<float *>(p)[i] = v;
+  else
+    reinterpret_cast<__nv_bfloat16 *>(p)[i] = __float2bfloat16_rn(v);
+}
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Logistic split on sign so exp never overflows (kernels.py:253-260).
+__device__ __forceinline__ float sigmoid_ref(float x) {
+  if (x >= 0.f) return 1.0f / (1.0f + expf(-x));
+  float e = expf(x);
+  return e / (1.0f + e);
+}
+
+}  // namespace skb

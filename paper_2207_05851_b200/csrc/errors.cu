@@ -1,0 +1,26 @@
+// Thread-local error message + status plumbing for the C ABI.
+#include "common.cuh"
+
+namespace skb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+}  // namespace skb
+
+extern "C" const char *skb_version(void) { return "skiff_b200 0.1 sm_100a"; }
+extern "C" const char *skb_last_error(void) { return skb::g_err; }

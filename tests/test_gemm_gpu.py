@@ -1,0 +1,120 @@
+"""GEMM kernels (tcgen05 bf16 and SIMT fp32) vs a torch fp32/fp64 reference
+of the same op (kernels.py:167-195, 479-484), all epilogues."""
+
+import ctypes as C
+
+import pytest
+import torch
+
+from paper_2207_05851_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(3, 48, 16), (5, 40, 32), (130, 64, 4096), (77, 8000, 256), (640, 1024, 1024),
+          (200, 3072, 1024), (640, 32000, 1024), (1, 4096, 1024), (257, 1000, 512)]
+
+
+def _epi(kind, out, ldo, out_dtype, bias=None, c_prev=None, c_next=None, src_row=None,
+         ld_state=0):
+    return N.Epilogue(kind, N.ptr(bias), N.ptr(out), ldo, out_dtype, N.ptr(c_prev),
+                      N.ptr(c_next), N.ptr(src_row), ld_state)
+
+
+def _run(fn, dt, A, W, epi):
+    M, K = A.shape
+    Nn = W.shape[0]
+    N.call(fn, dt, M, Nn, K, A.data_ptr(), A.stride(0), W.data_ptr(), W.stride(0),
+           C.byref(epi), torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("M,Nn,K", SHAPES)
+def test_tc_bf16_store_f32(M, Nn, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    out = torch.full((M, Nn), float("nan"), device="cuda")
+    _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_STORE, out, Nn, N.F32, bias))
+    ref = A.double() @ W.double().T + bias.double()
+    torch.cuda.synchronize()
+    err = (out.double() - ref).abs().max().item()
+    assert err <= 2e-3 * (K ** 0.5), err
+
+
+@pytest.mark.parametrize("M,Nn,K", [(5, 40, 32), (640, 4096, 1024), (300, 1024, 4096)])
+def test_tc_relu_bf16_out_and_resid(M, Nn, K):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    out = torch.zeros((M, Nn), device="cuda", dtype=torch.bfloat16)
+    _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_RELU, out, Nn, N.BF16, bias))
+    ref = torch.relu(A.float() @ W.float().T + bias)
+    torch.cuda.synchronize()
+    assert torch.allclose(out.float(), ref, rtol=1e-2, atol=0.05 * K ** 0.5 / 10)
+    x = torch.randn(M, Nn, device="cuda", generator=g)
+    x0 = x.clone()
+    _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_RESID, x, Nn, N.F32, bias))
+    torch.cuda.synchronize()
+    ref = x0.double() + (A.double() @ W.double().T + bias.double())
+    assert (x.double() - ref).abs().max().item() <= 2e-3 * K ** 0.5
+
+
+@pytest.mark.parametrize("fn", ["skb_gemm", "skb_gemm_simt"])
+@pytest.mark.parametrize("M,d", [(7, 32), (640, 1024)])
+def test_ssru_epilogue(fn, M, d):
+    g = torch.Generator(device="cuda").manual_seed(11)
+    h = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    wf = torch.randn(d, d, device="cuda", generator=g).bfloat16() * 0.05
+    w = torch.randn(d, d, device="cuda", generator=g).bfloat16() * 0.05
+    bf = torch.randn(d, device="cuda", generator=g)
+    Wi = torch.stack([wf, w], 1).reshape(2 * d, d).contiguous()     # rows (f_j, w_j)
+    bi = torch.stack([bf, torch.zeros_like(bf)], 1).reshape(2 * d).contiguous()
+    c_prev = torch.randn(M, d, device="cuda", generator=g)
+    src = torch.randint(0, M, (M,), device="cuda", generator=g, dtype=torch.int32)
+    c_next = torch.zeros(M, d, device="cuda")
+    x = torch.randn(M, d, device="cuda", generator=g)
+    x0 = x.clone()
+    _run(fn, N.BF16, h, Wi, _epi(N.EPI_SSRU, x, d, N.F32, bi, c_prev, c_next, src, d))
+    f = torch.sigmoid(h.double() @ wf.double().T + bf.double())
+    c = f * c_prev.double()[src.long()] + (1 - f) * (h.double() @ w.double().T)
+    torch.cuda.synchronize()
+    assert (c_next.double() - c).abs().max().item() < 1e-3
+    assert (x.double() - (x0.double() + torch.relu(c))).abs().max().item() < 1e-3
+
+
+@pytest.mark.parametrize("M,Nn,K", [(3, 48, 16), (130, 200, 300), (640, 1024, 1024)])
+def test_simt_fp32(M, Nn, K):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    W = torch.randn(Nn, K, device="cuda", generator=g)
+    out = torch.zeros(M, Nn, device="cuda")
+    _run("skb_gemm", N.F32, A, W, _epi(N.EPI_STORE, out, Nn, N.F32))
+    ref = A.double() @ W.double().T
+    torch.cuda.synchronize()
+    assert (out.double() - ref).abs().max().item() < 1e-5 * K
+
+
+def test_tc_matches_simt_bf16():
+    g = torch.Generator(device="cuda").manual_seed(9)
+    A = torch.randn(300, 1024, device="cuda", generator=g).bfloat16()
+    W = torch.randn(2000, 1024, device="cuda", generator=g).bfloat16()
+    o1 = torch.zeros(300, 2000, device="cuda")
+    o2 = torch.zeros(300, 2000, device="cuda")
+    _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_STORE, o1, 2000, N.F32))
+    _run("skb_gemm_simt", N.BF16, A, W, _epi(N.EPI_STORE, o2, 2000, N.F32))
+    torch.cuda.synchronize()
+    assert (o1 - o2).abs().max().item() < 5e-3
+
+
+def test_batch_invariance():
+    """A row's result must not depend on the other rows (test_search.py:400-405)."""
+    g = torch.Generator(device="cuda").manual_seed(2)
+    A = torch.randn(640, 1024, device="cuda", generator=g).bfloat16()
+    W = torch.randn(4096, 1024, device="cuda", generator=g).bfloat16()
+    full = torch.zeros(640, 4096, device="cuda")
+    part = torch.zeros(5, 4096, device="cuda")
+    _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_STORE, full, 4096, N.F32))
+    _run("skb_gemm", N.BF16, A[130:135], W, _epi(N.EPI_STORE, part, 4096, N.F32))
+    torch.cuda.synchronize()
+    assert torch.equal(full[130:135], part)
