@@ -57,6 +57,11 @@ typedef struct skb_epilogue {
   float *c_next;
   const int *src_row;    /* NULL => identity                                   */
   int ld_state;
+  /* Decode-loop mode (CUDA-graph friendly): if step != NULL, c_next is a    */
+  /* [2, state_rows, ld_state] double buffer; step t writes half (t&1) and  */
+  /* reads half ((t+1)&1) (zeros at t = 0); c_prev is ignored.              */
+  const int *step;
+  long long state_stride; /* elements between the two halves                 */
 } skb_epilogue;
 
 /* Library identity / diagnostics */
@@ -155,7 +160,8 @@ typedef struct skb_beam_state {
   int B, K, U;            /* sentences, beam, columns of the logits          */
   int S_max;              /* history capacity (steps)                        */
   int n_factors;          /* target factor streams                           */
-  double alpha;           /* length penalty exponent (search.py:74-75)       */
+  const double *len_pen;  /* [S_max+1] steps**alpha, computed on the host so */
+                          /* it is bit-identical to search.py:74-75          */
   const int *step;        /* device: current step t                          */
   const int *col_token;   /* [U] token id of column (NULL: identity)         */
   const unsigned *mask;   /* [B, ceil(U/32)] active-column bits (NULL: all)  */
@@ -167,17 +173,16 @@ typedef struct skb_beam_state {
   const int *prefix_fac;  /* [B, n_factors, P] prefix factor ids or -1        */
   int *n_alive;           /* [B] alive rows (starts at 1)                     */
   int *done;              /* [B] sentence finished flag                       */
-  double *score;          /* [R] alive hypothesis log-prob (float64)         */
-  double *score_next;     /* [R]                                              */
+  double *score;          /* [R] alive hypothesis log-prob (float64), in place*/
   int *tok_next;          /* [R] token fed at the next step                   */
   int *ftok_next;         /* [n_factors, R] factor ids fed next step          */
   int *parent;            /* [R] parent slot of each new row                   */
   int *tok_hist;          /* [S_max, R] token appended at step t              */
   int *par_hist;          /* [S_max, R] parent beam index at step t           */
   int *fac_hist;          /* [S_max, n_factors, R] factor of the new row       */
-  const float *fac_logits;/* [n_factors] x [R, fac_ld] concatenated, or NULL  */
+  const float *fac_logits;/* [R, fac_ld] all factor heads side by side, or NULL*/
   int fac_ld;             /* row stride of fac_logits                          */
-  const int *fac_off;     /* [n_factors+1] column offsets into fac_logits     */
+  const int *fac_off;     /* [n_factors+1] column offsets (device)            */
   /* scratch */
   double *cand_score;     /* [R, K] */
   float *cand_lp;         /* [R, K] */
@@ -191,7 +196,7 @@ typedef struct skb_beam_state {
   double *best_logprob;   /* [B] */
   int *best_steps;        /* [B] 0 = none yet */
   int *best_forced;       /* [B] */
-  int *best_parent;       /* [B] beam index of the parent row at best_t */
+  int *best_parent;       /* [B] beam index of the parent row at step steps-1 */
   int *best_fac;          /* [B, n_factors] factor entry of the EOS step */
   int *n_done;            /* [1] sentences finished (for host polling)      */
 } skb_beam_state;
@@ -220,12 +225,25 @@ int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, int *step, v
  * per-step history: tokens_out [B, S_max] (EOS excluded), factors_out
  * [B, n_factors, S_max] (one entry per step incl. the EOS step).
  */
-int skb_beam_finalize(const skb_beam_state *st, int best_t_from_steps, int *tokens_out,
-                      int *factors_out, void *stream);
+int skb_beam_finalize(const skb_beam_state *st, int *tokens_out, int *factors_out,
+                      void *stream);
 
 /* out[r] = max over positions l < len[b] of enc[b, l, :] (model.py:496-500). */
 int skb_masked_maxpool(int B, int L, int d, const float *enc, const int *lengths, float *out,
                        void *stream);
+
+/* Element-wise dtype conversion (fp32 <-> bf16) of n elements. */
+int skb_convert(long long n, const void *src, int src_dtype, void *dst, int dst_dtype,
+                void *stream);
+
+/* NVS vocabulary selection bits (model.py:511-517): bit c of row b is set iff
+ * sigmoid(logits[b, c]) > threshold.  mask: [B, ceil(V/32)]. */
+int skb_nvs_mask(int B, int V, const float *logits, int ld, float threshold, unsigned *mask,
+                 void *stream);
+
+/* Select the CUDA device used by this library's calls on the current thread
+ * (one process per GPU; mirrors torch.cuda.set_device). */
+int skb_set_device(int device);
 
 #ifdef __cplusplus
 }

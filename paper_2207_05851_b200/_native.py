@@ -24,15 +24,16 @@ i32 = C.c_int
 
 class Epilogue(C.Structure):
     _fields_ = [("kind", i32), ("bias", vp), ("out", vp), ("ldo", i32), ("out_dtype", i32),
-                ("c_prev", vp), ("c_next", vp), ("src_row", vp), ("ld_state", i32)]
+                ("c_prev", vp), ("c_next", vp), ("src_row", vp), ("ld_state", i32),
+                ("step", vp), ("state_stride", C.c_longlong)]
 
 
 class BeamState(C.Structure):
     _fields_ = [("B", i32), ("K", i32), ("U", i32), ("S_max", i32), ("n_factors", i32),
-                ("alpha", C.c_double), ("step", vp), ("col_token", vp), ("mask", vp),
+                ("len_pen", vp), ("step", vp), ("col_token", vp), ("mask", vp),
                 ("eos_col", i32), ("max_len", vp), ("prefix_len", vp), ("prefix_col", vp),
                 ("P", i32), ("prefix_fac", vp), ("n_alive", vp), ("done", vp), ("score", vp),
-                ("score_next", vp), ("tok_next", vp), ("ftok_next", vp), ("parent", vp),
+                ("tok_next", vp), ("ftok_next", vp), ("parent", vp),
                 ("tok_hist", vp), ("par_hist", vp), ("fac_hist", vp), ("fac_logits", vp),
                 ("fac_ld", i32), ("fac_off", vp), ("cand_score", vp), ("cand_lp", vp),
                 ("cand_col", vp), ("cand_cnt", vp), ("row_argmax", vp), ("fac_choice", vp),
@@ -58,8 +59,11 @@ SIGNATURES = {
     "skb_gather_rows": [i32, i32, vp, i32, vp, vp, i32, i32, vp],
     "skb_beam_step": [vp, i32, i32, C.POINTER(BeamState), vp],
     "skb_beam_reorder": [i32, i32, vp, vp, vp, vp],
-    "skb_beam_finalize": [C.POINTER(BeamState), i32, vp, vp, vp],
+    "skb_beam_finalize": [C.POINTER(BeamState), vp, vp, vp],
     "skb_masked_maxpool": [i32, i32, i32, vp, vp, vp, vp],
+    "skb_convert": [C.c_longlong, vp, i32, vp, i32, vp],
+    "skb_nvs_mask": [i32, i32, vp, i32, C.c_float, vp, vp],
+    "skb_set_device": [i32],
 }
 
 _lib = None
@@ -75,7 +79,10 @@ def lib():
                 "(there is no CPU fallback)")
         L = C.CDLL(str(LIB_PATH))
         for name, args in SIGNATURES.items():
-            fn = getattr(L, name)
+            try:
+                fn = getattr(L, name)
+            except AttributeError:
+                continue  # reported as missing by tests/test_native_lib.py
             fn.argtypes = args
             fn.restype = C.c_char_p if name in ("skb_version", "skb_last_error") else C.c_int
         _lib = L

@@ -30,6 +30,8 @@ struct EpiArgs {
   float *c_next;
   const int *src_row;
   int ld_state;
+  const int *step;
+  long long state_stride;
 };
 
 // Apply the epilogue to `cnt` consecutive accumulator columns n..n+cnt-1 of
@@ -41,16 +43,22 @@ __device__ __forceinline__ void epilogue_run(const EpiArgs &e, int m, int n, int
     // f = sigmoid(W_f h + b_f); c = f*c_prev + (1-f)*(W h); x += relu(c)
     float *x = reinterpret_cast<float *>(e.out);
     const int srow = e.src_row ? e.src_row[m] : m;
+    const float *cprev = e.c_prev;
+    float *cnext = e.c_next;
+    if (e.step) {  // decode-loop double buffer selected by step parity
+      const int t = *e.step;
+      cnext = e.c_next + (t & 1) * e.state_stride;
+      cprev = t == 0 ? nullptr : e.c_next + ((t + 1) & 1) * e.state_stride;
+    }
     for (int q = 0; q + 1 < cnt; q += 2) {
       const int nn = n + q;
-      if (nn + 1 >= N + 1) break;
       if (nn >= N) break;
       const int j = nn >> 1;
       float fpre = v[q] + (e.bias ? e.bias[nn] : 0.f);
       float f = sigmoid_ref(fpre);
-      float cp = e.c_prev ? e.c_prev[(size_t)srow * e.ld_state + j] : 0.f;
+      float cp = cprev ? cprev[(size_t)srow * e.ld_state + j] : 0.f;
       float c = f * cp + (1.0f - f) * v[q + 1];
-      e.c_next[(size_t)m * e.ld_state + j] = c;
+      cnext[(size_t)m * e.ld_state + j] = c;
       float *xp = x + (size_t)m * e.ldo + j;
       *xp = *xp + fmaxf(c, 0.f);
     }
@@ -477,6 +485,8 @@ static EpiArgs to_args(const skb_epilogue *e) {
   a.c_next = e->c_next;
   a.src_row = e->src_row;
   a.ld_state = e->ld_state;
+  a.step = e->step;
+  a.state_stride = e->state_stride;
   return a;
 }
 

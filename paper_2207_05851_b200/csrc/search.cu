@@ -1,0 +1,440 @@
+// Beam search bookkeeping on the device (skiff search.py:275-394).
+//
+// skb_beam_step: one CTA per row slot r = b*K + i.  Pass 1/2 compute the
+// masked row max and sum of exp (log_softmax over the sentence's active
+// columns, kernels.py:287-295); pass 3 computes lp = (x - max) - log(sum)
+// per column, the first-max column (np.argmax) and a per-thread top-K of the
+// float64 candidate scores s_r + lp (search.py:353-358), merged across the
+// CTA with warp shuffles.  The last CTA of a sentence to arrive (atomic
+// counter) merges the <= K row lists in the exact order (score desc, token
+// asc, parent asc) of np.lexsort (search.py:363), routes EOS candidates to
+// the finished set, compacts survivors into new rows and records history
+// for the final backtrack.  Forced steps (target prefix, final EOS) use the
+// float32 candidate keys the reference builds there (python float +
+// np.float32 -> float32 under NEP 50, search.py:353-355).
+
+#include "common.cuh"
+
+#include <cfloat>
+
+namespace skb {
+
+constexpr int BEAM_THREADS = 256;
+constexpr int EOS = 3, PAD = 0;
+
+struct Cand {
+  double key;
+  float lp;
+  int col;
+};
+
+__device__ __forceinline__ bool better(double k1, int c1, double k2, int c2) {
+  return k1 > k2 || (k1 == k2 && c1 < c2);
+}
+
+__device__ __forceinline__ bool col_active(const unsigned *mask, int c) {
+  return mask == nullptr || ((mask[c >> 5] >> (c & 31)) & 1u);
+}
+
+template <int MAXK>
+__device__ __forceinline__ void list_insert(double (&k)[MAXK], float (&l)[MAXK], int (&c)[MAXK],
+                                            double key, float lp, int col) {
+  // caller guarantees better(key, col, k[MAXK-1], c[MAXK-1])
+  k[MAXK - 1] = key;
+  l[MAXK - 1] = lp;
+  c[MAXK - 1] = col;
+#pragma unroll
+  for (int j = MAXK - 1; j > 0; --j) {
+    if (better(k[j], c[j], k[j - 1], c[j - 1])) {
+      double tk = k[j]; k[j] = k[j - 1]; k[j - 1] = tk;
+      float tl = l[j]; l[j] = l[j - 1]; l[j - 1] = tl;
+      int tc = c[j]; c[j] = c[j - 1]; c[j - 1] = tc;
+    }
+  }
+}
+
+template <int MAXK>
+__global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restrict__ logits,
+                                                            int ld, int lp_in, skb_beam_state st) {
+  const int r = blockIdx.x;
+  const int K = st.K, U = st.U;
+  const int b = r / K, i = r % K;
+  const int R = st.B * K;
+  const int t = *st.step;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = BEAM_THREADS / 32;
+
+  __shared__ float red_f[NW];
+  __shared__ int red_i[NW];
+  __shared__ double wk[NW][MAXK];
+  __shared__ float wl[NW][MAXK];
+  __shared__ int wc[NW][MAXK];
+  __shared__ int is_last;
+
+  const bool live = !st.done[b] && i < st.n_alive[b];
+  if (live) {
+    const float *row = logits + (size_t)r * ld;
+    const unsigned *mask = st.mask ? st.mask + (size_t)b * ((U + 31) >> 5) : nullptr;
+    // ---- pass 1: max over active columns
+    float mx = -INFINITY, lse = 0.f;
+    if (!lp_in) {
+      for (int c = tid; c < U; c += BEAM_THREADS)
+        if (col_active(mask, c)) mx = fmaxf(mx, row[c]);
+      mx = warp_max(mx);
+      if (lane == 0) red_f[warp] = mx;
+      __syncthreads();
+      mx = red_f[0];
+      for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red_f[w]);
+      __syncthreads();
+      // ---- pass 2: sum of exp(x - max)
+      float s = 0.f;
+      for (int c = tid; c < U; c += BEAM_THREADS)
+        if (col_active(mask, c)) s += expf(row[c] - mx);
+      s = warp_sum(s);
+      if (lane == 0) red_f[warp] = s;
+      __syncthreads();
+      s = 0.f;
+      for (int w = 0; w < NW; ++w) s += red_f[w];
+      __syncthreads();
+      lse = logf(s);
+    }
+    const int plen = st.prefix_len[b];
+    const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
+    const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
+    const double s_r = st.score[r];
+
+    // ---- pass 3: first-max column of lp and per-thread top-K of scores
+    double tk[MAXK];
+    float tl[MAXK];
+    int tc[MAXK];
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) {
+      tk[j] = -DBL_MAX;
+      tl[j] = 0.f;
+      tc[j] = INT_MAX;
+    }
+    float amax = -INFINITY;
+    int acol = INT_MAX;
+    const bool need_argmax = final_force;
+    if (fcol < 0 || need_argmax) {
+      for (int c = tid; c < U; c += BEAM_THREADS) {
+        if (!col_active(mask, c)) continue;
+        const float x = row[c];
+        const float lp = lp_in ? x : (x - mx) - lse;
+        if (lp > amax) {
+          amax = lp;
+          acol = c;
+        }
+        if (fcol < 0) {
+          const double key = s_r + (double)lp;
+          if (key > tk[MAXK - 1]) list_insert<MAXK>(tk, tl, tc, key, lp, c);
+        }
+      }
+    }
+    // first max of lp across the CTA (ties -> lowest column)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float oa = __shfl_xor_sync(0xffffffffu, amax, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, acol, o);
+      if (oa > amax || (oa == amax && oc < acol)) {
+        amax = oa;
+        acol = oc;
+      }
+    }
+    if (lane == 0) {
+      red_f[warp] = amax;
+      red_i[warp] = acol;
+    }
+    // warp-level merge of the 32 thread lists -> top MAXK per warp
+    if (fcol < 0) {
+      int head = 0;
+      for (int j = 0; j < MAXK; ++j) {
+        double hk = head < MAXK ? tk[0] : -DBL_MAX;
+        int hc = head < MAXK ? tc[0] : INT_MAX;
+        double bk = hk;
+        int bc = hc, bl = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+          if (better(ok, oc, bk, bc) || (ok == bk && oc == bc && ol < bl)) {
+            bk = ok;
+            bc = oc;
+            bl = ol;
+          }
+        }
+        const float blp = __shfl_sync(0xffffffffu, tl[0], bl);
+        if (lane == 0) {
+          wk[warp][j] = bk;
+          wl[warp][j] = blp;
+          wc[warp][j] = bc;
+        }
+        if (lane == bl) {  // pop the head of the winning lane's list
+#pragma unroll
+          for (int q = 0; q + 1 < MAXK; ++q) {
+            tk[q] = tk[q + 1];
+            tl[q] = tl[q + 1];
+            tc[q] = tc[q + 1];
+          }
+          tk[MAXK - 1] = -DBL_MAX;
+          tc[MAXK - 1] = INT_MAX;
+          ++head;
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // CTA-level first max
+      float a = lane < NW ? red_f[lane] : -INFINITY;
+      int ac = lane < NW ? red_i[lane] : INT_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float oa = __shfl_xor_sync(0xffffffffu, a, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, ac, o);
+        if (oa > a || (oa == a && oc < ac)) {
+          a = oa;
+          ac = oc;
+        }
+      }
+      if (lane == 0) st.row_argmax[r] = ac;
+      if (fcol >= 0) {
+        if (lane == 0) {
+          const float x = row[fcol];
+          const float lp = lp_in ? x : (x - mx) - lse;
+          // forced steps: float32 key fl32(fl32(s) + lp) (NEP 50 promotion)
+          const float key32 = (float)s_r + lp;
+          st.cand_score[(size_t)r * K] = (double)key32;
+          st.cand_lp[(size_t)r * K] = lp;
+          st.cand_col[(size_t)r * K] = fcol;
+          st.cand_cnt[r] = 1;
+        }
+      } else {
+        // merge NW warp lists (each sorted) -> top K
+        int head = 0;  // lane w (< NW) walks warp w's list
+        const int kk = K < MAXK ? K : MAXK;
+        for (int j = 0; j < kk; ++j) {
+          const bool has = lane < NW && head < MAXK;
+          double bk = has ? wk[lane][head] : -DBL_MAX;
+          int bc = has ? wc[lane][head] : INT_MAX;
+          const float my_lp = has ? wl[lane][head] : 0.f;
+          int bl = lane;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+            if (better(ok, oc, bk, bc) || (ok == bk && oc == bc && ol < bl)) {
+              bk = ok;
+              bc = oc;
+              bl = ol;
+            }
+          }
+          const float blp = __shfl_sync(0xffffffffu, my_lp, bl);
+          if (lane == 0) {
+            st.cand_score[(size_t)r * K + j] = bk;
+            st.cand_col[(size_t)r * K + j] = bc;
+            st.cand_lp[(size_t)r * K + j] = blp;
+          }
+          if (lane == bl) ++head;
+        }
+        if (lane == 0) {
+          int cnt = 0;
+          for (int j = 0; j < kk; ++j) cnt += st.cand_col[(size_t)r * K + j] != INT_MAX;
+          st.cand_cnt[r] = cnt;
+        }
+      }
+      // factor choices of this row (search.py:261-272)
+      if (lane == 0) {
+        for (int k = 0; k < st.n_factors; ++k) {
+          int choice = -1;
+          if (t >= 1 && st.prefix_fac) {
+            const int pf = t - 1 < st.P ? st.prefix_fac[((size_t)b * st.n_factors + k) * st.P + t - 1] : -1;
+            choice = pf;
+          }
+          if (choice < 0) {
+            const float *fr = st.fac_logits + (size_t)r * st.fac_ld;
+            const int lo = st.fac_off[k], hi = st.fac_off[k + 1];
+            float bm = -INFINITY;
+            int bcol = 0;
+            for (int c = lo; c < hi; ++c)
+              if (fr[c] > bm) {
+                bm = fr[c];
+                bcol = c - lo;
+              }
+            choice = bcol;
+          }
+          st.fac_choice[(size_t)r * st.n_factors + k] = choice;
+        }
+      }
+    }
+  } else if (tid == 0) {
+    st.cand_cnt[r] = 0;
+  }
+
+  // ---- arrival: the last row CTA of the sentence does the merge
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st.counter[b], 1u);
+    is_last = prev == (unsigned)(K - 1);
+  }
+  __syncthreads();
+  if (!is_last || tid != 0) return;
+  __threadfence();
+  st.counter[b] = 0;
+  if (st.done[b]) return;
+
+  const int base = b * K;
+  const int nalive = st.n_alive[b];
+  const int nf = st.n_factors;
+  const int plen = st.prefix_len[b];
+  const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
+  double s_par[32];
+  int head[32];
+  for (int q = 0; q < nalive; ++q) {
+    s_par[q] = st.score[base + q];
+    head[q] = 0;
+  }
+  int n_new = 0;
+  // parent factor choices must be read before rows are overwritten (they are
+  // per parent row and not modified here), so no copy is needed.
+  for (int sel = 0; sel < K; ++sel) {
+    int bq = -1;
+    double bk = 0.0;
+    int bc = 0;
+    for (int q = 0; q < nalive; ++q) {
+      const int rr = base + q;
+      if (head[q] >= st.cand_cnt[rr]) continue;
+      const double k = st.cand_score[(size_t)rr * K + head[q]];
+      const int c = st.cand_col[(size_t)rr * K + head[q]];
+      // order (key desc, token asc, parent asc); columns are sorted by token
+      if (bq < 0 || k > bk || (k == bk && c < bc)) {
+        bq = q;
+        bk = k;
+        bc = c;
+      }
+    }
+    if (bq < 0) break;
+    const int rr = base + bq;
+    const float lp = st.cand_lp[(size_t)rr * K + head[bq]];
+    head[bq]++;
+    const double score = s_par[bq] + (double)lp;
+    const int token = st.col_token ? st.col_token[bc] : bc;
+    if (token == EOS) {
+      const int steps = t + 1;
+      const double norm = score / st.len_pen[steps];
+      if (st.best_steps[b] == 0 || norm > st.best_norm[b]) {
+        st.best_norm[b] = norm;
+        st.best_logprob[b] = score;
+        st.best_steps[b] = steps;
+        st.best_forced[b] = final_force && st.row_argmax[rr] != bc;
+        st.best_parent[b] = bq;
+        for (int k = 0; k < nf; ++k)
+          st.best_fac[(size_t)b * nf + k] = st.fac_choice[(size_t)rr * nf + k];
+      }
+    } else {
+      const int slot = base + n_new;
+      st.tok_next[slot] = token;
+      st.parent[slot] = rr;
+      st.score[slot] = score;
+      st.tok_hist[(size_t)t * R + slot] = token;
+      st.par_hist[(size_t)t * R + slot] = bq;
+      for (int k = 0; k < nf; ++k) {
+        const int f = st.fac_choice[(size_t)rr * nf + k];
+        st.ftok_next[(size_t)k * R + slot] = f;
+        st.fac_hist[((size_t)t * nf + k) * R + slot] = f;
+      }
+      ++n_new;
+    }
+  }
+  for (int q = n_new; q < K; ++q) {
+    st.tok_next[base + q] = PAD;
+    st.parent[base + q] = base;
+    for (int k = 0; k < nf; ++k) st.ftok_next[(size_t)k * R + base + q] = PAD;
+  }
+  st.n_alive[b] = n_new;
+  if (n_new == 0) {
+    st.done[b] = 1;
+    atomicAdd(st.n_done, 1);
+  }
+}
+
+// ------------------------------------------------------------- reorder
+__global__ void k_beam_reorder(int R, int S_max, int *anc, const int *parent, const int *step) {
+  const int r = blockIdx.y;
+  const int t = *step;
+  const int p = parent[r];
+  const int *src = anc + ((size_t)(t & 1) * R + p) * S_max;
+  int *dst = anc + ((size_t)((t + 1) & 1) * R + r) * S_max;
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos <= t && pos < S_max;
+       pos += gridDim.x * blockDim.x)
+    dst[pos] = pos == t ? p : src[pos];
+}
+
+__global__ void k_step_advance(int *step) { *step += 1; }
+
+// ------------------------------------------------------------ finalize
+__global__ void k_beam_finalize(skb_beam_state st, int *tokens_out, int *factors_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= st.B) return;
+  const int K = st.K, R = st.B * K, nf = st.n_factors;
+  const int steps = st.best_steps[b];
+  if (steps <= 0) return;
+  const int tfin = steps - 1;
+  int q = st.best_parent[b];
+  for (int k = 0; k < nf; ++k)
+    factors_out[((size_t)b * nf + k) * st.S_max + tfin] = st.best_fac[(size_t)b * nf + k];
+  for (int pos = tfin - 1; pos >= 0; --pos) {
+    const int slot = b * K + q;
+    tokens_out[(size_t)b * st.S_max + pos] = st.tok_hist[(size_t)pos * R + slot];
+    for (int k = 0; k < nf; ++k)
+      factors_out[((size_t)b * nf + k) * st.S_max + pos] = st.fac_hist[((size_t)pos * nf + k) * R + slot];
+    q = st.par_hist[(size_t)pos * R + slot];
+  }
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, const skb_beam_state *st,
+                             void *stream) {
+  if (!st || st->B <= 0 || st->K <= 0 || st->U <= 0)
+    return fail(SKB_ERR_SHAPE, "beam_step: bad state");
+  if (st->K > 32) return fail(SKB_ERR_CONFIG, "beam size %d exceeds 32", st->K);
+  const int R = st->B * st->K;
+  cudaStream_t s = as_stream(stream);
+  if (st->K <= 1)
+    k_beam_step<1><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  else if (st->K <= 4)
+    k_beam_step<4><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  else if (st->K <= 8)
+    k_beam_step<8><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  else if (st->K <= 16)
+    k_beam_step<16><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  else
+    k_beam_step<32><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  SKB_CHECK_LAUNCH("k_beam_step");
+  return SKB_OK;
+}
+
+extern "C" int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, int *step,
+                                void *stream) {
+  if (R <= 0 || S_max <= 0) return fail(SKB_ERR_SHAPE, "beam_reorder: bad shape");
+  cudaStream_t s = as_stream(stream);
+  dim3 grid((S_max + 127) / 128, R);
+  k_beam_reorder<<<grid, 128, 0, s>>>(R, S_max, anc, parent, step);
+  SKB_CHECK_LAUNCH("k_beam_reorder");
+  k_step_advance<<<1, 1, 0, s>>>(step);
+  SKB_CHECK_LAUNCH("k_step_advance");
+  return SKB_OK;
+}
+
+extern "C" int skb_beam_finalize(const skb_beam_state *st, int *tokens_out, int *factors_out,
+                                 void *stream) {
+  if (!st || st->B <= 0) return fail(SKB_ERR_SHAPE, "beam_finalize: bad state");
+  k_beam_finalize<<<(st->B + 127) / 128, 128, 0, as_stream(stream)>>>(*st, tokens_out, factors_out);
+  SKB_CHECK_LAUNCH("k_beam_finalize");
+  return SKB_OK;
+}

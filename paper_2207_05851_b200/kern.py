@@ -1,0 +1,139 @@
+"""Thin torch-tensor wrappers over the C ABI (include/skiff_b200.h).
+
+Every function launches hand-written sm_100a kernels on the current torch
+stream and counts them in `launches` (the bench reports it as gpu_launches).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+
+launches = 0
+
+
+def _count(n: int = 1) -> None:
+    global launches
+    launches += n
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dcode(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return N.F32
+    if t.dtype == torch.bfloat16:
+        return N.BF16
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_row=None,
+         step=None, state_stride=0, simt=False):
+    """out (or residual x) <- epilogue(A[M,K] . W[N,K]^T)."""
+    M = A.shape[0] if M is None else M
+    Nn, K = W.shape
+    epi = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), out.stride(0), dcode(out), None,
+                     N.ptr(c_state), N.ptr(src_row), Nn // 2 if kind == N.EPI_SSRU else 0,
+                     N.ptr(step), state_stride)
+    N.call("skb_gemm_simt" if simt else "skb_gemm", dcode(A), M, Nn, K, A.data_ptr(),
+           A.stride(0), W.data_ptr(), W.stride(0), C.byref(epi), stream())
+    _count()
+
+
+def layernorm(x, gain, bias, out, rows=None, eps=1e-5):
+    rows = x.shape[0] if rows is None else rows
+    N.call("skb_layernorm", rows, x.shape[1], x.data_ptr(), x.stride(0), gain.data_ptr(),
+           bias.data_ptr(), C.c_float(eps), out.data_ptr(), out.stride(0), dcode(out), stream())
+    _count()
+
+
+def embed_target(tok, E, pe, step, ftok, ftables, x, rows=None):
+    rows = tok.shape[0] if rows is None else rows
+    nf = 0 if ftables is None else ftables.shape[0]
+    N.call("skb_embed_target", rows, E.shape[1], tok.data_ptr(), E.data_ptr(), pe.data_ptr(),
+           step.data_ptr(), nf, N.ptr(ftok) if nf else None, N.ptr(ftables) if nf else None,
+           x.data_ptr(), stream())
+    _count()
+
+
+def embed_source(ids, E, pe, fdims, fcombine, fids, ftables, x, B, L, d):
+    nf = len(fdims)
+    dims = (C.c_int * max(nf, 1))(*fdims)
+    comb = (C.c_int * max(nf, 1))(*fcombine)
+    N.call("skb_embed_source", B, L, d, E.shape[1], ids.data_ptr(), E.data_ptr(), pe.data_ptr(),
+           nf, dims, comb, N.ptr(fids) if nf else None, N.ptr(ftables) if nf else None,
+           x.data_ptr(), stream())
+    _count()
+
+
+def encoder_attention(qkv, lengths, ctx, B, L, H, dh):
+    N.call("skb_encoder_attention", B, L, H, dh, qkv.data_ptr(), qkv.stride(0), dcode(qkv),
+           lengths.data_ptr(), ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+    _count()
+
+
+def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max):
+    N.call("skb_self_attention_step", R, H, dh, qkv.data_ptr(), qkv.stride(0), dcode(qkv),
+           kc.data_ptr(), vc.data_ptr(), dcode(kc), S_max, anc.data_ptr(), step.data_ptr(),
+           ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+    _count()
+
+
+def cross_attention_step(q, kv, koff, voff, L, row_sent, lengths, ctx, R, H, dh):
+    N.call("skb_cross_attention_step", R, H, dh, q.data_ptr(), q.stride(0), dcode(q),
+           kv.data_ptr(), kv.stride(0), dcode(kv), koff, voff, L, row_sent.data_ptr(),
+           lengths.data_ptr(), ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+    _count()
+
+
+def gather_rows(table, idx, out):
+    n = idx.shape[0]
+    if table.dtype == torch.int32:
+        code = N.F32  # 4-byte rows; the kernel moves bytes
+    else:
+        code = dcode(table)
+    N.call("skb_gather_rows", n, table.shape[1], table.data_ptr(), table.stride(0),
+           idx.data_ptr(), out.data_ptr(), out.stride(0), code, stream())
+    _count()
+
+
+def convert(src, dst):
+    N.call("skb_convert", src.numel(), src.data_ptr(), dcode(src), dst.data_ptr(), dcode(dst),
+           stream())
+    _count()
+
+
+def masked_maxpool(enc, lengths, out, B, L, d):
+    N.call("skb_masked_maxpool", B, L, d, enc.data_ptr(), lengths.data_ptr(), out.data_ptr(),
+           stream())
+    _count()
+
+
+def nvs_mask(logits, threshold, mask):
+    B, V = logits.shape
+    N.call("skb_nvs_mask", B, V, logits.data_ptr(), logits.stride(0), C.c_float(threshold),
+           mask.data_ptr(), stream())
+    _count()
+
+
+def beam_step(logits, state: N.BeamState, lp_in=False):
+    N.call("skb_beam_step", logits.data_ptr(), logits.stride(0), int(lp_in), C.byref(state),
+           stream())
+    _count()
+
+
+def beam_reorder(anc, parent, step, R, S_max):
+    N.call("skb_beam_reorder", R, S_max, anc.data_ptr(), parent.data_ptr(), step.data_ptr(),
+           stream())
+    _count(2)
+
+
+def beam_finalize(state: N.BeamState, tokens_out, factors_out):
+    N.call("skb_beam_finalize", C.byref(state), tokens_out.data_ptr(), factors_out.data_ptr(),
+           stream())
+    _count()

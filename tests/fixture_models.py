@@ -24,3 +24,36 @@ def oracle_vocabs(name: str) -> dict:
         trg_f=[O.OVocab(specials + ["<shift>"] + [f"F{i}_{j}" for j in range(v - 5)])
                for i, v in enumerate(cfg.get("target_factor_specs", []))],
     )
+
+
+def product_config(name: str, **override):
+    from paper_2207_05851_b200.config import ModelConfig, SourceFactorSpec, TargetFactorSpec
+    cfg = dict(CONFIGS[name]["config"])
+    cfg.update(override)
+    cfg["source_factor_specs"] = [SourceFactorSpec(*s) for s in cfg.get("source_factor_specs", [])]
+    cfg["target_factor_specs"] = [TargetFactorSpec(v) for v in cfg.get("target_factor_specs", [])]
+    return ModelConfig(**cfg)
+
+
+_PM = {}
+
+
+def product_model(name: str, precision: str = "fp32", **override):
+    """The product's device Model with the fixture's random-init weights."""
+    from paper_2207_05851_b200.model import Model
+    key = (name, precision, tuple(sorted(override.items())))
+    if key not in _PM:
+        _PM[key] = Model(product_config(name, **override), params=oracle_model(name).p,
+                         precision=precision)
+    return _PM[key]
+
+
+def product_vocabs(name: str):
+    from types import SimpleNamespace
+
+    from paper_2207_05851_b200.checkpoint import Vocabulary
+    ov = oracle_vocabs(name)
+    return SimpleNamespace(src_vocab=Vocabulary(ov["src"].tokens),
+                           trg_vocab=Vocabulary(ov["trg"].tokens),
+                           src_factor_vocabs=[Vocabulary(v.tokens) for v in ov["src_f"]],
+                           trg_factor_vocabs=[Vocabulary(v.tokens) for v in ov["trg_f"]])

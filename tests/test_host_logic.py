@@ -1,0 +1,111 @@
+"""Host-side logic of the drop-in surface (CPU only): input parsing,
+chunking, config/checkpoint/vocab/shortlist I/O, init, cost model —
+checked against the reference's recorded behaviour (tests/golden)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from fixture_models import oracle_model, product_config
+from oracle.fixture_configs import CONFIGS
+
+
+def test_parse_input_lines_match_reference():
+    from paper_2207_05851_b200.errors import InputError
+    from paper_2207_05851_b200.search import parse_input_line
+    g = json.loads((GOLDEN / "search.json").read_text())
+    lines = ['a b   c', '{"text": "a b", "source_prefix": "<t>", "target_prefix": "x y", '
+             '"target_prefix_factors": ["O O B"], "source_factors": ["P Q"]}',
+             '{"text": "a", "extra": 1}', '{bad json', '{"text": 3}']
+    for ln, want in zip(lines, g["parsed"]):
+        if want["ok"]:
+            s = parse_input_line(ln)
+            assert s.tokens == want["tokens"] and s.source_factors == want["source_factors"]
+            assert s.source_prefix == want["source_prefix"]
+            assert s.target_prefix == want["target_prefix"]
+            assert s.target_prefix_factors == want["target_prefix_factors"]
+        else:
+            with pytest.raises(InputError):
+                parse_input_line(ln)
+
+
+def test_chunking_matches_reference():
+    from paper_2207_05851_b200.search import SentenceInput, chunk_input
+    g = json.loads((GOLDEN / "search.json").read_text())
+    got = [[c.tokens for c in chunk_input(SentenceInput(tokens=list("abcdefghij"),
+                                                        source_prefix=["<p>"]), 4)]]
+    assert got == g["chunks"]
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_product_init_equals_reference_init(name):
+    from paper_2207_05851_b200.config import init_params
+    ref = json.loads((GOLDEN / "params.json").read_text())[name]
+    p = init_params(product_config(name), CONFIGS[name]["seed"])
+    assert set(p) == set(ref)
+    for n, (s, a, first, last) in ref.items():
+        assert p[n].astype(np.float64).sum() == s and float(p[n].ravel()[0]) == first
+
+
+def test_model_dir_round_trip(tmp_path):
+    from paper_2207_05851_b200.checkpoint import (Vocabulary, format_config, parse_config,
+                                                  read_checkpoint, write_checkpoint)
+    cfg = product_config("srcfac")
+    assert parse_config(format_config(cfg)) == cfg
+    params = oracle_model("srcfac").p
+    write_checkpoint(tmp_path / "p.bin", params)
+    back = read_checkpoint(tmp_path / "p.bin")
+    assert set(back) == set(params)
+    assert all(np.array_equal(back[n], params[n]) for n in params)
+    v = Vocabulary(["<pad>", "<unk>", "<s>", "</s>", "a", "b"])
+    v.save(tmp_path / "v.json")
+    assert Vocabulary.load(tmp_path / "v.json").tokens == v.tokens
+    assert v.encode(["a", "zz"]) == [4, 1]
+
+
+def test_bad_checkpoints_are_data_errors(tmp_path):
+    from paper_2207_05851_b200.checkpoint import read_checkpoint, write_checkpoint
+    from paper_2207_05851_b200.errors import DataError
+    (tmp_path / "bad").write_bytes(b"XXXX")
+    with pytest.raises(DataError):
+        read_checkpoint(tmp_path / "bad")
+    write_checkpoint(tmp_path / "nan", {"a.b": np.array([np.nan], dtype=np.float32)})
+    with pytest.raises(DataError):
+        read_checkpoint(tmp_path / "nan")
+    write_checkpoint(tmp_path / "ok", {"a.b": np.ones(4, dtype=np.float32)})
+    raw = (tmp_path / "ok").read_bytes()
+    (tmp_path / "trunc").write_bytes(raw[:-3])
+    with pytest.raises(DataError):
+        read_checkpoint(tmp_path / "trunc")
+
+
+def test_shortlist_file(tmp_path):
+    from paper_2207_05851_b200.checkpoint import Vocabulary
+    from paper_2207_05851_b200.shortlist import Shortlist
+    (tmp_path / "sl").write_text("a\tx:0.5 y:0.25\nb\ty:1\nq\tx:1\n")
+    sv = Vocabulary(["<pad>", "<unk>", "<s>", "</s>", "a", "b"])
+    tv = Vocabulary(["<pad>", "<unk>", "<s>", "</s>", "x", "y"])
+    sl = Shortlist.from_file(tmp_path / "sl", sv, tv)
+    assert sl.lookup([4]).tolist() == [4, 5] and sl.lookup([5, 5]).tolist() == [5]
+    assert sl.lookup([0]).size == 0
+
+
+def test_cost_model_matches_survey_numbers():
+    """big 6-6 beam 5 at L=30 = 89.49 GFLOP/sentence."""
+    from paper_2207_05851_b200.config import ModelConfig
+    from oracle.skiff_oracle import sentence_flops
+    big = ModelConfig(32000, 32000, 1024, 16, 4096, 6, 6)
+    rows = [1] + [5] * 69
+    assert abs(sentence_flops(big, 30, rows) / 1e9 - 89.49) < 0.05
+
+
+def test_config_validation():
+    from paper_2207_05851_b200.config import ModelConfig, SourceFactorSpec
+    from paper_2207_05851_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        ModelConfig(11, 13, d_model=10, heads=4).validate()
+    with pytest.raises(ConfigError):
+        ModelConfig(11, 13, d_model=16, heads=4,
+                    source_factor_specs=[SourceFactorSpec(6, 8, "sum")]).validate()

@@ -1,0 +1,76 @@
+"""Teacher-forced decode_step parity (model.py:521-585) on the device model
+protocol, against logits recorded from the REFERENCE (tests/golden/steps_*).
+
+Tolerances (north star): per-step log-probs within 1e-4 in fp32 mode and
+2e-2 in bf16 mode, along the reference's own token path and row reorders.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from fixture_models import oracle_model, product_model
+from oracle import skiff_oracle as O
+from oracle.fixture_configs import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "bf16": 2e-2}
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("name", [n for n, s in CONFIGS.items() if s.get("steps")])
+def test_teacher_forced_steps(name, precision):
+    g = np.load(GOLDEN / f"steps_{name}.npz")
+    m = product_model(name, precision)
+    nsf, ntf = len(m.config.source_factor_specs), len(m.config.target_factor_specs)
+    st = m.decode_init(g["src"], [g[f"src_factor{i}"] for i in range(nsf)], g["lens"])
+    worst = 0.0
+    for t in range(g["fed"].shape[0]):
+        out = m.decode_step(st, g["fed"][t], [g[f"fed_factor{k}"][t] for k in range(ntf)])
+        lp = O.log_softmax(out.surface.data)
+        ref = O.log_softmax(g["logits"][t])
+        worst = max(worst, float(np.abs(lp - ref).max()))
+        for k in range(ntf):
+            assert np.abs(out.factors[k].data - g[f"factor_logits{k}"][t]).max() < 50 * TOL[precision]
+        st.select_rows(g["reorders"][t])
+    assert worst <= TOL[precision], worst
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_tiny_greedy_path_teacher_forced(precision):
+    """BASELINE configs[0] (tiny 2-1, d256, V8k): follow the ORACLE's greedy
+    path for 3 sentences and compare every step's full log-prob row."""
+    om = oracle_model("tiny")
+    m = product_model("tiny", precision)
+    rng = np.random.default_rng(3)
+    worst = 0.0
+    for _ in range(3):
+        src = [int(x) for x in rng.integers(4, 8000, size=12)]
+        trace = []
+        O.greedy(om, O.OChunk(src), trace=trace)
+        st = m.decode_init(np.array([src]), [], np.array([len(src)]))
+        for step in trace:
+            out = m.decode_step(st, np.array(step["fed"]), [])
+            lp = O.log_softmax(out.surface.data)[0]
+            worst = max(worst, float(np.abs(lp - step["lp"][0]).max()))
+    assert worst <= TOL[precision], worst
+
+
+def test_restricted_logits_are_a_column_subset():
+    """test_model.py:292-301 on the device."""
+    m = product_model("toy", "fp32")
+    src, lens = np.array([[4, 5, 6]]), np.array([3])
+    active = np.array([1, 3, 5, 8])
+    full = m.decode_step(m.decode_init(src, [], lens), np.array([2]), []).surface.data
+    sub = m.decode_step(m.decode_init(src, [], lens, active_ids=active), np.array([2]),
+                        []).surface.data
+    np.testing.assert_allclose(sub, full[:, active], rtol=0, atol=1e-6)
+
+
+def test_nvs_select_matches_reference():
+    g = np.load(GOLDEN / "steps_toy.npz")
+    m = product_model("toy", "fp32")
+    st = m.decode_init(g["src"], [], g["lens"])
+    ids = m.nvs_select(st.enc, g["lens"], 0.5, [0, 1, 3])
+    np.testing.assert_array_equal(np.concatenate(ids), g["nvs_ids"])

@@ -1,0 +1,115 @@
+"""End-to-end translate() on the GPU vs the reference's own records
+(tests/golden/search.json, produced by the reference) and vs the oracle.
+
+fp32 mode: output token sequences identical on >= 99% of records and
+scores within 1e-4 (north star: per-step log-probs within 1e-4 in fp32).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from fixture_models import product_model, product_vocabs
+from oracle.fixture_configs import SEARCH_CASES
+
+pytestmark = pytest.mark.gpu
+
+GOLD = {c["name"]: c["records"] for c in json.loads((GOLDEN / "search.json").read_text())["cases"]}
+
+
+def _settings(case):
+    from paper_2207_05851_b200.search import (NvsRestriction, SearchSettings,
+                                              ShortlistRestriction)
+    from paper_2207_05851_b200.shortlist import Shortlist
+    restriction = None
+    if case.get("shortlist"):
+        restriction = ShortlistRestriction(Shortlist(
+            {int(k): np.asarray(v, dtype=np.int64) for k, v in case["shortlist"].items()}))
+    elif case.get("nvs") is not None:
+        restriction = NvsRestriction(case["nvs"])
+    return SearchSettings(beam=case.get("beam", 1), length_alpha=case.get("alpha", 1.0),
+                          restriction=restriction, use_greedy=case.get("use_greedy"))
+
+
+def _run(case, precision):
+    from paper_2207_05851_b200.search import SentenceInput, translate
+    over = {"max_seq_len": case["max_seq_len"]} if case.get("max_seq_len") else {}
+    m = product_model(case["config"], precision, **over)
+    inputs = [SentenceInput(**inp) for inp in case["inputs"]]
+    return translate(m, product_vocabs(case["config"]), inputs, _settings(case))
+
+
+STATS = {"n": 0, "same": 0}
+
+
+@pytest.mark.parametrize("case", SEARCH_CASES, ids=lambda c: c["name"])
+def test_translate_fp32_matches_reference(case):
+    recs = _run(case, "fp32")
+    gold = GOLD[case["name"]]
+    assert len(recs) == len(gold)
+    mismatched = []
+    for r, g in zip(recs, gold):
+        assert (r.error is None) == (g["error"] is None), (r, g)
+        if g["error"] is not None:
+            assert r.text == "" and r.chunks == 0
+            continue
+        STATS["n"] += 1
+        assert r.chunks == g["chunks"]
+        if r.text == g["text"] and r.factors == g["factors"]:
+            STATS["same"] += 1
+            assert r.forced_eos == g["forced_eos"]
+            assert abs(r.score - g["score"]) <= 1e-4, (r.score, g["score"])
+        else:
+            mismatched.append((r.text, g["text"]))
+    # >= 99% identical overall; a small case may not lose a single record
+    assert len(mismatched) <= len(recs) // 100, mismatched
+
+
+def test_batch_equals_one_by_one():
+    """test_search.py:400-405 on the device path (batch composition invariance)."""
+    from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
+    case = next(c for c in SEARCH_CASES if c["name"] == "toy_beam3")
+    m = product_model("toy", "bf16")
+    v = product_vocabs("toy")
+    inputs = [SentenceInput(**i) for i in case["inputs"]]
+    together = translate(m, v, inputs, SearchSettings(beam=3))
+    single = [translate(m, v, [i], SearchSettings(beam=3))[0] for i in inputs]
+    assert together == single
+
+
+def test_greedy_equals_beam_one_device():
+    """test_search.py:170-177: bit-exact logprob and tokens."""
+    from paper_2207_05851_b200.search import SentenceInput, beam_search, greedy_search
+    m = product_model("toy", "bf16")
+    v = product_vocabs("toy")
+    for inp in next(c for c in SEARCH_CASES if c["name"] == "toy_greedy")["inputs"]:
+        s = SentenceInput(**inp)
+        g = greedy_search(m, v, s)
+        b = beam_search(m, v, s, beam=1)
+        assert g == b
+
+
+def test_wider_beam_never_scores_worse():
+    from paper_2207_05851_b200.search import SentenceInput, beam_search
+    m = product_model("toy", "fp32")
+    v = product_vocabs("toy")
+    for inp in next(c for c in SEARCH_CASES if c["name"] == "toy_beam3")["inputs"]:
+        s = SentenceInput(**inp)
+        assert beam_search(m, v, s, 4).normalized(1.0) >= beam_search(m, v, s, 1).normalized(1.0)
+
+
+def test_tiny_bf16_agreement_report():
+    """bf16 tensor-core mode on BASELINE configs[0]: outputs are NOT required
+    to be identical (random-init margins ~1e-3); per-step parity
+    is checked teacher-forced in test_model_gpu.py.  Here: sanity + report."""
+    case = next(c for c in SEARCH_CASES if c["name"] == "tiny_greedy_16x32")
+    recs = _run(case, "bf16")
+    gold = GOLD[case["name"]]
+    same = sum(r.text == g["text"] for r, g in zip(recs, gold))
+    tok_agree = np.mean([np.mean([a == b for a, b in zip(r.text.split(), g["text"].split())])
+                         for r, g in zip(recs, gold)])
+    print(f"bf16 tiny greedy: {same}/{len(gold)} identical, token agreement {tok_agree:.3f}")
+    assert all(r.forced_eos == g["forced_eos"] for r, g in zip(recs, gold))
+    assert tok_agree > 0.5
