@@ -561,9 +561,11 @@ def beam_select(lp, alive_scores, beam, active, forced_col=None):
 
 
 def beam(model: OracleModel, chunk: OChunk, beam_size: int, restriction=None,
-         alpha: float = 1.0, trace=None) -> OHyp:
+         alpha: float = 1.0, trace=None, normalize=log_softmax) -> OHyp:
     """search.py:325-394.  trace, if a list, receives per step the fed
-    tokens, the fp32 log-prob matrix, alive scores and the selection."""
+    tokens, the fp32 log-prob matrix, alive scores and the selection.
+    `normalize` maps the step's surface logits to log-probs (identity when a
+    test feeds log-probs directly, as the kernel's lp_in mode does)."""
     if beam_size < 1:
         raise OracleError("ConfigError", f"beam size must be at least 1, got {beam_size}")
     st, max_len = _start(model, chunk, restriction)
@@ -575,7 +577,7 @@ def beam(model: OracleModel, chunk: OChunk, beam_size: int, restriction=None,
     npre = len(chunk.prefix_ids)
     for t in range(max_len):
         surface, fac = model.decode_step(st, np.array(prev), [np.array(f) for f in prev_f])
-        lp = log_softmax(surface)
+        lp = normalize(surface)
         final_force = t == max_len - 1 and t >= npre
         forced_col = None
         if t < npre or final_force:

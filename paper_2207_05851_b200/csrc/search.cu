@@ -292,8 +292,10 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
   const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
   double s_par[32];
   int head[32];
+  // Other CTAs' row lists are read through L2 (ld.global.cg): they were
+  // written by other SMs during this launch.
   for (int q = 0; q < nalive; ++q) {
-    s_par[q] = st.score[base + q];
+    s_par[q] = __ldcg(st.score + base + q);
     head[q] = 0;
   }
   int n_new = 0;
@@ -305,9 +307,9 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
     int bc = 0;
     for (int q = 0; q < nalive; ++q) {
       const int rr = base + q;
-      if (head[q] >= st.cand_cnt[rr]) continue;
-      const double k = st.cand_score[(size_t)rr * K + head[q]];
-      const int c = st.cand_col[(size_t)rr * K + head[q]];
+      if (head[q] >= __ldcg(st.cand_cnt + rr)) continue;
+      const double k = __ldcg(st.cand_score + (size_t)rr * K + head[q]);
+      const int c = __ldcg(st.cand_col + (size_t)rr * K + head[q]);
       // order (key desc, token asc, parent asc); columns are sorted by token
       if (bq < 0 || k > bk || (k == bk && c < bc)) {
         bq = q;
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
     }
     if (bq < 0) break;
     const int rr = base + bq;
-    const float lp = st.cand_lp[(size_t)rr * K + head[bq]];
+    const float lp = __ldcg(st.cand_lp + (size_t)rr * K + head[bq]);
     head[bq]++;
     const double score = s_par[bq] + (double)lp;
     const int token = st.col_token ? st.col_token[bc] : bc;
@@ -328,10 +330,10 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
         st.best_norm[b] = norm;
         st.best_logprob[b] = score;
         st.best_steps[b] = steps;
-        st.best_forced[b] = final_force && st.row_argmax[rr] != bc;
+        st.best_forced[b] = final_force && __ldcg(st.row_argmax + rr) != bc;
         st.best_parent[b] = bq;
         for (int k = 0; k < nf; ++k)
-          st.best_fac[(size_t)b * nf + k] = st.fac_choice[(size_t)rr * nf + k];
+          st.best_fac[(size_t)b * nf + k] = __ldcg(st.fac_choice + (size_t)rr * nf + k);
       }
     } else {
       const int slot = base + n_new;
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
       st.tok_hist[(size_t)t * R + slot] = token;
       st.par_hist[(size_t)t * R + slot] = bq;
       for (int k = 0; k < nf; ++k) {
-        const int f = st.fac_choice[(size_t)rr * nf + k];
+        const int f = __ldcg(st.fac_choice + (size_t)rr * nf + k);
         st.ftok_next[(size_t)k * R + slot] = f;
         st.fac_hist[((size_t)t * nf + k) * R + slot] = f;
       }

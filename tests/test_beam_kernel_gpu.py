@@ -129,7 +129,7 @@ class _OracleAdapter:
 def test_ties_match_oracle(seed, beam):
     m = TieModel(V=9, seed=seed)
     src = [5, 6]
-    want = O.beam(_OracleAdapter(m), O.OChunk(src), beam)
+    want = O.beam(_OracleAdapter(m), O.OChunk(src), beam, normalize=lambda x: x)
     ps = _device_beam(m, src, beam)
     ps.lp_in = True
     got = ps.run()
@@ -140,7 +140,8 @@ def test_ties_match_oracle(seed, beam):
 def test_prefix_forcing_and_forced_keys():
     m = TieModel(V=9, seed=11)
     src = [5, 6, 7]
-    want = O.beam(_OracleAdapter(m), O.OChunk(src, prefix_ids=[7, 8, 4]), 4)
+    want = O.beam(_OracleAdapter(m), O.OChunk(src, prefix_ids=[7, 8, 4]), 4,
+                  normalize=lambda x: x)
     ps = _device_beam(m, src, 4, prefix=[7, 8, 4])
     ps.lp_in = True
     got = ps.run()
