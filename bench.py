@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark: transformer-big 6-6 beam-5 translation throughput on B200.
+
+Metric (BASELINE.json): sentences/sec (transformer-big beam 5) at 1/2/4/8
+B200.  Workload per GPU and step: one batch of 128 synthetic WMT-shaped
+sentences (L = 30 source tokens, uniform ids) decoded with beam
+5 and length penalty alpha = 1.0 (search.py:74-75) in bf16 on random-init
+weights (seed 13, model.py:244-265).  Every random-init decode runs to the
+2L+10 = 70-step cap, so the work per sentence is fixed.
+
+  value       device throughput: inputs staged in HBM, timed region =
+              encoder + cross K/V + 70 captured decode steps + finalize
+  e2e         the public API: translate(model, vocabs, SentenceInput list)
+              from host strings to TranslationRecords (H2D/D2H inside)
+  roofline    all tcgen05 GEMMs of one decode step (the dominant kernel
+              class), timed live with CUDA events on their stream
+  cpu_baseline the reference algorithm (oracle port, float64 numpy) on this
+              box's host cores, bounded sample, rank 0 at N=1 only
+
+Multi-GPU: `python -m torch.distributed.run --nproc-per-node N bench.py
+--gpus N`; sentences are sharded (weak scaling, replicas), the only
+collective is the final gather of hypotheses to rank 0.
+`--impl reference` times the reference's CPU algorithm (oracle port) on the
+same workload instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+from types import SimpleNamespace
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sentences/sec (transformer-big beam 5)"
+UNIT = "sentences/s"
+BIG = dict(src_vocab_size=32000, trg_vocab_size=32000, d_model=1024, heads=16, ff_dim=4096,
+           encoder_layers=6, decoder_layers=6, decoder_kind="self_attention", max_seq_len=128)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--beam", type=int, default=5)
+    ap.add_argument("--src-len", type=int, default=30)
+    ap.add_argument("--alpha", type=float, default=1.0)
+    ap.add_argument("--cpu-steps", type=int, default=6, help="decode steps in the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON rules)")
+    return ap.parse_args()
+
+
+def synth_sentences(n, L, V, seed):
+    """default_rng(seed).integers(0, V-4) -> tokens w{i} (ids 4..V-1)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    return [[f"w{int(i)}" for i in rng.integers(0, V - 4, size=L)] for _ in range(n)]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(device_index)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        loaded = [x for x in sm if smax and x > 0.3 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- our path
+def build_model(precision="bf16"):
+    from paper_2207_05851_b200.checkpoint import SPECIALS, Vocabulary
+    from paper_2207_05851_b200.config import ModelConfig, init_params
+    from paper_2207_05851_b200.model import Model
+    cfg = ModelConfig(**BIG)
+    model = Model(cfg, params=init_params(cfg, 13), precision=precision)
+    words = SPECIALS + [f"w{i}" for i in range(cfg.trg_vocab_size - 4)]
+    v = Vocabulary(words)
+    vocabs = SimpleNamespace(src_vocab=v, trg_vocab=v, src_factor_vocabs=[], trg_factor_vocabs=[])
+    return model, vocabs
+
+
+def make_batch(model, vocabs, sentences, beam, alpha):
+    from paper_2207_05851_b200.engine import BeamBatch
+    from paper_2207_05851_b200.search import SentenceInput, _chunk_job
+    jobs = [_chunk_job(model, SentenceInput(tokens=s), vocabs, None)[0] for s in sentences]
+    return BeamBatch(model, jobs, beam, alpha)
+
+
+def gemm_roofline(model, R, L, peak):
+    """Time every GEMM of one decode step (all 6 layers + output projection)
+    with CUDA events on the launching stream; achieved = algorithmic FLOPs
+    (2*M*N*K summed) / measured time."""
+    import torch
+    from paper_2207_05851_b200 import _native as N
+    from paper_2207_05851_b200 import kern
+    c = model.config
+    d = c.d_model
+    dev, cdt = model.device, model.cdt
+    h = torch.randn(R, d, device=dev).to(cdt)
+    f = torch.randn(R, c.ff_dim, device=dev).to(cdt)
+    x = torch.zeros(R, d, device=dev)
+    qkv = torch.empty(R, 3 * d, device=dev, dtype=cdt)
+    q = torch.empty(R, d, device=dev, dtype=cdt)
+    ff = torch.empty(R, c.ff_dim, device=dev, dtype=cdt)
+    logits = torch.empty(R, c.trg_vocab_size, device=dev)
+    calls, flops = [], 0
+    for Ly in model.dec:
+        calls += [(h, Ly.wqkv, qkv, N.EPI_STORE, None), (h, Ly.wo, x, N.EPI_RESID, None),
+                  (h, Ly.wq_c, q, N.EPI_STORE, None), (h, Ly.wo_c, x, N.EPI_RESID, None),
+                  (h, Ly.w1, ff, N.EPI_RELU, Ly.b1), (f, Ly.w2, x, N.EPI_RESID, Ly.b2)]
+    out_call = (h, model.E_trg_c, logits, N.EPI_STORE, None)
+    calls.append(out_call)
+    for A, W, o, kind, b in calls:
+        flops += 2 * R * W.shape[0] * W.shape[1]
+
+    def run(cs):
+        for A, W, o, kind, b in cs:
+            kern.gemm(A, W, o, kind, b)
+
+    for _ in range(3):
+        run(calls)
+    torch.cuda.synchronize()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run(calls)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    e0.record()
+    for _ in range(reps):
+        run([out_call])
+    e1.record()
+    torch.cuda.synchronize()
+    ms_out = e0.elapsed_time(e1) / reps
+    out_flops = 2 * R * model.E_trg_c.shape[0] * d
+    achieved = flops / (ms / 1e3) / 1e12
+    return {"kernel": "k_gemm_tc (tcgen05 bf16, all GEMMs of one decode step, R=%d)" % R,
+            "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "flops_per_step": flops, "ms_per_decode_step_gemms": round(ms, 4),
+            "out_proj": {"ms": round(ms_out, 4),
+                         "tflops": round(out_flops / (ms_out / 1e3) / 1e12, 1)}}
+
+
+def step_breakdown(bb):
+    """Eager replay of one mid-sequence decode step with CUDA events between
+    kernel groups (attention, GEMMs, LN, beam) — explains `value`."""
+    import torch
+    from paper_2207_05851_b200 import engine, kern
+    from paper_2207_05851_b200 import _native as N
+    sb = bb.sb
+    sb.step.fill_(35)
+    bb.done.zero_()
+    bb.n_alive.fill_(bb.K)
+    groups = {}
+    ev = []
+
+    orig = {n: getattr(kern, n) for n in ("gemm", "layernorm", "self_attention_step",
+                                          "cross_attention_step", "embed_target", "beam_step",
+                                          "beam_reorder")}
+
+    def wrap(name, fn):
+        def inner(*a, **k):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn(*a, **k)
+            e.record()
+            ev.append((name, s, e))
+        return inner
+
+    for n, fn in orig.items():
+        setattr(kern, n, wrap(n, fn))
+    try:
+        for _ in range(2):
+            ev.clear()
+            engine.step_forward(bb.model, sb)
+            kern.beam_step(sb.logits, bb.state)
+        torch.cuda.synchronize()
+    finally:
+        for n, fn in orig.items():
+            setattr(kern, n, fn)
+    for name, s, e in ev:
+        groups[name] = groups.get(name, 0.0) + s.elapsed_time(e)
+    total = sum(groups.values())
+    return {k: round(v, 4) for k, v in sorted(groups.items(), key=lambda kv: -kv[1])} | {
+        "total_ms": round(total, 4)}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2207_05851_b200 import kern
+    from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    from paper_2207_05851_b200 import _native as N
+    N.call("skb_set_device", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak_tf = peaks.get("bf16_tflops", 1590.0)
+    peak_src = "measured (MEASURED_PEAKS.json bf16_tflops, burst)" if peaks else "fallback"
+
+    model, vocabs = build_model("bf16")
+    V = model.config.trg_vocab_size
+    B, K, L = args.batch, args.beam, args.src_len
+
+    def sents(step):
+        return synth_sentences(B, L, V, seed=13 + 7919 * rank + 104729 * step)
+
+    def gather(bb):
+        if world > 1:
+            toks = bb.tokens_out
+            out = [torch.empty_like(toks) for _ in range(world)] if rank == 0 else None
+            dist.gather(toks, out, dst=0)
+
+    # ---- warm-up (also compiles TMA descriptors, captures graphs)
+    for w in range(args.warmup):
+        bb = make_batch(model, vocabs, sents(1000 + w), K, args.alpha)
+        bb.run()
+        gather(bb)
+    torch.cuda.synchronize()
+    # ---- value: inputs staged in HBM before the timed region
+    batches = [make_batch(model, vocabs, sents(s), K, args.alpha) for s in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    l0 = kern.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    results = []
+    for bb in batches:
+        results.append(bb.run())
+        gather(bb)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = kern.launches - l0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * B * args.steps / (ms_max / 1e3)
+    forced = sum(r.forced_eos for res in results for r in res)
+    steps_per_sent = statistics.mean(r.steps for res in results for r in res)
+
+    # ---- e2e: the public API from host strings to records
+    e2e = None
+    if not args.no_e2e:
+        settings = SearchSettings(beam=K, length_alpha=args.alpha)
+        host_inputs = [[SentenceInput(tokens=s) for s in sents(500 + s)] for s in range(args.steps)]
+        translate(model, vocabs, host_inputs[0][:8], settings)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record()
+        for inp in host_inputs:
+            recs = translate(model, vocabs, inp, settings, max_rows=B * K)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        S = 2 * L + 10
+        h2d = B * L * 4 + B * 4 * 4 + B * 8          # ids, lengths/limits/prefix, step tables
+        d2h = B * S * 4 + B * (8 + 4 + 4) + B * S * 4  # tokens, best score/steps/forced, factors
+        e2e = {"value": round(world * B * args.steps / (e2e_ms / 1e3), 2), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "paper_2207_05851_b200.search.translate"}
+        assert len(recs) == B and all(r.error is None for r in recs)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    roof = gemm_roofline(model, B * K, L, peak_tf)
+    roof["peak_source"] = peak_src
+    breakdown = step_breakdown(batches[-1])
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (uniform random source ids, random-init weights seed 13)",
+        "config": {"workload": f"transformer-big 6-6 (d1024 H16 ff4096 V32000) beam {K} "
+                               f"alpha {args.alpha}, batch {B} sentences/GPU, src len {L}, "
+                               f"{2 * L + 10}-step cap",
+                   "global_batch": B * world, "seq_len": L, "parallelism": f"replicas x{world}",
+                   "l2": "working set > L2 (weights 0.48 GB + KV cache 1.1 GB per batch)"},
+        "e2e": e2e, "roofline": roof, "gpu_launches": launches, "clocks": clk,
+        "decode": {"mean_steps_per_sentence": round(steps_per_sent, 2),
+                   "forced_eos_sentences": forced, "step_breakdown_ms": breakdown},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg(args, L, K)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_leg(args, L, K, pool=None):
+    import numpy as np
+    from oracle.cpu_baseline import CpuBaseline
+    own = pool is None
+    pool = pool or CpuBaseline(BIG)
+    rng = np.random.default_rng(13)
+    srcs = [[int(i) + 4 for i in rng.integers(0, BIG["trg_vocab_size"] - 4, size=L)]
+            for _ in range(pool.procs)]
+    rate, wall, det = pool.sample(srcs, K, args.alpha, args.cpu_steps)
+    if own:
+        pool.close()
+    return {"value": round(rate, 4), "unit": UNIT, "cores": pool.procs, "kind": "port",
+            "sample": f"{pool.procs} single-thread processes x 1 sentence (L={L}, beam {K}): "
+                      f"encode + first {args.cpu_steps} of {2 * L + 10} steps, extrapolated "
+                      f"linearly; {det['sec_per_sentence']:.1f} s/sentence/core",
+            "wall_s": round(wall, 2)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import CpuBaseline
+    pool = CpuBaseline(BIG)
+    L, K = args.src_len, args.beam
+    for _ in range(args.warmup):
+        cpu_baseline_leg(args, L, K, pool)
+    vals, walls = [], []
+    for _ in range(args.steps):
+        r = cpu_baseline_leg(args, L, K, pool)
+        vals.append(r["value"])
+        walls.append(r["wall_s"])
+    pool.close()
+    value = statistics.mean(vals)
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.mean(walls), 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
+            "data": "synthetic", "config": {"workload": f"transformer-big 6-6 beam {K} alpha "
+                                                        f"{args.alpha}, src len {L}"},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": pool.procs,
+                             "kind": "port",
+                             "sample": f"per step: {pool.procs} processes x 1 sentence, encode + "
+                                       f"{args.cpu_steps} of {2 * L + 10} steps, extrapolated"},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -561,11 +561,16 @@ def beam_select(lp, alive_scores, beam, active, forced_col=None):
 
 
 def beam(model: OracleModel, chunk: OChunk, beam_size: int, restriction=None,
-         alpha: float = 1.0, trace=None, normalize=log_softmax) -> OHyp:
+         alpha: float = 1.0, trace=None, normalize=log_softmax, max_steps=None,
+         timings=None) -> OHyp:
     """search.py:325-394.  trace, if a list, receives per step the fed
     tokens, the fp32 log-prob matrix, alive scores and the selection.
     `normalize` maps the step's surface logits to log-probs (identity when a
-    test feeds log-probs directly, as the kernel's lp_in mode does)."""
+    test feeds log-probs directly, as the kernel's lp_in mode does).
+    max_steps / timings bound the run for CPU-baseline sampling: timings
+    receives the wall time of decode_init and of every executed step."""
+    import time as _time
+    t_start = _time.perf_counter()
     if beam_size < 1:
         raise OracleError("ConfigError", f"beam size must be at least 1, got {beam_size}")
     st, max_len = _start(model, chunk, restriction)
@@ -575,7 +580,12 @@ def beam(model: OracleModel, chunk: OChunk, beam_size: int, restriction=None,
     finished: list[OHyp] = []
     prev, prev_f = [BOS_ID], [[SHIFT_ID] for _ in range(nf)]
     npre = len(chunk.prefix_ids)
+    if timings is not None:
+        timings.append(_time.perf_counter() - t_start)
     for t in range(max_len):
+        if max_steps is not None and t >= max_steps:
+            return None
+        t0 = _time.perf_counter()
         surface, fac = model.decode_step(st, np.array(prev), [np.array(f) for f in prev_f])
         lp = normalize(surface)
         final_force = t == max_len - 1 and t >= npre
@@ -604,6 +614,8 @@ def beam(model: OracleModel, chunk: OChunk, beam_size: int, restriction=None,
         if not new_alive:
             break
         st.select_rows(parents)
+        if timings is not None:
+            timings.append(_time.perf_counter() - t0)
         alive = new_alive
         prev = nxt
         prev_f = [[c[k] for c in nxt_f] for k in range(nf)]

@@ -165,7 +165,11 @@ def nvs_active_sets(model: Model, enc, len_d, B, L, threshold, jobs) -> list[np.
 
 
 class BeamBatch:
-    """Device state of one batched beam (or greedy, K=1) run."""
+    """Device state of one batched beam (or greedy, K=1) run.
+
+    Construction does the host work and stages every input on the device
+    (ids, lengths, prefixes, restriction masks, buffers); `run()` is pure
+    device work: encoder, cross K/V, the captured decode loop, finalize."""
 
     GRAPH_POLL = 8
 
@@ -177,43 +181,78 @@ class BeamBatch:
             raise ConfigError(f"beam size {beam} exceeds the device limit of 32")
         self.model, self.jobs, self.K, self.alpha = model, jobs, beam, alpha
         self.use_graph = use_graph
+        self.nvs_threshold = nvs_threshold
         c = model.config
         dev = model.device
         nf = len(c.target_factor_specs)
-        enc, len_d, B, L = _encode_batch(model, jobs)
+        self.nf = nf
+        B = len(jobs)
+        L = max(len(j.src_ids) for j in jobs)
         self.B, self.L = B, L
-        ckv = model.cross_kv_device(enc) if c.decoder_layers else None
-        # ---- restricted output vocabulary (search.py:235-242)
-        actives = [j.active_ids for j in jobs]
-        if nvs_threshold is not None:
-            actives = nvs_active_sets(model, enc, len_d, B, L, nvs_threshold, jobs)
+        # ---- source ids (padded), staged on the device
+        ids = np.zeros((B, L), dtype=np.int32)
+        nsf = len(c.source_factor_specs)
+        fids = np.zeros((max(nsf, 1), B, L), dtype=np.int32)
+        lengths = np.zeros(B, dtype=np.int32)
+        for b, j in enumerate(jobs):
+            n = len(j.src_ids)
+            ids[b, :n] = j.src_ids
+            lengths[b] = n
+            for k in range(nsf):
+                fids[k, b, :n] = j.src_factor_ids[k]
+        if (ids < 0).any() or (ids >= c.src_vocab_size).any():
+            raise ShapeError(f"ids out of range [0, {c.src_vocab_size}) for embedding table")
+        self.h2d_bytes = ids.nbytes + lengths.nbytes + (fids.nbytes if nsf else 0)
+        self.ids_d = torch.from_numpy(ids.reshape(-1)).to(dev)
+        self.fids_d = torch.from_numpy(fids.reshape(max(nsf, 1), -1)).to(dev) if nsf else None
+        self.len_d = torch.from_numpy(lengths).to(dev)
+        # ---- per-chunk limits
+        max_len = np.array([2 * len(j.src_ids) + 10 for j in jobs], dtype=np.int32)
+        self.S_max = int(max_len.max())
+        self.max_len = torch.from_numpy(max_len).to(dev)
+        self.prefix_len = torch.tensor([len(j.prefix_ids) for j in jobs], dtype=I32, device=dev)
+        self.R = B * beam
+        self.row_sent = torch.arange(self.R, dtype=I32, device=dev) // beam
+        self.len_pen = torch.tensor([float(s) ** alpha if s > 0 else 1.0
+                                     for s in range(self.S_max + 1)],
+                                    dtype=torch.float64, device=dev)
+        self.sb = None
+        if nvs_threshold is None:
+            self._setup_vocab([j.active_ids for j in jobs])
+        self.graph = None
+        self.steps_run = 0
+        self.launches_per_step = 0
+
+    def _setup_vocab(self, actives):
+        """Restricted output vocabulary (search.py:235-242) as the union U of
+        the chunks' active sets plus a per-chunk column bitmask; then every
+        buffer of the decode loop."""
+        model, c, dev = self.model, self.model.config, self.model.device
+        B, K, nf, jobs = self.B, self.K, self.nf, self.jobs
         restricted = any(a is not None for a in actives)
         V = c.trg_vocab_size
         if restricted:
             actives = [a if a is not None else np.arange(V, dtype=np.int64) for a in actives]
             U_ids = np.unique(np.concatenate(actives)).astype(np.int64)
             U = int(U_ids.size)
-            words = (U + 31) // 32
-            mask = np.zeros((B, words), dtype=np.uint32)
+            mask = np.zeros((B, (U + 31) // 32), dtype=np.uint32)
             for b, a in enumerate(actives):
                 cols = np.searchsorted(U_ids, a)
-                np.bitwise_or.at(mask[b], cols >> 5, (np.uint32(1) << (cols & 31).astype(np.uint32)))
+                np.bitwise_or.at(mask[b], cols >> 5,
+                                 (np.uint32(1) << (cols & 31).astype(np.uint32)))
             self.col_token = torch.from_numpy(U_ids.astype(np.int32)).to(dev)
             self.mask = torch.from_numpy(mask.view(np.int32)).to(dev)
             E_out = torch.empty(U, c.d_model, device=dev, dtype=model.cdt)
-            kern.gather_rows(model.E_trg_c, self.col_token, E_out)
+            self._gather_E = True
             col_of = {int(t): i for i, t in enumerate(U_ids)}
         else:
             U = V
             self.col_token = self.mask = None
             E_out = model.E_trg_c
+            self._gather_E = False
             col_of = None
         self.U = U
         eos_col = col_of[EOS_ID] if restricted else EOS_ID
-        # ---- per-chunk limits and prefixes
-        max_len = np.array([2 * len(j.src_ids) + 10 for j in jobs], dtype=np.int32)
-        S_max = int(max_len.max())
-        self.S_max = S_max
         P = max(1, max(len(j.prefix_ids) for j in jobs))
         prefix_col = np.full((B, P), -1, dtype=np.int32)
         prefix_fac = np.full((B, max(nf, 1), P), -1, dtype=np.int32)
@@ -227,19 +266,16 @@ class BeamBatch:
                     prefix_col[b, t] = tok
             for k, stream in enumerate(j.prefix_factor_ids[:nf]):
                 prefix_fac[b, k, :len(stream)] = stream
-        K = beam
-        R = B * K
-        self.R = R
-        row_sent = torch.arange(R, dtype=I32, device=dev) // K
-        self.sb = StepBuffers(model, R, B, L, S_max, U, E_out, ckv, len_d, row_sent)
+        R, S_max = self.R, self.S_max
+        D2 = 2 * c.d_model * c.decoder_layers
+        ckv = torch.empty(B * self.L, max(D2, 1), device=dev, dtype=model.cdt)
+        self.sb = StepBuffers(model, R, B, self.L, S_max, U, E_out, ckv, self.len_d,
+                              self.row_sent)
+        sb = self.sb
 
         def z(n, dt=I32):
             return torch.zeros(n, dtype=dt, device=dev)
 
-        self.len_pen = torch.tensor([float(s) ** alpha if s > 0 else 1.0 for s in range(S_max + 1)],
-                                    dtype=torch.float64, device=dev)
-        self.max_len = torch.from_numpy(max_len).to(dev)
-        self.prefix_len = torch.tensor([len(j.prefix_ids) for j in jobs], dtype=I32, device=dev)
         self.prefix_col = torch.from_numpy(prefix_col).to(dev)
         self.prefix_fac = torch.from_numpy(prefix_fac).to(dev)
         self.n_alive = torch.ones(B, dtype=I32, device=dev)
@@ -262,7 +298,8 @@ class BeamBatch:
         self.best_parent = z(B)
         self.best_fac = z(B * max(nf, 1))
         self.n_done = z(1)
-        sb = self.sb
+        self.tokens_out = z(B * S_max).view(B, S_max)
+        self.factors_out = z(B * max(nf, 1) * S_max).view(B, max(nf, 1), S_max)
         self.state = N.BeamState(
             B, K, U, S_max, nf, self.len_pen.data_ptr(), sb.step.data_ptr(),
             N.ptr(self.col_token), N.ptr(self.mask), eos_col, self.max_len.data_ptr(),
@@ -277,9 +314,20 @@ class BeamBatch:
             self.best_logprob.data_ptr(), self.best_steps.data_ptr(),
             self.best_forced.data_ptr(), self.best_parent.data_ptr(), self.best_fac.data_ptr(),
             self.n_done.data_ptr())
-        self.graph = None
-        self.steps_run = 0
-        self.launches_per_step = 0
+
+    def _encode(self):
+        """Encoder + all layers' cross K/V (model.py:414-430, 527-531)."""
+        m = self.model
+        nsf = len(m.config.source_factor_specs)
+        enc = m.encode_device(self.ids_d, self.fids_d if nsf else None, self.len_d,
+                              self.B, self.L)
+        if self.nvs_threshold is not None:
+            self._setup_vocab(nvs_active_sets(m, enc, self.len_d, self.B, self.L,
+                                              self.nvs_threshold, self.jobs))
+        if m.config.decoder_layers:
+            m.cross_kv_device(enc, out=self.sb.ckv)
+        if self._gather_E:
+            kern.gather_rows(m.E_trg_c, self.col_token, self.sb.E_out)
 
     # ------------------------------------------------------------- stepping
     def _one_step(self):
@@ -288,6 +336,7 @@ class BeamBatch:
         kern.beam_reorder(self.sb.anc, self.sb.parent, self.sb.step, self.R, self.S_max)
 
     def run(self) -> list[ChunkResult]:
+        self._encode()
         before = kern.launches
         self._one_step()                      # step 0 eagerly (also warms every kernel)
         self.launches_per_step = kern.launches - before
@@ -319,11 +368,9 @@ class BeamBatch:
     def collect(self) -> list[ChunkResult]:
         c = self.model.config
         nf = len(c.target_factor_specs)
-        B, S = self.B, self.S_max
-        toks = torch.zeros(B, S, dtype=I32, device=self.model.device)
-        facs = torch.zeros(B, max(nf, 1), S, dtype=I32, device=self.model.device)
-        kern.beam_finalize(self.state, toks, facs)
-        toks, facs = toks.cpu().numpy(), facs.cpu().numpy()
+        B = self.B
+        kern.beam_finalize(self.state, self.tokens_out, self.factors_out)
+        toks, facs = self.tokens_out.cpu().numpy(), self.factors_out.cpu().numpy()
         steps = self.best_steps.cpu().numpy()
         lp = self.best_logprob.cpu().numpy()
         forced = self.best_forced.cpu().numpy()

@@ -196,7 +196,7 @@ class Model:
             kern.gemm(f, Ly.w2, x, N.EPI_RESID, Ly.b2)
         return x
 
-    def cross_kv_device(self, enc: torch.Tensor) -> torch.Tensor:
+    def cross_kv_device(self, enc: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """All decoder layers' cross K|V in one GEMM (model.py:527-531)."""
         n, d = enc.shape
         if self.cdt == torch.float32:
@@ -204,7 +204,8 @@ class Model:
         else:
             a = torch.empty(n, d, device=self.device, dtype=self.cdt)
             kern.convert(enc, a)
-        out = torch.empty(n, self.w_ckv.shape[0], device=self.device, dtype=self.cdt)
+        if out is None:
+            out = torch.empty(n, self.w_ckv.shape[0], device=self.device, dtype=self.cdt)
         kern.gemm(a, self.w_ckv, out)
         return out
 
