@@ -44,6 +44,8 @@ extern "C" {
 #define SKB_EPI_RESID 2  /* x  += acc (+bias), x fp32     (model.py:565-574)   */
 #define SKB_EPI_SSRU 3   /* SSRU cell, columns interleaved (f_j, Wx_j)         */
                          /*                               (model.py:268-272)   */
+#define SKB_EPI_LOGITS 4 /* fp32 logits + fused log-softmax partials          */
+                         /* (kernels.py:287-295, search.py:294/347)            */
 
 /* GEMM epilogue parameters (plain C struct, passed by pointer). */
 typedef struct skb_epilogue {
@@ -62,6 +64,15 @@ typedef struct skb_epilogue {
   /* reads half ((t+1)&1) (zeros at t = 0); c_prev is ignored.              */
   const int *step;
   long long state_stride; /* elements between the two halves                 */
+  /* SKB_EPI_LOGITS: besides storing fp32 logits in out, write for every row  */
+  /* m and 32-column group g the partial (max, sum exp(x - max)) over the     */
+  /* row's active columns as float2 lse_part[m * lse_ld + g]; the active set  */
+  /* of row m is bit row (m / rows_per_group) of mask (NULL = all columns).   */
+  float *lse_part;
+  int lse_ld;
+  const unsigned *mask;
+  int mask_words;
+  int rows_per_group;
 } skb_epilogue;
 
 /* Library identity / diagnostics */
@@ -138,12 +149,14 @@ int skb_self_attention_step(int R, int H, int dh, const void *qkv, int ld_qkv, i
  * Cross-attention for one step (model.py:568-573): q [R, ldq]; row r reads
  * sentence row_sent[r] of the per-sentence encoder K/V memory
  * kv [B*L, ld_kv] (K at column offset koff, V at voff), masked past
- * lengths[sentence].
+ * lengths[sentence].  Rows [g*G, g*G+G) (G = rows_per_group, the beam) must
+ * share one sentence: its K/V slice is staged in shared memory once per
+ * (group, head) and read by all G rows.
  */
 int skb_cross_attention_step(int R, int H, int dh, const void *q, int ldq, int q_dtype,
                              const void *kv, int ld_kv, int kv_dtype, int koff, int voff,
-                             int L, const int *row_sent, const int *lengths, void *ctx,
-                             int ldc, int ctx_dtype, void *stream);
+                             int L, const int *row_sent, const int *lengths, int rows_per_group,
+                             void *ctx, int ldc, int ctx_dtype, void *stream);
 
 /* Gather rows of a table: out[i] = table[idx[i]] (row width w, dtype). Used to
  * build the restricted output-projection operand E[active] (model.py:577-581). */
@@ -183,6 +196,9 @@ typedef struct skb_beam_state {
   const float *fac_logits;/* [R, fac_ld] all factor heads side by side, or NULL*/
   int fac_ld;             /* row stride of fac_logits                          */
   const int *fac_off;     /* [n_factors+1] column offsets (device)            */
+  const float *lse_part;  /* [R, lse_ld] float2 partials from SKB_EPI_LOGITS  */
+                          /* (NULL: the step kernel reduces the row itself)  */
+  int lse_ld;
   /* scratch */
   double *cand_score;     /* [R, K] */
   float *cand_lp;         /* [R, K] */

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libskiff_b200.so"
 
 SKB_OK, SKB_ERR_SHAPE, SKB_ERR_CONFIG, SKB_ERR_LAUNCH, SKB_ERR_NUMERIC, SKB_ERR_UNSUPPORTED = range(6)
 F32, BF16 = 0, 1
-EPI_STORE, EPI_RELU, EPI_RESID, EPI_SSRU = 0, 1, 2, 3
+EPI_STORE, EPI_RELU, EPI_RESID, EPI_SSRU, EPI_LOGITS = 0, 1, 2, 3, 4
 
 vp = C.c_void_p
 i32 = C.c_int
@@ -25,7 +25,8 @@ i32 = C.c_int
 class Epilogue(C.Structure):
     _fields_ = [("kind", i32), ("bias", vp), ("out", vp), ("ldo", i32), ("out_dtype", i32),
                 ("c_prev", vp), ("c_next", vp), ("src_row", vp), ("ld_state", i32),
-                ("step", vp), ("state_stride", C.c_longlong)]
+                ("step", vp), ("state_stride", C.c_longlong), ("lse_part", vp),
+                ("lse_ld", i32), ("mask", vp), ("mask_words", i32), ("rows_per_group", i32)]
 
 
 class BeamState(C.Structure):
@@ -35,7 +36,8 @@ class BeamState(C.Structure):
                 ("P", i32), ("prefix_fac", vp), ("n_alive", vp), ("done", vp), ("score", vp),
                 ("tok_next", vp), ("ftok_next", vp), ("parent", vp),
                 ("tok_hist", vp), ("par_hist", vp), ("fac_hist", vp), ("fac_logits", vp),
-                ("fac_ld", i32), ("fac_off", vp), ("cand_score", vp), ("cand_lp", vp),
+                ("fac_ld", i32), ("fac_off", vp), ("lse_part", vp), ("lse_ld", i32),
+                ("cand_score", vp), ("cand_lp", vp),
                 ("cand_col", vp), ("cand_cnt", vp), ("row_argmax", vp), ("fac_choice", vp),
                 ("counter", vp), ("best_norm", vp), ("best_logprob", vp), ("best_steps", vp),
                 ("best_forced", vp), ("best_parent", vp), ("best_fac", vp), ("n_done", vp)]
@@ -55,7 +57,7 @@ SIGNATURES = {
     "skb_self_attention_step": [i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp, vp, vp, i32,
                                 i32, vp],
     "skb_cross_attention_step": [i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp,
-                                 vp, vp, i32, i32, vp],
+                                 vp, i32, vp, i32, i32, vp],
     "skb_gather_rows": [i32, i32, vp, i32, vp, vp, i32, i32, vp],
     "skb_beam_step": [vp, i32, i32, C.POINTER(BeamState), vp],
     "skb_beam_reorder": [i32, i32, vp, vp, vp, vp],

@@ -211,6 +211,221 @@ __global__ void __launch_bounds__(128) k_cross_attention_step(
   write_ctx(st, ctx, ctx_dtype, (size_t)r * ldc + h * dh, dh, lane);
 }
 
+// ------------------------------------------- grouped attention (smem K/V)
+// One CTA per (group of query rows, head).  All rows of a group attend over
+// the same sentence memory, so its K/V slice is loaded into shared memory
+// once (fp32, rows padded to dh+1 floats: conflict-free column reads) and
+// reused by every row: the beam rows of a sentence in cross-attention
+// (model.py:568-573), or the L query positions of a sentence in the encoder
+// (model.py:420-429).  Warp w handles rows w, w+nw, ... of the group.
+__global__ void __launch_bounds__(256) k_attn_smem(
+    int R, int G, int H, int dh, const void *q, int ldq, int q_dtype, int qoff, const void *kv,
+    int ld_kv, int kv_dtype, int koff, int voff, int L, const int *row_sent, const int *lengths,
+    float scale, void *ctx, int ldc, int ctx_dtype) {
+  extern __shared__ float sm[];
+  const int g = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int row0 = g * G;
+  const int b = row_sent ? row_sent[row0] : g;
+  const int len = lengths[b];
+  const int ldk = dh + 1;
+  float *Ks = sm;
+  float *Vs = sm + (size_t)L * ldk;
+  float *Qs = Vs + (size_t)L * ldk;  // [nw][dh]
+  // ---- stage K/V of (sentence b, head h) in shared memory
+  for (int idx = threadIdx.x; idx < len * dh; idx += blockDim.x) {
+    const int j = idx / dh, c = idx % dh;
+    const size_t kr = (size_t)(b * L + j) * ld_kv + h * dh + c;
+    Ks[j * ldk + c] = load_f(kv, kv_dtype, kr + koff);
+    Vs[j * ldk + c] = load_f(kv, kv_dtype, kr + voff);
+  }
+  __syncthreads();
+  for (int i = warp; i < G; i += nw) {
+    const int r = row0 + i;
+    if (r >= R) break;
+    float *qs = Qs + warp * dh;
+    for (int c = lane; c < dh; c += 32) qs[c] = load_f(q, q_dtype, (size_t)r * ldq + qoff + h * dh + c);
+    __syncwarp();
+    WarpSoftmax st;
+    st.init();
+    for (int k0 = 0; k0 < len; k0 += 32) {
+      const int j = k0 + lane;
+      float s = -INFINITY;
+      if (j < len) {
+        const float *kr = Ks + j * ldk;
+        float a = 0.f;
+        for (int c = 0; c < dh; ++c) a = fmaf(qs[c], kr[c], a);
+        s = a * scale;
+      }
+      const float cmax = warp_max(s);
+      const float mnew = fmaxf(st.m, cmax);
+      const float corr = st.m == -INFINITY ? 0.f : expf(st.m - mnew);
+      const float p = s == -INFINITY ? 0.f : expf(s - mnew);
+      st.l = st.l * corr + warp_sum(p);
+#pragma unroll
+      for (int jj = 0; jj < MAX_DH / 32; ++jj) st.o[jj] *= corr;
+      st.m = mnew;
+      const int nk = min(32, len - k0);
+      for (int k = 0; k < nk; ++k) {
+        const float pk = __shfl_sync(0xffffffffu, p, k);
+        const float *vr = Vs + (k0 + k) * ldk;
+#pragma unroll
+        for (int jj = 0; jj < MAX_DH / 32; ++jj) {
+          const int c = lane + 32 * jj;
+          if (c < dh) st.o[jj] = fmaf(pk, vr[c], st.o[jj]);
+        }
+      }
+    }
+    write_ctx(st, ctx, ctx_dtype, (size_t)r * ldc + h * dh, dh, lane);
+    __syncwarp();
+  }
+}
+
+// ------------------------------- decoder self-attention, vectorised (bf16)
+// One warp per (row, head); LPK = DH/8 lanes cooperate on one cached
+// position (each lane moves one 16-byte uint4 = 8 bf16 of K or V), so a warp
+// reads 32/LPK full 128-byte rows per instruction.  Positions p < t come
+// from slot anc[t&1][r][p]; the new k/v are written to slot (r, t) first.
+// grid (ceil(R/4), H): the 4 warps of a CTA are 4 consecutive rows of one
+// head — beam rows of a sentence share ancestor slots, which then hit L1.
+template <int DH>
+__global__ void __launch_bounds__(128) k_self_attn_vec(
+    int R, int H, const void *qkv, int ld_qkv, int qkv_dtype, __nv_bfloat16 *kc,
+    __nv_bfloat16 *vc, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
+    int ctx_dtype) {
+  constexpr int LPK = DH / 8;      // lanes per key row
+  constexpr int KPI = 32 / LPK;    // keys per warp instruction
+  constexpr int ITER = 32 / KPI;   // = LPK instructions per 32-position chunk
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 4 + warp, h = blockIdx.y;
+  if (r >= R) return;
+  const int D = H * DH;
+  const int t = *step;
+  const int sub = lane % LPK, grp = lane / LPK;
+  // q (8 dims per lane) and this step's k, v
+  float q8[8];
+  {
+    const size_t base = (size_t)r * ld_qkv + h * DH + sub * 8;
+    const size_t cslot = ((size_t)r * S_max + t) * D + h * DH + sub * 8;
+    if (qkv_dtype == SKB_BF16) {
+      const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(qkv);
+      const uint4 qv = *reinterpret_cast<const uint4 *>(src + base);
+      const __nv_bfloat162 *qp = reinterpret_cast<const __nv_bfloat162 *>(&qv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(qp[u]);
+        q8[2 * u] = f.x;
+        q8[2 * u + 1] = f.y;
+      }
+      if (grp == 0) {
+        *reinterpret_cast<uint4 *>(kc + cslot) = *reinterpret_cast<const uint4 *>(src + base + D);
+        *reinterpret_cast<uint4 *>(vc + cslot) = *reinterpret_cast<const uint4 *>(src + base + 2 * D);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q8[u] = load_f(qkv, qkv_dtype, base + u);
+      if (grp == 0)
+        for (int u = 0; u < 8; ++u) {
+          kc[cslot + u] = __float2bfloat16_rn(load_f(qkv, qkv_dtype, base + D + u));
+          vc[cslot + u] = __float2bfloat16_rn(load_f(qkv, qkv_dtype, base + 2 * D + u));
+        }
+    }
+  }
+  __threadfence_block();
+  __syncwarp();
+  const int *arow = anc + ((size_t)(t & 1) * R + r) * S_max;
+  float m_run = -INFINITY, l_run = 0.f;
+  float o8[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) o8[u] = 0.f;
+  for (int p0 = 0; p0 <= t; p0 += 32) {
+    size_t off[ITER];
+    float sc[ITER];
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int p = p0 + it * KPI + grp;
+      off[it] = (size_t)-1;
+      if (p <= t) {
+        const int slot = p == t ? r : __ldg(arow + p);
+        off[it] = ((size_t)slot * S_max + p) * D + h * DH + sub * 8;
+      }
+    }
+    uint4 kv4[ITER];
+#pragma unroll
+    for (int it = 0; it < ITER; ++it)
+      kv4[it] = off[it] != (size_t)-1 ? *reinterpret_cast<const uint4 *>(kc + off[it])
+                                      : make_uint4(0, 0, 0, 0);
+    float cmax = -INFINITY;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kv4[it]);
+      float a = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(kp[u]);
+        a = fmaf(q8[2 * u], f.x, a);
+        a = fmaf(q8[2 * u + 1], f.y, a);
+      }
+#pragma unroll
+      for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      sc[it] = off[it] != (size_t)-1 ? a * scale : -INFINITY;
+      cmax = fmaxf(cmax, sc[it]);
+    }
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    const float mnew = fmaxf(m_run, cmax);
+    const float corr = m_run == -INFINITY ? 0.f : expf(m_run - mnew);
+    float psum = 0.f;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      sc[it] = sc[it] == -INFINITY ? 0.f : expf(sc[it] - mnew);
+      psum += sc[it];
+    }
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+    l_run = l_run * corr + psum;
+    m_run = mnew;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o8[u] *= corr;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it)
+      kv4[it] = off[it] != (size_t)-1 ? *reinterpret_cast<const uint4 *>(vc + off[it])
+                                      : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&kv4[it]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(vp[u]);
+        o8[2 * u] = fmaf(sc[it], f.x, o8[2 * u]);
+        o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
+      }
+    }
+  }
+  // reduce the KPI key groups; lanes of group 0 own the output
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) o8[u] += __shfl_xor_sync(0xffffffffu, o8[u], o);
+  if (grp == 0) {
+    const float inv = 1.0f / l_run;
+    const size_t ob = (size_t)r * ldc + h * DH + sub * 8;
+    if (ctx_dtype == SKB_BF16) {
+      uint4 w;
+      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        __nv_bfloat162 pr = __floats2bfloat162_rn(o8[2 * u] * inv, o8[2 * u + 1] * inv);
+        wp[u] = *reinterpret_cast<uint32_t *>(&pr);
+      }
+      *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(ctx) + ob) = w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) reinterpret_cast<float *>(ctx)[ob + u] = o8[u] * inv;
+    }
+  }
+}
+
 static float attn_scale(int dh) { return (float)(1.0 / sqrt((double)dh)); }
 
 }  // namespace skb
@@ -222,6 +437,24 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
                                      int ctx_dtype, void *stream) {
   if (B <= 0 || L <= 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "encoder_attention: shape");
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "encoder_attention: head dim %d > %d", dh, MAX_DH);
+  {
+    const int nw = L < 8 ? L : 8;
+    const size_t smem = ((size_t)2 * L * (dh + 1) + (size_t)nw * dh) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_attn_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      const int D = H * dh;
+      dim3 g2(B, H);
+      k_attn_smem<<<g2, 32 * nw, smem, as_stream(stream)>>>(
+          B * L, L, H, dh, qkv, ld_qkv, qkv_dtype, 0, qkv, ld_qkv, qkv_dtype, D, 2 * D, L, nullptr,
+          lengths, attn_scale(dh), ctx, ldc, ctx_dtype);
+      SKB_CHECK_LAUNCH("k_attn_smem(encoder)");
+      return SKB_OK;
+    }
+  }
   dim3 grid(B * H, (L + 7) / 8);
   k_encoder_attention<<<grid, 256, 0, as_stream(stream)>>>(B, L, H, dh, qkv, ld_qkv, qkv_dtype,
                                                            lengths, attn_scale(dh), ctx, ldc, ctx_dtype);
@@ -236,6 +469,25 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
   if (R < 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "self_attention_step: shape");
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "self_attention_step: head dim %d", dh);
   if (R == 0) return SKB_OK;
+  if (cache_dtype == SKB_BF16 && (dh == 32 || dh == 64 || dh == 128) && ld_qkv % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (reinterpret_cast<uintptr_t>(kc) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(vc) & 15) == 0) {
+    dim3 grid((R + 3) / 4, H);
+    auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
+    auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
+    const float sc = attn_scale(dh);
+    if (dh == 64)
+      k_self_attn_vec<64><<<grid, 128, 0, as_stream(stream)>>>(R, H, qkv, ld_qkv, qkv_dtype, k, v,
+                                                               S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+    else if (dh == 32)
+      k_self_attn_vec<32><<<grid, 128, 0, as_stream(stream)>>>(R, H, qkv, ld_qkv, qkv_dtype, k, v,
+                                                               S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+    else
+      k_self_attn_vec<128><<<grid, 128, 0, as_stream(stream)>>>(R, H, qkv, ld_qkv, qkv_dtype, k, v,
+                                                                S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+    SKB_CHECK_LAUNCH("k_self_attn_vec");
+    return SKB_OK;
+  }
   const int warps = R * H;
   k_self_attention_step<<<(warps + 3) / 4, 128, 0, as_stream(stream)>>>(
       R, H, dh, qkv, ld_qkv, qkv_dtype, kc, vc, cache_dtype, S_max, anc, step, attn_scale(dh), ctx,
@@ -246,11 +498,31 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
 
 extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int ldq, int q_dtype,
                                         const void *kv, int ld_kv, int kv_dtype, int koff, int voff,
-                                        int L, const int *row_sent, const int *lengths, void *ctx,
-                                        int ldc, int ctx_dtype, void *stream) {
+                                        int L, const int *row_sent, const int *lengths,
+                                        int rows_per_group, void *ctx, int ldc, int ctx_dtype,
+                                        void *stream) {
   if (R < 0 || H <= 0 || dh <= 0 || L <= 0) return fail(SKB_ERR_SHAPE, "cross_attention_step: shape");
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "cross_attention_step: head dim %d", dh);
   if (R == 0) return SKB_OK;
+  const int G = rows_per_group > 0 ? rows_per_group : 1;
+  {
+    const int nw = G < 8 ? G : 8;
+    const size_t smem = ((size_t)2 * L * (dh + 1) + (size_t)nw * dh) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_attn_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      dim3 g2((R + G - 1) / G, H);
+      k_attn_smem<<<g2, 32 * nw, smem, as_stream(stream)>>>(R, G, H, dh, q, ldq, q_dtype, 0, kv,
+                                                            ld_kv, kv_dtype, koff, voff, L, row_sent,
+                                                            lengths, attn_scale(dh), ctx, ldc,
+                                                            ctx_dtype);
+      SKB_CHECK_LAUNCH("k_attn_smem(cross)");
+      return SKB_OK;
+    }
+  }
   const int warps = R * H;
   k_cross_attention_step<<<(warps + 3) / 4, 128, 0, as_stream(stream)>>>(
       R, H, dh, q, ldq, q_dtype, kv, ld_kv, kv_dtype, koff, voff, L, row_sent, lengths,

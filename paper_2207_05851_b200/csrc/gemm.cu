@@ -32,7 +32,32 @@ struct EpiArgs {
   int ld_state;
   const int *step;
   long long state_stride;
+  float *lse_part;
+  int lse_ld;
+  const unsigned *mask;
+  int mask_words;
+  int rows_per_group;
 };
+
+// Partial log-softmax statistics of `cnt` consecutive logits of row m
+// starting at column n (a 32-column group): (max, sum exp(x - max)) over the
+// row's active columns.  Empty groups give (-inf, 0).
+__device__ __forceinline__ float2 group_stats(const EpiArgs &e, int m, int n, int N,
+                                              const float *v, int cnt) {
+  const unsigned *mrow = e.mask ? e.mask + (size_t)(m / e.rows_per_group) * e.mask_words : nullptr;
+  float mx = -INFINITY;
+  for (int q = 0; q < cnt; ++q) {
+    const int c = n + q;
+    if (c < N && (!mrow || ((mrow[c >> 5] >> (c & 31)) & 1u))) mx = fmaxf(mx, v[q]);
+  }
+  float s = 0.f;
+  if (mx != -INFINITY)
+    for (int q = 0; q < cnt; ++q) {
+      const int c = n + q;
+      if (c < N && (!mrow || ((mrow[c >> 5] >> (c & 31)) & 1u))) s += expf(v[q] - mx);
+    }
+  return make_float2(mx, s);
+}
 
 // Apply the epilogue to `cnt` consecutive accumulator columns n..n+cnt-1 of
 // row m (cnt even, n even for SSRU).  v holds the raw fp32 accumulators.
@@ -75,7 +100,7 @@ __device__ __forceinline__ void epilogue_run(const EpiArgs &e, int m, int n, int
     return;
   }
   const bool relu = e.kind == SKB_EPI_RELU;
-  if (e.out_dtype == SKB_F32) {
+  if (e.out_dtype == SKB_F32 || e.kind == SKB_EPI_LOGITS) {
     float *o = reinterpret_cast<float *>(e.out) + (size_t)m * e.ldo;
     for (int q = 0; q < cnt; ++q) {
       const int nn = n + q;
@@ -98,6 +123,13 @@ __device__ __forceinline__ void epilogue_run(const EpiArgs &e, int m, int n, int
 // the tcgen05 epilogue when the chunk is in-bounds and 16-byte aligned.
 __device__ __forceinline__ bool epilogue_vec32(const EpiArgs &e, int m, int n, float *v) {
   if (e.kind == SKB_EPI_SSRU) return false;
+  if (e.kind == SKB_EPI_LOGITS) {
+    float4 *o = reinterpret_cast<float4 *>(reinterpret_cast<float *>(e.out) +
+                                           (size_t)m * e.ldo + n);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return true;
+  }
   if (e.bias) {
 #pragma unroll
     for (int q = 0; q < 32; ++q) v[q] += __ldg(e.bias + n + q);
@@ -327,6 +359,9 @@ __global__ void __launch_bounds__(128, 1)
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
     const int n = n0 + c;
     if (row < M && n < N) {
+      if (ep.kind == SKB_EPI_LOGITS)
+        reinterpret_cast<float2 *>(ep.lse_part)[(size_t)row * ep.lse_ld + (n >> 5)] =
+            group_stats(ep, row, n, N, v, 32);
       if (!(vec_ok && n + 32 <= N && epilogue_vec32(ep, row, n, v)))
         epilogue_run(ep, row, n, N, v, 32);
     }
@@ -470,6 +505,23 @@ __global__ void __launch_bounds__(256) k_gemm_simt(int M, int N, int K, const T 
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + ty * 4 + i;
+    if (ep.kind == SKB_EPI_LOGITS) {
+      // group = 8 consecutive tx (32 columns); combine the 8 (max, sum) pairs
+      float2 st = m < M ? group_stats(ep, m, n0 + tx * 4, N, acc[i], 4)
+                        : make_float2(-INFINITY, 0.f);
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, st.x, o);
+        const float os = __shfl_xor_sync(0xffffffffu, st.y, o);
+        const float nm = fmaxf(st.x, om);
+        float ns = 0.f;
+        if (nm != -INFINITY) ns = st.y * expf(st.x - nm) + os * expf(om - nm);
+        st = make_float2(nm, ns);
+      }
+      const int n = n0 + tx * 4;
+      if (m < M && (tx & 7) == 0 && n < N)
+        reinterpret_cast<float2 *>(ep.lse_part)[(size_t)m * ep.lse_ld + (n >> 5)] = st;
+    }
     if (m < M) epilogue_run(ep, m, n0 + tx * 4, N, acc[i], 4);
   }
 }
@@ -487,6 +539,11 @@ static EpiArgs to_args(const skb_epilogue *e) {
   a.ld_state = e->ld_state;
   a.step = e->step;
   a.state_stride = e->state_stride;
+  a.lse_part = e->lse_part;
+  a.lse_ld = e->lse_ld;
+  a.mask = e->mask;
+  a.mask_words = e->mask_words;
+  a.rows_per_group = e->rows_per_group > 0 ? e->rows_per_group : 1;
   return a;
 }
 
@@ -499,6 +556,9 @@ static int check_args(int in_dtype, int M, int N, int K, const void *A, const vo
     return fail(SKB_ERR_CONFIG, "gemm: residual/SSRU target must be fp32");
   if (epi->kind == SKB_EPI_SSRU && (N % 2 != 0 || !epi->c_next))
     return fail(SKB_ERR_CONFIG, "gemm: SSRU needs even N and a cell buffer");
+  if (epi->kind == SKB_EPI_LOGITS && (!epi->lse_part || epi->lse_ld < (N + 31) / 32 ||
+                                      epi->out_dtype != SKB_F32))
+    return fail(SKB_ERR_CONFIG, "gemm: LOGITS needs fp32 out and a partials buffer");
   return SKB_OK;
 }
 

@@ -75,9 +75,34 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
   if (live) {
     const float *row = logits + (size_t)r * ld;
     const unsigned *mask = st.mask ? st.mask + (size_t)b * ((U + 31) >> 5) : nullptr;
-    // ---- pass 1: max over active columns
-    float mx = -INFINITY, lse = 0.f;
-    if (!lp_in) {
+    float mx = 0.f, lse = 0.f;
+    if (!lp_in && st.lse_part) {
+      // ---- fused path: combine the GEMM epilogue's per-32-column partials
+      const float2 *part = reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld;
+      const int G = (U + 31) >> 5;
+      float m = -INFINITY;
+      for (int g = tid; g < G; g += BEAM_THREADS) m = fmaxf(m, part[g].x);
+      m = warp_max(m);
+      if (lane == 0) red_f[warp] = m;
+      __syncthreads();
+      mx = red_f[0];
+      for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red_f[w]);
+      __syncthreads();
+      float s = 0.f;
+      for (int g = tid; g < G; g += BEAM_THREADS) {
+        const float2 p = part[g];
+        if (p.x != -INFINITY) s += p.y * expf(p.x - mx);
+      }
+      s = warp_sum(s);
+      if (lane == 0) red_f[warp] = s;
+      __syncthreads();
+      s = 0.f;
+      for (int w = 0; w < NW; ++w) s += red_f[w];
+      __syncthreads();
+      lse = logf(s);
+    } else if (!lp_in) {
+      // ---- pass 1: max over active columns
+      mx = -INFINITY;
       for (int c = tid; c < U; c += BEAM_THREADS)
         if (col_active(mask, c)) mx = fmaxf(mx, row[c]);
       mx = warp_max(mx);
@@ -103,32 +128,59 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
     const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
     const double s_r = st.score[r];
 
-    // ---- pass 3: first-max column of lp and per-thread top-K of scores
+    // ---- single pass: lp = (x - max) - lse, first-max column, per-thread
+    // top-K of the float64 scores.  A float32 prefilter (lp >= lp of the
+    // list's last entry) skips the float64 work for almost every column;
+    // it is exact because s_r + lp is monotone in lp and columns arrive in
+    // increasing order per thread.
     double tk[MAXK];
     float tl[MAXK];
     int tc[MAXK];
 #pragma unroll
     for (int j = 0; j < MAXK; ++j) {
       tk[j] = -DBL_MAX;
-      tl[j] = 0.f;
+      tl[j] = -INFINITY;
       tc[j] = INT_MAX;
     }
     float amax = -INFINITY;
     int acol = INT_MAX;
     const bool need_argmax = final_force;
-    if (fcol < 0 || need_argmax) {
-      for (int c = tid; c < U; c += BEAM_THREADS) {
-        if (!col_active(mask, c)) continue;
-        const float x = row[c];
-        const float lp = lp_in ? x : (x - mx) - lse;
-        if (lp > amax) {
-          amax = lp;
-          acol = c;
+    const bool do_topk = fcol < 0;
+    auto visit = [&](int c, float x) {
+      if (mask && !col_active(mask, c)) return;
+      const float lp = lp_in ? x : (x - mx) - lse;
+      if (need_argmax && lp > amax) {
+        amax = lp;
+        acol = c;
+      }
+      if (do_topk && lp >= tl[MAXK - 1]) {
+        const double key = s_r + (double)lp;
+        if (key > tk[MAXK - 1]) list_insert<MAXK>(tk, tl, tc, key, lp, c);
+      }
+    };
+    if (do_topk || need_argmax) {
+      const bool vec = (U & 3) == 0 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+      if (vec) {
+        const float4 *row4 = reinterpret_cast<const float4 *>(row);
+        const int U4 = U >> 2;
+        int c4 = tid;
+        for (; c4 + 3 * BEAM_THREADS < U4; c4 += 4 * BEAM_THREADS) {
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldcs(row4 + c4 + u * BEAM_THREADS);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = 4 * (c4 + u * BEAM_THREADS);
+            visit(c, v[u].x); visit(c + 1, v[u].y); visit(c + 2, v[u].z); visit(c + 3, v[u].w);
+          }
         }
-        if (fcol < 0) {
-          const double key = s_r + (double)lp;
-          if (key > tk[MAXK - 1]) list_insert<MAXK>(tk, tl, tc, key, lp, c);
+        for (; c4 < U4; c4 += BEAM_THREADS) {
+          const float4 v = __ldcs(row4 + c4);
+          const int c = 4 * c4;
+          visit(c, v.x); visit(c + 1, v.y); visit(c + 2, v.z); visit(c + 3, v.w);
         }
+      } else {
+        for (int c = tid; c < U; c += BEAM_THREADS) visit(c, row[c]);
       }
     }
     // first max of lp across the CTA (ties -> lowest column)
@@ -409,8 +461,12 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
   cudaStream_t s = as_stream(stream);
   if (st->K <= 1)
     k_beam_step<1><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  else if (st->K <= 2)
+    k_beam_step<2><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 4)
     k_beam_step<4><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+  else if (st->K <= 5)
+    k_beam_step<5><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 8)
     k_beam_step<8><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 16)

@@ -58,6 +58,10 @@ class StepBuffers:
         self.q = torch.zeros(R, d, device=dev, dtype=cdt)
         self.f = torch.zeros(R, c.ff_dim, device=dev, dtype=cdt)
         self.logits = torch.zeros(R, U, device=dev)
+        # fused log-softmax partials: (max, sum exp) per 32-column group
+        self.lse_part = torch.zeros(R, 2 * ((U + 31) // 32), device=dev)
+        self.mask = None          # [B, words] active-column bits (restricted vocab)
+        self.group = 1            # rows per sentence group (beam size)
         self.fac = torch.zeros(R, int(model.fac_off[-1].item()) if nf else 1, device=dev)
         if c.decoder_kind == SSRU:
             self.cell = torch.zeros(D, 2, R, d, device=dev)
@@ -92,13 +96,14 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
         kern.layernorm(sb.x, *Ly.ln_cross, sb.h)
         kern.gemm(sb.h, Ly.wq_c, sb.q)
         kern.cross_attention_step(sb.q, sb.ckv, li * 2 * d, li * 2 * d + d, sb.L, sb.row_sent,
-                                  sb.lengths, sb.ctx, R, H, dh)
+                                  sb.lengths, sb.ctx, R, H, dh, sb.group)
         kern.gemm(sb.ctx, Ly.wo_c, sb.x, N.EPI_RESID)
         kern.layernorm(sb.x, *Ly.ln_ffn, sb.h)
         kern.gemm(sb.h, Ly.w1, sb.f, N.EPI_RELU, Ly.b1)
         kern.gemm(sb.f, Ly.w2, sb.x, N.EPI_RESID, Ly.b2)
     kern.layernorm(sb.x, *model.ln_final, sb.h)
-    kern.gemm(sb.h, sb.E_out, sb.logits)
+    kern.gemm(sb.h, sb.E_out, sb.logits, N.EPI_LOGITS, lse_part=sb.lse_part, mask=sb.mask,
+              rows_per_group=sb.group)
     if nf:
         kern.gemm(sb.h, model.w_fac, sb.fac, N.EPI_STORE, model.b_fac)
 
@@ -272,6 +277,8 @@ class BeamBatch:
         self.sb = StepBuffers(model, R, B, self.L, S_max, U, E_out, ckv, self.len_d,
                               self.row_sent)
         sb = self.sb
+        sb.group = K
+        sb.mask = self.mask
 
         def z(n, dt=I32):
             return torch.zeros(n, dtype=dt, device=dev)
@@ -308,7 +315,8 @@ class BeamBatch:
             self.done.data_ptr(), self.score.data_ptr(), sb.tok.data_ptr(), sb.ftok.data_ptr(),
             sb.parent.data_ptr(), self.tok_hist.data_ptr(), self.par_hist.data_ptr(),
             self.fac_hist.data_ptr(), sb.fac.data_ptr() if nf else None, sb.fac.stride(0),
-            model.fac_off.data_ptr(), self.cand_score.data_ptr(), self.cand_lp.data_ptr(),
+            model.fac_off.data_ptr(), sb.lse_part.data_ptr(), sb.lse_part.shape[1] // 2,
+            self.cand_score.data_ptr(), self.cand_lp.data_ptr(),
             self.cand_col.data_ptr(), self.cand_cnt.data_ptr(), self.row_argmax.data_ptr(),
             self.fac_choice.data_ptr(), self.counter.data_ptr(), self.best_norm.data_ptr(),
             self.best_logprob.data_ptr(), self.best_steps.data_ptr(),

@@ -33,13 +33,15 @@ def dcode(t: torch.Tensor) -> int:
 
 
 def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_row=None,
-         step=None, state_stride=0, simt=False):
+         step=None, state_stride=0, lse_part=None, mask=None, rows_per_group=1, simt=False):
     """out (or residual x) <- epilogue(A[M,K] . W[N,K]^T)."""
     M = A.shape[0] if M is None else M
     Nn, K = W.shape
     epi = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), out.stride(0), dcode(out), None,
                      N.ptr(c_state), N.ptr(src_row), Nn // 2 if kind == N.EPI_SSRU else 0,
-                     N.ptr(step), state_stride)
+                     N.ptr(step), state_stride, N.ptr(lse_part),
+                     lse_part.shape[1] // 2 if lse_part is not None else 0, N.ptr(mask),
+                     mask.shape[1] if mask is not None else 0, rows_per_group)
     N.call("skb_gemm_simt" if simt else "skb_gemm", dcode(A), M, Nn, K, A.data_ptr(),
            A.stride(0), W.data_ptr(), W.stride(0), C.byref(epi), stream())
     _count()
@@ -84,10 +86,10 @@ def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max):
     _count()
 
 
-def cross_attention_step(q, kv, koff, voff, L, row_sent, lengths, ctx, R, H, dh):
+def cross_attention_step(q, kv, koff, voff, L, row_sent, lengths, ctx, R, H, dh, group=1):
     N.call("skb_cross_attention_step", R, H, dh, q.data_ptr(), q.stride(0), dcode(q),
            kv.data_ptr(), kv.stride(0), dcode(kv), koff, voff, L, row_sent.data_ptr(),
-           lengths.data_ptr(), ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+           lengths.data_ptr(), group, ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
     _count()
 
 

@@ -118,3 +118,42 @@ def test_batch_invariance():
     _run("skb_gemm", N.BF16, A[130:135], W, _epi(N.EPI_STORE, part, 4096, N.F32))
     torch.cuda.synchronize()
     assert torch.equal(full[130:135], part)
+
+
+@pytest.mark.parametrize("fn", ["skb_gemm", "skb_gemm_simt"])
+@pytest.mark.parametrize("M,Nn,K,masked", [(10, 100, 64, False), (640, 32000, 1024, False),
+                                           (12, 1000, 256, True)])
+def test_logits_epilogue_partials(fn, M, Nn, K, masked):
+    """SKB_EPI_LOGITS: fp32 logits + per-32-column (max, sum exp) partials
+    that combine into the row log-sum-exp (kernels.py:287-295)."""
+    g = torch.Generator(device="cuda").manual_seed(4)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
+    out = torch.zeros(M, Nn, device="cuda")
+    G = (Nn + 31) // 32
+    part = torch.zeros(M, 2 * G, device="cuda")
+    words = (Nn + 31) // 32
+    rows_per_group = 3
+    active = torch.rand((M + 2) // 3, Nn, device="cuda", generator=g) < 0.3 if masked else None
+    mask = None
+    if masked:
+        bits = torch.zeros(active.shape[0], words * 32, dtype=torch.int64, device="cuda")
+        bits[:, :Nn] = active.long()
+        weights = (1 << torch.arange(32, device="cuda", dtype=torch.int64))
+        mask = (bits.view(-1, words, 32) * weights).sum(-1)
+        mask = torch.where(mask >= 2 ** 31, mask - 2 ** 32, mask).to(torch.int32).contiguous()
+    epi = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None, 0,
+                     part.data_ptr(), G, N.ptr(mask), words if masked else 0, rows_per_group)
+    _run(fn, N.BF16, A, W, epi)
+    torch.cuda.synchronize()
+    ref = A.double() @ W.double().T
+    assert (out.double() - ref).abs().max().item() <= 2e-3 * K ** 0.5
+    p = part.view(M, G, 2)
+    m = p[..., 0].max(1).values
+    lse = m + torch.log((p[..., 1] * torch.exp(p[..., 0] - m[:, None])).nansum(1))
+    x = out.double()
+    if masked:
+        act = active.repeat_interleave(rows_per_group, 0)[:M]
+        x = torch.where(act, x, torch.tensor(float("-inf"), device="cuda", dtype=torch.float64))
+    want = torch.logsumexp(x, 1)
+    assert (lse.double() - want).abs().max().item() < 1e-4
