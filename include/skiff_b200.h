@@ -73,6 +73,14 @@ typedef struct skb_epilogue {
   const unsigned *mask;
   int mask_words;
   int rows_per_group;
+  /* Optional split-K workspace (caller-owned; NULL disables split-K): fp32  */
+  /* partial tiles and zero-initialised per-tile arrival counters.  Partial  */
+  /* tiles are summed in split order by the last CTA to arrive, so results  */
+  /* are deterministic and independent of scheduling.                       */
+  float *splitk_ws;
+  long long splitk_ws_elems;
+  unsigned *splitk_counters;
+  int splitk_counters_n;
 } skb_epilogue;
 
 /* Library identity / diagnostics */

@@ -26,7 +26,9 @@ class Epilogue(C.Structure):
     _fields_ = [("kind", i32), ("bias", vp), ("out", vp), ("ldo", i32), ("out_dtype", i32),
                 ("c_prev", vp), ("c_next", vp), ("src_row", vp), ("ld_state", i32),
                 ("step", vp), ("state_stride", C.c_longlong), ("lse_part", vp),
-                ("lse_ld", i32), ("mask", vp), ("mask_words", i32), ("rows_per_group", i32)]
+                ("lse_ld", i32), ("mask", vp), ("mask_words", i32), ("rows_per_group", i32),
+                ("splitk_ws", vp), ("splitk_ws_elems", C.c_longlong), ("splitk_counters", vp),
+                ("splitk_counters_n", i32)]
 
 
 class BeamState(C.Structure):

@@ -13,6 +13,14 @@ import torch
 from . import _native as N
 
 launches = 0
+_splitk = None  # (workspace fp32, counters int32) shared by all GEMMs of a device
+
+
+def set_splitk_workspace(ws, counters) -> None:
+    """Split-K scratch for the tcgen05 GEMM (fp32 partial tiles + zeroed
+    per-tile counters).  Calls on one stream may share it."""
+    global _splitk
+    _splitk = (ws, counters)
 
 
 def _count(n: int = 1) -> None:

@@ -80,6 +80,10 @@ class Model:
             N.call("skb_set_device", self.device.index)
         self.cdt = torch.bfloat16 if precision == "bf16" else torch.float32
         self.quantized: dict = {}
+        if precision == "bf16":
+            # split-K scratch of the tcgen05 GEMM: 32 MB of fp32 partial tiles
+            kern.set_splitk_workspace(torch.empty(8 << 20, device=self.device),
+                                      torch.zeros(8192, dtype=torch.int32, device=self.device))
         self._upload(params)
         self.params = params
 

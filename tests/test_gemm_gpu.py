@@ -157,3 +157,37 @@ def test_logits_epilogue_partials(fn, M, Nn, K, masked):
         x = torch.where(act, x, torch.tensor(float("-inf"), device="cuda", dtype=torch.float64))
     want = torch.logsumexp(x, 1)
     assert (lse.double() - want).abs().max().item() < 1e-4
+
+
+def _splitk_epi(kind, out, ldo, dtype, bias=None):
+    ws = torch.empty(8 << 20, device="cuda")
+    cnt = torch.zeros(8192, dtype=torch.int32, device="cuda")
+    e = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), ldo, dtype, None, None, None, 0, None, 0,
+                   None, 0, None, 0, 1, ws.data_ptr(), ws.numel(), cnt.data_ptr(), cnt.numel())
+    e._keep = (ws, cnt)
+    return e
+
+
+@pytest.mark.parametrize("M,Nn,K", [(640, 1024, 4096), (640, 1024, 1024), (5, 1024, 4096),
+                                    (1000, 1024, 2048)])
+def test_splitk_resid_deterministic_and_batch_invariant(M, Nn, K):
+    """Split-K (chosen from (N, K) only) sums partial tiles in split order:
+    bitwise deterministic, and a row's result is independent of M."""
+    g = torch.Generator(device="cuda").manual_seed(8)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    x0 = torch.randn(M, Nn, device="cuda", generator=g)
+    outs = []
+    for _ in range(2):
+        x = x0.clone()
+        _run("skb_gemm", N.BF16, A, W, _splitk_epi(N.EPI_RESID, x, Nn, N.F32, bias))
+        outs.append(x)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    ref = x0.double() + A.double() @ W.double().T + bias.double()
+    assert (outs[0].double() - ref).abs().max().item() <= 2e-3 * K ** 0.5
+    x1 = x0[:1].clone()
+    _run("skb_gemm", N.BF16, A[:1], W, _splitk_epi(N.EPI_RESID, x1, Nn, N.F32, bias))
+    torch.cuda.synchronize()
+    assert torch.equal(x1[0], outs[0][0])

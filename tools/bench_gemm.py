@@ -1,4 +1,5 @@
-"""Time the tcgen05 GEMM on the decode-step shapes (CUDA events)."""
+"""Time the tcgen05 GEMM on the decode-step shapes (CUDA events).
+Run with SKB_GEMM_BN=64|128|256 to force a tile width."""
 import ctypes as C
 import json
 import sys
@@ -8,18 +9,19 @@ import torch
 sys.path.insert(0, ".")
 from paper_2207_05851_b200 import _native as N  # noqa: E402
 
-SHAPES = {"qkv": (640, 3072, 1024), "wo": (640, 1024, 1024), "ffn1": (640, 4096, 1024),
-          "ffn2": (640, 1024, 4096), "out_proj": (640, 32000, 1024), "big": (8192, 8192, 8192)}
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 640
+SHAPES = {"qkv": (M, 3072, 1024), "wo": (M, 1024, 1024), "ffn1": (M, 4096, 1024),
+          "ffn2": (M, 1024, 4096), "out_proj": (M, 32000, 1024), "big": (8192, 8192, 8192)}
 res = {}
-for name, (M, Nn, K) in SHAPES.items():
-    A = torch.randn(M, K, device="cuda").bfloat16()
+for name, (m, Nn, K) in SHAPES.items():
+    A = torch.randn(m, K, device="cuda").bfloat16()
     W = torch.randn(Nn, K, device="cuda").bfloat16()
-    out = torch.zeros(M, Nn, device="cuda")
-    epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.F32, None, None, None, 0)
+    out = torch.zeros(m, Nn, device="cuda")
+    epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.F32)
     st = torch.cuda.current_stream().cuda_stream
 
     def run():
-        N.call("skb_gemm", N.BF16, M, Nn, K, A.data_ptr(), K, W.data_ptr(), K, C.byref(epi), st)
+        N.call("skb_gemm", N.BF16, m, Nn, K, A.data_ptr(), K, W.data_ptr(), K, C.byref(epi), st)
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -33,5 +35,5 @@ for name, (M, Nn, K) in SHAPES.items():
     ms = e0.elapsed_time(e1) / reps
     ref = (A.float() @ W.float().T)
     err = (out - ref).abs().max().item()
-    res[name] = dict(ms=ms, tflops=2 * M * Nn * K / ms / 1e9, err=err)
+    res[name] = dict(ms=round(ms, 4), tflops=round(2 * m * Nn * K / ms / 1e9, 1), err=err)
     print(name, json.dumps(res[name]), flush=True)
