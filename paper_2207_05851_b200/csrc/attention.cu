@@ -233,11 +233,35 @@ __global__ void __launch_bounds__(256) k_attn_smem(
   float *Vs = sm + (size_t)L * ldk;
   float *Qs = Vs + (size_t)L * ldk;  // [nw][dh]
   // ---- stage K/V of (sentence b, head h) in shared memory
-  for (int idx = threadIdx.x; idx < len * dh; idx += blockDim.x) {
-    const int j = idx / dh, c = idx % dh;
-    const size_t kr = (size_t)(b * L + j) * ld_kv + h * dh + c;
-    Ks[j * ldk + c] = load_f(kv, kv_dtype, kr + koff);
-    Vs[j * ldk + c] = load_f(kv, kv_dtype, kr + voff);
+  if (kv_dtype == SKB_BF16 && (dh & 7) == 0 && (ld_kv & 7) == 0 && (koff & 7) == 0 &&
+      (voff & 7) == 0 && (reinterpret_cast<uintptr_t>(kv) & 15) == 0) {
+    // 16-byte loads: 8 bf16 of one K row and the matching V row per thread
+    const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(kv);
+    const int cpr = dh >> 3;
+    for (int idx = threadIdx.x; idx < len * cpr; idx += blockDim.x) {
+      const int j = idx / cpr, c8 = (idx % cpr) * 8;
+      const size_t kr = (size_t)(b * L + j) * ld_kv + h * dh + c8;
+      const uint4 ku = __ldg(reinterpret_cast<const uint4 *>(src + kr + koff));
+      const uint4 vu = __ldg(reinterpret_cast<const uint4 *>(src + kr + voff));
+      const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&ku);
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vu);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 kf = __bfloat1622float2(kp[u]);
+        const float2 vf = __bfloat1622float2(vp[u]);
+        Ks[j * ldk + c8 + 2 * u] = kf.x;
+        Ks[j * ldk + c8 + 2 * u + 1] = kf.y;
+        Vs[j * ldk + c8 + 2 * u] = vf.x;
+        Vs[j * ldk + c8 + 2 * u + 1] = vf.y;
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < len * dh; idx += blockDim.x) {
+      const int j = idx / dh, c = idx % dh;
+      const size_t kr = (size_t)(b * L + j) * ld_kv + h * dh + c;
+      Ks[j * ldk + c] = load_f(kv, kv_dtype, kr + koff);
+      Vs[j * ldk + c] = load_f(kv, kv_dtype, kr + voff);
+    }
   }
   __syncthreads();
   for (int i = warp; i < G; i += nw) {

@@ -68,6 +68,52 @@ __global__ void __launch_bounds__(256) k_layernorm(int rows, int d, const float 
   }
 }
 
+// Register-resident variant for d = NV * 128: one warp per row, each lane
+// holds NV float4 of the row, so x is read from memory exactly once.
+template <int NV>
+__global__ void __launch_bounds__(256) k_layernorm_reg(int rows, const float *__restrict__ x,
+                                                       int ldx, const float *__restrict__ gain,
+                                                       const float *__restrict__ bias, float eps,
+                                                       void *out, int ldo, int out_dtype) {
+  constexpr int d = NV * 128;
+  const int warp = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float4 *xr = reinterpret_cast<const float4 *>(x + (size_t)warp * ldx);
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = xr[lane + 32 * i];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float mu = warp_sum(s) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a = v[i].x - mu, b = v[i].y - mu, e = v[i].z - mu, f = v[i].w - mu;
+    q += (a * a + b * b) + (e * e + f * f);
+  }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / (float)d + eps);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gain);
+  const float4 *b4 = reinterpret_cast<const float4 *>(bias);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c4 = lane + 32 * i;
+    const float4 g = __ldg(g4 + c4), bb = __ldg(b4 + c4);
+    const float o0 = ((v[i].x - mu) * inv) * g.x + bb.x, o1 = ((v[i].y - mu) * inv) * g.y + bb.y;
+    const float o2 = ((v[i].z - mu) * inv) * g.z + bb.z, o3 = ((v[i].w - mu) * inv) * g.w + bb.w;
+    if (out_dtype == SKB_F32) {
+      reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + (size_t)warp * ldo)[c4] =
+          make_float4(o0, o1, o2, o3);
+    } else {
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t *>(&p0);
+      w.y = *reinterpret_cast<uint32_t *>(&p1);
+      reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(out) + (size_t)warp * ldo)[c4] = w;
+    }
+  }
+}
+
 // ------------------------------------------------------- step embedding
 // model.py:399-410 with offset = step (model.py:545-547).
 __global__ void k_embed_target(int rows, int d, const int *__restrict__ tok,
@@ -156,8 +202,21 @@ extern "C" int skb_layernorm(int rows, int d, const float *x, int ldx, const flo
                              void *stream) {
   if (rows < 0 || d <= 0) return fail(SKB_ERR_SHAPE, "layernorm: rows=%d d=%d", rows, d);
   if (rows == 0) return SKB_OK;
-  k_layernorm<<<(rows + 7) / 8, 256, 0, as_stream(stream)>>>(rows, d, x, ldx, gain, bias, eps, out,
-                                                              ldo, out_dtype);
+  const bool aligned = ldx % 4 == 0 && ldo % 4 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out) |
+                         reinterpret_cast<uintptr_t>(gain) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0;
+  const int blocks = (rows + 7) / 8;
+  cudaStream_t s = as_stream(stream);
+  if (aligned && d == 1024)
+    k_layernorm_reg<8><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+  else if (aligned && d == 512)
+    k_layernorm_reg<4><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+  else if (aligned && d == 256)
+    k_layernorm_reg<2><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+  else if (aligned && d == 2048)
+    k_layernorm_reg<16><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+  else
+    k_layernorm<<<blocks, 256, 0, s>>>(rows, d, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   SKB_CHECK_LAUNCH("k_layernorm");
   return SKB_OK;
 }

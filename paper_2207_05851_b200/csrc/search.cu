@@ -332,58 +332,98 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
     is_last = prev == (unsigned)(K - 1);
   }
   __syncthreads();
-  if (!is_last || tid != 0) return;
+  if (!is_last) return;
   __threadfence();
-  st.counter[b] = 0;
-  if (st.done[b]) return;
-
+  __shared__ double m_key[MAXK * MAXK];
+  __shared__ float m_lp[MAXK * MAXK];
+  __shared__ int m_col[MAXK * MAXK];
+  __shared__ int m_cnt[MAXK], m_arg[MAXK];
+  __shared__ double m_s[MAXK];
+  __shared__ int p_q[MAXK], p_c[MAXK], p_tok[MAXK];
+  __shared__ float p_lp[MAXK];
+  __shared__ int n_pick;
   const int base = b * K;
-  const int nalive = st.n_alive[b];
   const int nf = st.n_factors;
-  const int plen = st.prefix_len[b];
-  const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
-  double s_par[32];
-  int head[32];
-  // Other CTAs' row lists are read through L2 (ld.global.cg): they were
-  // written by other SMs during this launch.
-  for (int q = 0; q < nalive; ++q) {
-    s_par[q] = __ldcg(st.score + base + q);
-    head[q] = 0;
+  if (__ldcg(st.done + b)) {
+    if (tid == 0) st.counter[b] = 0;
+    return;
   }
-  int n_new = 0;
-  // parent factor choices must be read before rows are overwritten (they are
-  // per parent row and not modified here), so no copy is needed.
+  const int nalive = __ldcg(st.n_alive + b);
+  // stage every row list of the sentence in shared memory with one parallel
+  // round of L2 reads (they were written by other CTAs of this launch)
+  for (int idx = tid; idx < nalive * K; idx += BEAM_THREADS) {
+    const int q = idx / K, j = idx % K;
+    const size_t g = (size_t)(base + q) * K + j;
+    m_key[q * MAXK + j] = __ldcg(st.cand_score + g);
+    m_lp[q * MAXK + j] = __ldcg(st.cand_lp + g);
+    m_col[q * MAXK + j] = __ldcg(st.cand_col + g);
+  }
+  if (tid < nalive) {
+    m_cnt[tid] = __ldcg(st.cand_cnt + base + tid);
+    m_s[tid] = __ldcg(st.score + base + tid);
+    m_arg[tid] = __ldcg(st.row_argmax + base + tid);
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  // ---- warp 0: K rounds of a warp-wide argmax over the row-list heads in the
+  // exact order (score desc, token asc, parent asc); columns are sorted by
+  // token, so token order is column order.
+  int head = 0;
+  int npk = 0;
   for (int sel = 0; sel < K; ++sel) {
-    int bq = -1;
-    double bk = 0.0;
-    int bc = 0;
-    for (int q = 0; q < nalive; ++q) {
-      const int rr = base + q;
-      if (head[q] >= __ldcg(st.cand_cnt + rr)) continue;
-      const double k = __ldcg(st.cand_score + (size_t)rr * K + head[q]);
-      const int c = __ldcg(st.cand_col + (size_t)rr * K + head[q]);
-      // order (key desc, token asc, parent asc); columns are sorted by token
-      if (bq < 0 || k > bk || (k == bk && c < bc)) {
-        bq = q;
-        bk = k;
-        bc = c;
+    bool has = lane < nalive && head < m_cnt[lane];
+    double bk = has ? m_key[lane * MAXK + head] : 0.0;
+    int bc = has ? m_col[lane * MAXK + head] : 0;
+    int bq = lane;
+    bool bh = has;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+      const bool oh = __shfl_xor_sync(0xffffffffu, (int)bh, o) != 0;
+      const bool take = oh && (!bh || ok > bk || (ok == bk && (oc < bc || (oc == bc && oq < bq))));
+      if (take) {
+        bk = ok;
+        bc = oc;
+        bq = oq;
+        bh = true;
       }
     }
-    if (bq < 0) break;
-    const int rr = base + bq;
-    const float lp = __ldcg(st.cand_lp + (size_t)rr * K + head[bq]);
-    head[bq]++;
-    const double score = s_par[bq] + (double)lp;
-    const int token = st.col_token ? st.col_token[bc] : bc;
+    if (!bh) break;
+    if (lane == bq) {
+      p_q[sel] = bq;
+      p_c[sel] = bc;
+      p_lp[sel] = m_lp[lane * MAXK + head];
+      p_tok[sel] = st.col_token ? st.col_token[bc] : bc;
+      ++head;
+    }
+    npk = sel + 1;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  // ---- sequential routing of the picks (search.py:370-386) from shared memory
+  const int plen = st.prefix_len[b];
+  const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
+  const int steps = t + 1;
+  const double pen = st.len_pen[steps];
+  int best_steps = st.best_steps[b];
+  double best_norm = st.best_norm[b];
+  int n_new = 0;
+  for (int sel = 0; sel < npk; ++sel) {
+    const int q = p_q[sel], c = p_c[sel], token = p_tok[sel];
+    const int rr = base + q;
+    const double score = m_s[q] + (double)p_lp[sel];
     if (token == EOS) {
-      const int steps = t + 1;
-      const double norm = score / st.len_pen[steps];
-      if (st.best_steps[b] == 0 || norm > st.best_norm[b]) {
+      const double norm = score / pen;
+      if (best_steps == 0 || norm > best_norm) {
+        best_norm = norm;
+        best_steps = steps;
         st.best_norm[b] = norm;
         st.best_logprob[b] = score;
         st.best_steps[b] = steps;
-        st.best_forced[b] = final_force && __ldcg(st.row_argmax + rr) != bc;
-        st.best_parent[b] = bq;
+        st.best_forced[b] = final_force && m_arg[q] != c;
+        st.best_parent[b] = q;
         for (int k = 0; k < nf; ++k)
           st.best_fac[(size_t)b * nf + k] = __ldcg(st.fac_choice + (size_t)rr * nf + k);
       }
@@ -393,7 +433,7 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
       st.parent[slot] = rr;
       st.score[slot] = score;
       st.tok_hist[(size_t)t * R + slot] = token;
-      st.par_hist[(size_t)t * R + slot] = bq;
+      st.par_hist[(size_t)t * R + slot] = q;
       for (int k = 0; k < nf; ++k) {
         const int f = __ldcg(st.fac_choice + (size_t)rr * nf + k);
         st.ftok_next[(size_t)k * R + slot] = f;
@@ -408,10 +448,12 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
     for (int k = 0; k < nf; ++k) st.ftok_next[(size_t)k * R + base + q] = PAD;
   }
   st.n_alive[b] = n_new;
+  st.counter[b] = 0;
   if (n_new == 0) {
     st.done[b] = 1;
     atomicAdd(st.n_done, 1);
   }
+  (void)n_pick;
 }
 
 // ------------------------------------------------------------- reorder
