@@ -207,6 +207,8 @@ typedef struct skb_beam_state {
   const float *lse_part;  /* [R, lse_ld] float2 partials from SKB_EPI_LOGITS  */
                           /* (NULL: the step kernel reduces the row itself)  */
   int lse_ld;
+  int prune;              /* 1: read only the 32-column groups whose partial  */
+                          /* max can reach the top K (exact, see search.cu)  */
   /* scratch */
   double *cand_score;     /* [R, K] */
   float *cand_lp;         /* [R, K] */

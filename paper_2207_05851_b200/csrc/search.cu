@@ -53,6 +53,47 @@ __device__ __forceinline__ void list_insert(double (&k)[MAXK], float (&l)[MAXK],
   }
 }
 
+
+// K-th largest of the values held by a CTA (each thread passes its values
+// through `feed`); K <= MAXK.  Exact; used to bound the beam threshold from
+// the per-32-column group maxima the output GEMM wrote.
+template <int MAXK>
+__device__ __forceinline__ void warp_topk_vals(float (&v)[MAXK], int K, float *out_warp) {
+  // v sorted descending per lane; K rounds of warp max with pop-one
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < K; ++j) {
+    float b = v[0];
+    int bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ob > b || (ob == b && ol < bl)) {
+        b = ob;
+        bl = ol;
+      }
+    }
+    if (lane == 0) out_warp[j] = b;
+    if (lane == bl) {
+#pragma unroll
+      for (int q = 0; q + 1 < MAXK; ++q) v[q] = v[q + 1];
+      v[MAXK - 1] = -INFINITY;
+    }
+  }
+}
+
+template <int MAXK>
+__device__ __forceinline__ void vals_insert(float (&v)[MAXK], float x) {
+  v[MAXK - 1] = x;
+#pragma unroll
+  for (int j = MAXK - 1; j > 0; --j)
+    if (v[j] > v[j - 1]) {
+      const float t = v[j];
+      v[j] = v[j - 1];
+      v[j - 1] = t;
+    }
+}
+
 template <int MAXK>
 __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restrict__ logits,
                                                             int ld, int lp_in, skb_beam_state st) {
@@ -158,7 +199,59 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
         if (key > tk[MAXK - 1]) list_insert<MAXK>(tk, tl, tc, key, lp, c);
       }
     };
-    if (do_topk || need_argmax) {
+    const bool pruned = !lp_in && st.lse_part != nullptr && st.prune;
+    if (pruned && (do_topk || need_argmax)) {
+      // ---- pruned scan: only 32-column groups whose maximum logit can reach
+      // the top K are read.  T = K-th largest group maximum <= K-th largest
+      // logit, and lp / the float64 key are monotone in x, so every column
+      // that can enter the top K by (key desc, col asc) has
+      // x >= T - delta, delta covering the float32 rounding of
+      // (x - max) - lse and the float64 rounding of s_r + lp (so exact
+      // ties are never lost).  At the final step the first-max column of lp
+      // is searched the same way around the row maximum.
+      __shared__ float wtop[NW][MAXK];
+      __shared__ float thr_s;
+      const float2 *part = reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld;
+      const int G = (U + 31) >> 5;
+      float thr_top = INFINITY;
+      if (do_topk) {
+        float gv[MAXK];
+#pragma unroll
+        for (int j = 0; j < MAXK; ++j) gv[j] = -INFINITY;
+        for (int g = tid; g < G; g += BEAM_THREADS) {
+          const float v = part[g].x;
+          if (v > gv[MAXK - 1]) vals_insert<MAXK>(gv, v);
+        }
+        const int kk = K < MAXK ? K : MAXK;
+        warp_topk_vals<MAXK>(gv, kk, wtop[warp]);
+        __syncthreads();
+        if (warp == 0) {
+          float w[MAXK];
+#pragma unroll
+          for (int j = 0; j < MAXK; ++j) w[j] = (lane < NW && j < kk) ? wtop[lane][j] : -INFINITY;
+          __shared__ float fin[MAXK];
+          warp_topk_vals<MAXK>(w, kk, fin);
+          __syncwarp();
+          if (lane == 0) {
+            const float T = fin[kk - 1];
+            const float delta = 4e-6f * (fabsf(T) + fabsf(mx) + fabsf(lse) + 1.0f) +
+                                (float)(1e-15 * (fabs(s_r) + 1.0));
+            thr_s = T == -INFINITY ? -INFINITY : T - delta;
+          }
+        }
+        __syncthreads();
+        thr_top = thr_s;
+      }
+      const float thr_arg =
+          need_argmax ? mx - 4e-6f * (2.0f * fabsf(mx) + fabsf(lse) + 1.0f) : INFINITY;
+      const float thr = fminf(thr_top, thr_arg);
+      for (int g = tid; g < G; g += BEAM_THREADS) {
+        if (!(part[g].x >= thr)) continue;
+        const int c0 = g << 5;
+        const int c1 = min(U, c0 + 32);
+        for (int c = c0; c < c1; ++c) visit(c, row[c]);
+      }
+    } else if (do_topk || need_argmax) {
       const bool vec = (U & 3) == 0 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0;
       if (vec) {
         const float4 *row4 = reinterpret_cast<const float4 *>(row);
