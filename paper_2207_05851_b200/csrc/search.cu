@@ -19,7 +19,6 @@
 
 namespace skb {
 
-constexpr int BEAM_THREADS = 256;
 constexpr int EOS = 3, PAD = 0;
 
 struct Cand {
@@ -94,86 +93,107 @@ __device__ __forceinline__ void vals_insert(float (&v)[MAXK], float x) {
     }
 }
 
+// K-th largest value across the warp's per-lane sorted lists (K <= MAXK).
 template <int MAXK>
-__global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restrict__ logits,
-                                                            int ld, int lp_in, skb_beam_state st) {
-  const int r = blockIdx.x;
-  const int K = st.K, U = st.U;
-  const int b = r / K, i = r % K;
-  const int R = st.B * K;
-  const int t = *st.step;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = BEAM_THREADS / 32;
+__device__ __forceinline__ float warp_kth(float (&v)[MAXK], int K) {
+  const int lane = threadIdx.x & 31;
+  float last = -INFINITY;
+  for (int j = 0; j < K; ++j) {
+    float b = v[0];
+    int bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ob > b || (ob == b && ol < bl)) {
+        b = ob;
+        bl = ol;
+      }
+    }
+    last = b;
+    if (lane == bl) {
+#pragma unroll
+      for (int q = 0; q + 1 < MAXK; ++q) v[q] = v[q + 1];
+      v[MAXK - 1] = -INFINITY;
+    }
+  }
+  return last;
+}
 
-  __shared__ float red_f[NW];
-  __shared__ int red_i[NW];
-  __shared__ double wk[NW][MAXK];
-  __shared__ float wl[NW][MAXK];
-  __shared__ int wc[NW][MAXK];
-  __shared__ int is_last;
+constexpr int BEAM_WARPS = 8;  // rows per CTA (one warp per row)
+
+// One warp per row slot r = b*K + i (no block barriers).  See the file
+// header for the algorithm; the per-row phases are:
+//   1. log-softmax statistics: combine the output GEMM's per-32-column
+//      (max, sum exp) partials, or reduce the row itself;
+//   2. candidate columns: with partials, only 32-column groups whose max can
+//      reach the top K (exact pruning, margin covers fp32/fp64 rounding);
+//      otherwise every active column;
+//   3. per-lane top-K of float64 keys s_r + lp (first-max argmax of lp at the
+//      final step), merged across the warp with shuffles;
+//   4. the last row of a sentence to arrive merges the <= K row lists in
+//      lexsort order and routes EOS / survivors (search.py:363-393).
+template <int MAXK>
+__global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__restrict__ logits,
+                                                               int ld, int lp_in, skb_beam_state st) {
+  extern __shared__ uint8_t beam_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int K = st.K, U = st.U;
+  const int R = st.B * K;
+  const int r = blockIdx.x * BEAM_WARPS + wib;
+  if (r >= R) return;
+  const int b = r / K, i = r % K;
+  const int t = *st.step;
+  const int nf = st.n_factors;
 
   const bool live = !st.done[b] && i < st.n_alive[b];
   if (live) {
     const float *row = logits + (size_t)r * ld;
     const unsigned *mask = st.mask ? st.mask + (size_t)b * ((U + 31) >> 5) : nullptr;
-    float mx = 0.f, lse = 0.f;
-    if (!lp_in && st.lse_part) {
-      // ---- fused path: combine the GEMM epilogue's per-32-column partials
-      const float2 *part = reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld;
-      const int G = (U + 31) >> 5;
-      float m = -INFINITY;
-      for (int g = tid; g < G; g += BEAM_THREADS) m = fmaxf(m, part[g].x);
-      m = warp_max(m);
-      if (lane == 0) red_f[warp] = m;
-      __syncthreads();
-      mx = red_f[0];
-      for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red_f[w]);
-      __syncthreads();
-      float s = 0.f;
-      for (int g = tid; g < G; g += BEAM_THREADS) {
-        const float2 p = part[g];
-        if (p.x != -INFINITY) s += p.y * expf(p.x - mx);
-      }
-      s = warp_sum(s);
-      if (lane == 0) red_f[warp] = s;
-      __syncthreads();
-      s = 0.f;
-      for (int w = 0; w < NW; ++w) s += red_f[w];
-      __syncthreads();
-      lse = logf(s);
-    } else if (!lp_in) {
-      // ---- pass 1: max over active columns
-      mx = -INFINITY;
-      for (int c = tid; c < U; c += BEAM_THREADS)
-        if (col_active(mask, c)) mx = fmaxf(mx, row[c]);
-      mx = warp_max(mx);
-      if (lane == 0) red_f[warp] = mx;
-      __syncthreads();
-      mx = red_f[0];
-      for (int w = 1; w < NW; ++w) mx = fmaxf(mx, red_f[w]);
-      __syncthreads();
-      // ---- pass 2: sum of exp(x - max)
-      float s = 0.f;
-      for (int c = tid; c < U; c += BEAM_THREADS)
-        if (col_active(mask, c)) s += expf(row[c] - mx);
-      s = warp_sum(s);
-      if (lane == 0) red_f[warp] = s;
-      __syncthreads();
-      s = 0.f;
-      for (int w = 0; w < NW; ++w) s += red_f[w];
-      __syncthreads();
-      lse = logf(s);
-    }
     const int plen = st.prefix_len[b];
     const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
     const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
+    const bool do_topk = fcol < 0;
+    const bool need_argmax = final_force;
+    const int kk = K < MAXK ? K : MAXK;
     const double s_r = st.score[r];
+    const bool use_part = !lp_in && st.lse_part != nullptr;
+    const float2 *part = use_part ? reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld
+                                  : nullptr;
+    const int G = (U + 31) >> 5;
 
-    // ---- single pass: lp = (x - max) - lse, first-max column, per-thread
-    // top-K of the float64 scores.  A float32 prefilter (lp >= lp of the
-    // list's last entry) skips the float64 work for almost every column;
-    // it is exact because s_r + lp is monotone in lp and columns arrive in
-    // increasing order per thread.
+    // ---- 1. statistics (and the K-th largest group maximum for pruning)
+    float mx = 0.f, lse = 0.f, T = -INFINITY;
+    if (use_part) {
+      float gv[MAXK];
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j) gv[j] = -INFINITY;
+      float m = -INFINITY;
+      for (int g = lane; g < G; g += 32) {
+        const float v = part[g].x;
+        m = fmaxf(m, v);
+        if (v > gv[MAXK - 1]) vals_insert<MAXK>(gv, v);
+      }
+      mx = warp_max(m);
+      float sum = 0.f;
+      for (int g = lane; g < G; g += 32) {
+        const float2 p = part[g];
+        if (p.x != -INFINITY) sum += p.y * expf(p.x - mx);
+      }
+      lse = logf(warp_sum(sum));
+      if (do_topk) T = warp_kth<MAXK>(gv, kk);
+    } else if (!lp_in) {
+      float m = -INFINITY;
+      for (int c = lane; c < U; c += 32)
+        if (col_active(mask, c)) m = fmaxf(m, row[c]);
+      mx = warp_max(m);
+      float sum = 0.f;
+      for (int c = lane; c < U; c += 32)
+        if (col_active(mask, c)) sum += expf(row[c] - mx);
+      lse = logf(warp_sum(sum));
+    }
+
+    // ---- 2./3. candidates -> per-lane top-K and first-max argmax
     double tk[MAXK];
     float tl[MAXK];
     int tc[MAXK];
@@ -185,8 +205,6 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
     }
     float amax = -INFINITY;
     int acol = INT_MAX;
-    const bool need_argmax = final_force;
-    const bool do_topk = fcol < 0;
     auto visit = [&](int c, float x) {
       if (mask && !col_active(mask, c)) return;
       const float lp = lp_in ? x : (x - mx) - lse;
@@ -199,84 +217,43 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
         if (key > tk[MAXK - 1]) list_insert<MAXK>(tk, tl, tc, key, lp, c);
       }
     };
-    const bool pruned = !lp_in && st.lse_part != nullptr && st.prune;
-    if (pruned && (do_topk || need_argmax)) {
-      // ---- pruned scan: only 32-column groups whose maximum logit can reach
-      // the top K are read.  T = K-th largest group maximum <= K-th largest
-      // logit, and lp / the float64 key are monotone in x, so every column
-      // that can enter the top K by (key desc, col asc) has
-      // x >= T - delta, delta covering the float32 rounding of
-      // (x - max) - lse and the float64 rounding of s_r + lp (so exact
-      // ties are never lost).  At the final step the first-max column of lp
-      // is searched the same way around the row maximum.
-      __shared__ float wtop[NW][MAXK];
-      __shared__ float thr_s;
-      const float2 *part = reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld;
-      const int G = (U + 31) >> 5;
-      float thr_top = INFINITY;
-      if (do_topk) {
-        float gv[MAXK];
-#pragma unroll
-        for (int j = 0; j < MAXK; ++j) gv[j] = -INFINITY;
-        for (int g = tid; g < G; g += BEAM_THREADS) {
-          const float v = part[g].x;
-          if (v > gv[MAXK - 1]) vals_insert<MAXK>(gv, v);
-        }
-        const int kk = K < MAXK ? K : MAXK;
-        warp_topk_vals<MAXK>(gv, kk, wtop[warp]);
-        __syncthreads();
-        if (warp == 0) {
-          float w[MAXK];
-#pragma unroll
-          for (int j = 0; j < MAXK; ++j) w[j] = (lane < NW && j < kk) ? wtop[lane][j] : -INFINITY;
-          __shared__ float fin[MAXK];
-          warp_topk_vals<MAXK>(w, kk, fin);
-          __syncwarp();
-          if (lane == 0) {
-            const float T = fin[kk - 1];
-            const float delta = 4e-6f * (fabsf(T) + fabsf(mx) + fabsf(lse) + 1.0f) +
-                                (float)(1e-15 * (fabs(s_r) + 1.0));
-            thr_s = T == -INFINITY ? -INFINITY : T - delta;
-          }
-        }
-        __syncthreads();
-        thr_top = thr_s;
-      }
+    if (use_part && st.prune && (do_topk || need_argmax)) {
+      // exact pruning: T <= K-th largest logit and lp, s_r + lp are monotone
+      // in x, so every column that can enter the top K by (key desc, col
+      // asc) has x >= T - delta (delta covers the float32 rounding of
+      // (x - max) - lse and the float64 rounding of s_r + lp, so ties are
+      // never lost); the first-max argmax lies within delta of the max.
+      const float thr_top = do_topk ? (T == -INFINITY ? -INFINITY
+                                       : T - (4e-6f * (fabsf(T) + fabsf(mx) + fabsf(lse) + 1.0f) +
+                                              (float)(1e-15 * (fabs(s_r) + 1.0))))
+                                    : INFINITY;
       const float thr_arg =
           need_argmax ? mx - 4e-6f * (2.0f * fabsf(mx) + fabsf(lse) + 1.0f) : INFINITY;
       const float thr = fminf(thr_top, thr_arg);
-      for (int g = tid; g < G; g += BEAM_THREADS) {
-        if (!(part[g].x >= thr)) continue;
-        const int c0 = g << 5;
-        const int c1 = min(U, c0 + 32);
-        for (int c = c0; c < c1; ++c) visit(c, row[c]);
+      for (int g0 = 0; g0 < G; g0 += 32) {
+        const int g = g0 + lane;
+        unsigned cand = __ballot_sync(0xffffffffu, g < G && part[g].x >= thr);
+        while (cand) {
+          const int gg = g0 + __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int c = (gg << 5) + lane;  // lane = column: coalesced 128 B
+          if (c < U) visit(c, __ldcs(row + c));
+        }
       }
     } else if (do_topk || need_argmax) {
       const bool vec = (U & 3) == 0 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0;
       if (vec) {
         const float4 *row4 = reinterpret_cast<const float4 *>(row);
-        const int U4 = U >> 2;
-        int c4 = tid;
-        for (; c4 + 3 * BEAM_THREADS < U4; c4 += 4 * BEAM_THREADS) {
-          float4 v[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) v[u] = __ldcs(row4 + c4 + u * BEAM_THREADS);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = 4 * (c4 + u * BEAM_THREADS);
-            visit(c, v[u].x); visit(c + 1, v[u].y); visit(c + 2, v[u].z); visit(c + 3, v[u].w);
-          }
-        }
-        for (; c4 < U4; c4 += BEAM_THREADS) {
+        for (int c4 = lane; c4 < (U >> 2); c4 += 32) {
           const float4 v = __ldcs(row4 + c4);
           const int c = 4 * c4;
           visit(c, v.x); visit(c + 1, v.y); visit(c + 2, v.z); visit(c + 3, v.w);
         }
       } else {
-        for (int c = tid; c < U; c += BEAM_THREADS) visit(c, row[c]);
+        for (int c = lane; c < U; c += 32) visit(c, row[c]);
       }
     }
-    // first max of lp across the CTA (ties -> lowest column)
+    // first max of lp across the warp (ties -> lowest column)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float oa = __shfl_xor_sync(0xffffffffu, amax, o);
@@ -286,18 +263,23 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
         acol = oc;
       }
     }
-    if (lane == 0) {
-      red_f[warp] = amax;
-      red_i[warp] = acol;
-    }
-    // warp-level merge of the 32 thread lists -> top MAXK per warp
-    if (fcol < 0) {
-      int head = 0;
-      for (int j = 0; j < MAXK; ++j) {
-        double hk = head < MAXK ? tk[0] : -DBL_MAX;
-        int hc = head < MAXK ? tc[0] : INT_MAX;
-        double bk = hk;
-        int bc = hc, bl = lane;
+    if (lane == 0) st.row_argmax[r] = acol;
+    if (!do_topk) {
+      if (lane == 0) {
+        const float x = row[fcol];
+        const float lp = lp_in ? x : (x - mx) - lse;
+        // forced steps: float32 key fl32(fl32(s) + lp) (NEP 50 promotion)
+        const float key32 = (float)s_r + lp;
+        st.cand_score[(size_t)r * K] = (double)key32;
+        st.cand_lp[(size_t)r * K] = lp;
+        st.cand_col[(size_t)r * K] = fcol;
+        st.cand_cnt[r] = 1;
+      }
+    } else {
+      int cnt = 0;
+      for (int j = 0; j < kk; ++j) {
+        double bk = tk[0];
+        int bc = tc[0], bl = lane;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
@@ -310,12 +292,14 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
           }
         }
         const float blp = __shfl_sync(0xffffffffu, tl[0], bl);
+        if (bc == INT_MAX) break;
         if (lane == 0) {
-          wk[warp][j] = bk;
-          wl[warp][j] = blp;
-          wc[warp][j] = bc;
+          st.cand_score[(size_t)r * K + j] = bk;
+          st.cand_lp[(size_t)r * K + j] = blp;
+          st.cand_col[(size_t)r * K + j] = bc;
         }
-        if (lane == bl) {  // pop the head of the winning lane's list
+        ++cnt;
+        if (lane == bl) {
 #pragma unroll
           for (int q = 0; q + 1 < MAXK; ++q) {
             tk[q] = tk[q + 1];
@@ -323,150 +307,86 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
             tc[q] = tc[q + 1];
           }
           tk[MAXK - 1] = -DBL_MAX;
+          tl[MAXK - 1] = -INFINITY;
           tc[MAXK - 1] = INT_MAX;
-          ++head;
         }
       }
+      if (lane == 0) st.cand_cnt[r] = cnt;
     }
-    __syncthreads();
-    if (warp == 0) {
-      // CTA-level first max
-      float a = lane < NW ? red_f[lane] : -INFINITY;
-      int ac = lane < NW ? red_i[lane] : INT_MAX;
+    // factor choices of this row (search.py:261-272): prefix override at
+    // t - 1, else first-max of the factor logits
+    for (int k = 0; k < nf; ++k) {
+      int choice = -1;
+      if (t >= 1 && st.prefix_fac && t - 1 < st.P)
+        choice = st.prefix_fac[((size_t)b * nf + k) * st.P + t - 1];
+      if (choice < 0) {
+        const float *fr = st.fac_logits + (size_t)r * st.fac_ld;
+        const int lo = st.fac_off[k], hi = st.fac_off[k + 1];
+        float bm = -INFINITY;
+        int bcol = INT_MAX;
+        for (int c = lo + lane; c < hi; c += 32)
+          if (fr[c] > bm) {
+            bm = fr[c];
+            bcol = c - lo;
+          }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float oa = __shfl_xor_sync(0xffffffffu, a, o);
-        const int oc = __shfl_xor_sync(0xffffffffu, ac, o);
-        if (oa > a || (oa == a && oc < ac)) {
-          a = oa;
-          ac = oc;
+        for (int o = 16; o > 0; o >>= 1) {
+          const float om = __shfl_xor_sync(0xffffffffu, bm, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bcol, o);
+          if (om > bm || (om == bm && oc < bcol)) {
+            bm = om;
+            bcol = oc;
+          }
         }
+        choice = bcol == INT_MAX ? 0 : bcol;
       }
-      if (lane == 0) st.row_argmax[r] = ac;
-      if (fcol >= 0) {
-        if (lane == 0) {
-          const float x = row[fcol];
-          const float lp = lp_in ? x : (x - mx) - lse;
-          // forced steps: float32 key fl32(fl32(s) + lp) (NEP 50 promotion)
-          const float key32 = (float)s_r + lp;
-          st.cand_score[(size_t)r * K] = (double)key32;
-          st.cand_lp[(size_t)r * K] = lp;
-          st.cand_col[(size_t)r * K] = fcol;
-          st.cand_cnt[r] = 1;
-        }
-      } else {
-        // merge NW warp lists (each sorted) -> top K
-        int head = 0;  // lane w (< NW) walks warp w's list
-        const int kk = K < MAXK ? K : MAXK;
-        for (int j = 0; j < kk; ++j) {
-          const bool has = lane < NW && head < MAXK;
-          double bk = has ? wk[lane][head] : -DBL_MAX;
-          int bc = has ? wc[lane][head] : INT_MAX;
-          const float my_lp = has ? wl[lane][head] : 0.f;
-          int bl = lane;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-            const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-            if (better(ok, oc, bk, bc) || (ok == bk && oc == bc && ol < bl)) {
-              bk = ok;
-              bc = oc;
-              bl = ol;
-            }
-          }
-          const float blp = __shfl_sync(0xffffffffu, my_lp, bl);
-          if (lane == 0) {
-            st.cand_score[(size_t)r * K + j] = bk;
-            st.cand_col[(size_t)r * K + j] = bc;
-            st.cand_lp[(size_t)r * K + j] = blp;
-          }
-          if (lane == bl) ++head;
-        }
-        if (lane == 0) {
-          int cnt = 0;
-          for (int j = 0; j < kk; ++j) cnt += st.cand_col[(size_t)r * K + j] != INT_MAX;
-          st.cand_cnt[r] = cnt;
-        }
-      }
-      // factor choices of this row (search.py:261-272)
-      if (lane == 0) {
-        for (int k = 0; k < st.n_factors; ++k) {
-          int choice = -1;
-          if (t >= 1 && st.prefix_fac) {
-            const int pf = t - 1 < st.P ? st.prefix_fac[((size_t)b * st.n_factors + k) * st.P + t - 1] : -1;
-            choice = pf;
-          }
-          if (choice < 0) {
-            const float *fr = st.fac_logits + (size_t)r * st.fac_ld;
-            const int lo = st.fac_off[k], hi = st.fac_off[k + 1];
-            float bm = -INFINITY;
-            int bcol = 0;
-            for (int c = lo; c < hi; ++c)
-              if (fr[c] > bm) {
-                bm = fr[c];
-                bcol = c - lo;
-              }
-            choice = bcol;
-          }
-          st.fac_choice[(size_t)r * st.n_factors + k] = choice;
-        }
-      }
+      if (lane == 0) st.fac_choice[(size_t)r * nf + k] = choice;
     }
-  } else if (tid == 0) {
+  } else if (lane == 0) {
     st.cand_cnt[r] = 0;
   }
 
-  // ---- arrival: the last row CTA of the sentence does the merge
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&st.counter[b], 1u);
-    is_last = prev == (unsigned)(K - 1);
-  }
-  __syncthreads();
-  if (!is_last) return;
+  // ---- 4. arrival: the last row of the sentence merges
   __threadfence();
-  __shared__ double m_key[MAXK * MAXK];
-  __shared__ float m_lp[MAXK * MAXK];
-  __shared__ int m_col[MAXK * MAXK];
-  __shared__ int m_cnt[MAXK], m_arg[MAXK];
-  __shared__ double m_s[MAXK];
-  __shared__ int p_q[MAXK], p_c[MAXK], p_tok[MAXK];
-  __shared__ float p_lp[MAXK];
-  __shared__ int n_pick;
+  __syncwarp();
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(&st.counter[b], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != (unsigned)(K - 1)) return;
+  __threadfence();
   const int base = b * K;
-  const int nf = st.n_factors;
   if (__ldcg(st.done + b)) {
-    if (tid == 0) st.counter[b] = 0;
+    if (lane == 0) st.counter[b] = 0;
     return;
   }
   const int nalive = __ldcg(st.n_alive + b);
-  // stage every row list of the sentence in shared memory with one parallel
-  // round of L2 reads (they were written by other CTAs of this launch)
-  for (int idx = tid; idx < nalive * K; idx += BEAM_THREADS) {
-    const int q = idx / K, j = idx % K;
-    const size_t g = (size_t)(base + q) * K + j;
-    m_key[q * MAXK + j] = __ldcg(st.cand_score + g);
-    m_lp[q * MAXK + j] = __ldcg(st.cand_lp + g);
-    m_col[q * MAXK + j] = __ldcg(st.cand_col + g);
+  // per-warp staging area: K*K (key, lp, col) + per-row (count, score, argmax)
+  double *m_key = reinterpret_cast<double *>(beam_smem) + (size_t)wib * K * K;
+  float *m_lp = reinterpret_cast<float *>(reinterpret_cast<double *>(beam_smem) + (size_t)BEAM_WARPS * K * K) +
+                (size_t)wib * K * K;
+  int *m_col = reinterpret_cast<int *>(reinterpret_cast<float *>(
+                   reinterpret_cast<double *>(beam_smem) + (size_t)BEAM_WARPS * K * K) +
+               (size_t)BEAM_WARPS * K * K) + (size_t)wib * K * K;
+  for (int idx = lane; idx < nalive * K; idx += 32) {
+    const size_t g = (size_t)base * K + idx;
+    m_key[idx] = __ldcg(st.cand_score + g);
+    m_lp[idx] = __ldcg(st.cand_lp + g);
+    m_col[idx] = __ldcg(st.cand_col + g);
   }
-  if (tid < nalive) {
-    m_cnt[tid] = __ldcg(st.cand_cnt + base + tid);
-    m_s[tid] = __ldcg(st.score + base + tid);
-    m_arg[tid] = __ldcg(st.row_argmax + base + tid);
-  }
-  __syncthreads();
-  if (warp != 0) return;
-  // ---- warp 0: K rounds of a warp-wide argmax over the row-list heads in the
-  // exact order (score desc, token asc, parent asc); columns are sorted by
-  // token, so token order is column order.
+  const int my_cnt = lane < nalive ? __ldcg(st.cand_cnt + base + lane) : 0;
+  const double my_s = lane < nalive ? __ldcg(st.score + base + lane) : 0.0;
+  const int my_arg = lane < nalive ? __ldcg(st.row_argmax + base + lane) : 0;
+  __syncwarp();
+  // K rounds of a warp argmax over the row-list heads in the exact order
+  // (score desc, token asc, parent asc); columns are sorted by token.
   int head = 0;
   int npk = 0;
+  int pick_q = 0, pick_c = 0;  // lane j keeps pick j
+  float pick_lp = 0.f;
   for (int sel = 0; sel < K; ++sel) {
-    bool has = lane < nalive && head < m_cnt[lane];
-    double bk = has ? m_key[lane * MAXK + head] : 0.0;
-    int bc = has ? m_col[lane * MAXK + head] : 0;
+    const bool has = lane < nalive && head < my_cnt;
+    double bk = has ? m_key[lane * K + head] : 0.0;
+    int bc = has ? m_col[lane * K + head] : 0;
     int bq = lane;
     bool bh = has;
 #pragma unroll
@@ -484,69 +404,81 @@ __global__ void __launch_bounds__(BEAM_THREADS) k_beam_step(const float *__restr
       }
     }
     if (!bh) break;
-    if (lane == bq) {
-      p_q[sel] = bq;
-      p_c[sel] = bc;
-      p_lp[sel] = m_lp[lane * MAXK + head];
-      p_tok[sel] = st.col_token ? st.col_token[bc] : bc;
-      ++head;
+    const float plp = __shfl_sync(0xffffffffu, has ? m_lp[lane * K + head] : 0.f, bq);
+    if (lane == sel) {
+      pick_q = bq;
+      pick_c = bc;
+      pick_lp = plp;
     }
+    if (lane == bq) ++head;
     npk = sel + 1;
   }
-  __syncwarp();
-  if (lane != 0) return;
-  // ---- sequential routing of the picks (search.py:370-386) from shared memory
+  // scores and tokens of the picks (lane j = pick j), then sequential routing
+  const double pick_score = __shfl_sync(0xffffffffu, my_s, pick_q) + (double)pick_lp;
+  const int pick_arg = __shfl_sync(0xffffffffu, my_arg, pick_q);
+  const int pick_tok = (lane < npk) ? (st.col_token ? st.col_token[pick_c] : pick_c) : -1;
   const int plen = st.prefix_len[b];
   const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
   const int steps = t + 1;
   const double pen = st.len_pen[steps];
-  int best_steps = st.best_steps[b];
-  double best_norm = st.best_norm[b];
-  int n_new = 0;
-  for (int sel = 0; sel < npk; ++sel) {
-    const int q = p_q[sel], c = p_c[sel], token = p_tok[sel];
-    const int rr = base + q;
-    const double score = m_s[q] + (double)p_lp[sel];
-    if (token == EOS) {
-      const double norm = score / pen;
-      if (best_steps == 0 || norm > best_norm) {
-        best_norm = norm;
-        best_steps = steps;
-        st.best_norm[b] = norm;
-        st.best_logprob[b] = score;
-        st.best_steps[b] = steps;
-        st.best_forced[b] = final_force && m_arg[q] != c;
-        st.best_parent[b] = q;
-        for (int k = 0; k < nf; ++k)
-          st.best_fac[(size_t)b * nf + k] = __ldcg(st.fac_choice + (size_t)rr * nf + k);
-      }
-    } else {
-      const int slot = base + n_new;
-      st.tok_next[slot] = token;
-      st.parent[slot] = rr;
-      st.score[slot] = score;
-      st.tok_hist[(size_t)t * R + slot] = token;
-      st.par_hist[(size_t)t * R + slot] = q;
-      for (int k = 0; k < nf; ++k) {
-        const int f = __ldcg(st.fac_choice + (size_t)rr * nf + k);
-        st.ftok_next[(size_t)k * R + slot] = f;
-        st.fac_hist[((size_t)t * nf + k) * R + slot] = f;
-      }
-      ++n_new;
+  // survivor rank of each pick (exclusive prefix count of non-EOS picks)
+  const unsigned surv = __ballot_sync(0xffffffffu, lane < npk && pick_tok != EOS);
+  const int n_new = __popc(surv);
+  if (lane < npk && pick_tok != EOS) {
+    const int slot = base + __popc(surv & ((1u << lane) - 1u));
+    const int rr = base + pick_q;
+    st.tok_next[slot] = pick_tok;
+    st.parent[slot] = rr;
+    st.score[slot] = pick_score;
+    st.tok_hist[(size_t)t * R + slot] = pick_tok;
+    st.par_hist[(size_t)t * R + slot] = pick_q;
+    for (int k = 0; k < nf; ++k) {
+      const int f = __ldcg(st.fac_choice + (size_t)rr * nf + k);
+      st.ftok_next[(size_t)k * R + slot] = f;
+      st.fac_hist[((size_t)t * nf + k) * R + slot] = f;
     }
   }
-  for (int q = n_new; q < K; ++q) {
-    st.tok_next[base + q] = PAD;
-    st.parent[base + q] = base;
-    for (int k = 0; k < nf; ++k) st.ftok_next[(size_t)k * R + base + q] = PAD;
+  if (lane >= n_new && lane < K) {
+    st.tok_next[base + lane] = PAD;
+    st.parent[base + lane] = base;
+    for (int k = 0; k < nf; ++k) st.ftok_next[(size_t)k * R + base + lane] = PAD;
   }
-  st.n_alive[b] = n_new;
-  st.counter[b] = 0;
-  if (n_new == 0) {
-    st.done[b] = 1;
-    atomicAdd(st.n_done, 1);
+  // finished hypotheses in rank order: the first maximum of logprob/steps^a
+  const unsigned fin = __ballot_sync(0xffffffffu, lane < npk && pick_tok == EOS);
+  if (lane == 0) {
+    st.n_alive[b] = n_new;
+    st.counter[b] = 0;
+    if (n_new == 0) {
+      st.done[b] = 1;
+      atomicAdd(st.n_done, 1);
+    }
   }
-  (void)n_pick;
+  // lanes with EOS picks, processed in rank order by shuffling to lane 0
+  unsigned f = fin;
+  int best_steps = __shfl_sync(0xffffffffu, lane == 0 ? st.best_steps[b] : 0, 0);
+  double best_norm = __shfl_sync(0xffffffffu, lane == 0 ? st.best_norm[b] : 0.0, 0);
+  while (f) {
+    const int j = __ffs(f) - 1;
+    f &= f - 1;
+    const double sc = __shfl_sync(0xffffffffu, pick_score, j);
+    const int q = __shfl_sync(0xffffffffu, pick_q, j);
+    const int c = __shfl_sync(0xffffffffu, pick_c, j);
+    const int ar = __shfl_sync(0xffffffffu, pick_arg, j);
+    const double norm = sc / pen;
+    if (best_steps == 0 || norm > best_norm) {
+      best_steps = steps;
+      best_norm = norm;
+      if (lane == 0) {
+        st.best_norm[b] = norm;
+        st.best_logprob[b] = sc;
+        st.best_steps[b] = steps;
+        st.best_forced[b] = final_force && ar != c;
+        st.best_parent[b] = q;
+        for (int k = 0; k < nf; ++k)
+          st.best_fac[(size_t)b * nf + k] = __ldcg(st.fac_choice + (size_t)(base + q) * nf + k);
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------- reorder
@@ -594,20 +526,29 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
   if (st->K > 32) return fail(SKB_ERR_CONFIG, "beam size %d exceeds 32", st->K);
   const int R = st->B * st->K;
   cudaStream_t s = as_stream(stream);
+  const int grid = (R + BEAM_WARPS - 1) / BEAM_WARPS;
+  const size_t smem = (size_t)BEAM_WARPS * st->K * st->K * (sizeof(double) + sizeof(float) + sizeof(int));
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_beam_step<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+  }
   if (st->K <= 1)
-    k_beam_step<1><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<1><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 2)
-    k_beam_step<2><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<2><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 4)
-    k_beam_step<4><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<4><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 5)
-    k_beam_step<5><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<5><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 8)
-    k_beam_step<8><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<8><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   else if (st->K <= 16)
-    k_beam_step<16><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<16><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   else
-    k_beam_step<32><<<R, BEAM_THREADS, 0, s>>>(logits, ld_logits, lp_in, *st);
+    k_beam_step<32><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
   SKB_CHECK_LAUNCH("k_beam_step");
   return SKB_OK;
 }
