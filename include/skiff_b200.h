@@ -209,6 +209,7 @@ typedef struct skb_beam_state {
   int lse_ld;
   int prune;              /* 1: read only the 32-column groups whose partial  */
                           /* max can reach the top K (exact, see search.cu)  */
+  int stage_partials;     /* set by the library (shared-memory staging)      */
   /* scratch */
   double *cand_score;     /* [R, K] */
   float *cand_lp;         /* [R, K] */

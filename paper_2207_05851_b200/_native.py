@@ -39,6 +39,7 @@ class BeamState(C.Structure):
                 ("tok_next", vp), ("ftok_next", vp), ("parent", vp),
                 ("tok_hist", vp), ("par_hist", vp), ("fac_hist", vp), ("fac_logits", vp),
                 ("fac_ld", i32), ("fac_off", vp), ("lse_part", vp), ("lse_ld", i32), ("prune", i32),
+                ("stage_partials", i32),
                 ("cand_score", vp), ("cand_lp", vp),
                 ("cand_col", vp), ("cand_cnt", vp), ("row_argmax", vp), ("fac_choice", vp),
                 ("counter", vp), ("best_norm", vp), ("best_logprob", vp), ("best_steps", vp),

@@ -120,51 +120,82 @@ __device__ __forceinline__ float warp_kth(float (&v)[MAXK], int K) {
   return last;
 }
 
-constexpr int BEAM_WARPS = 8;  // rows per CTA (one warp per row)
+// Shared-memory layout of one sentence CTA (K warps).
+template <int MAXK>
+struct BeamSmem {
+  double key[MAXK][MAXK];   // row lists (row, rank)
+  float lp[MAXK][MAXK];
+  int col[MAXK][MAXK];
+  int cnt[MAXK];
+  int arg[MAXK];
+  int cg[MAXK][64];         // per-warp candidate group list
+};
 
-// One warp per row slot r = b*K + i (no block barriers).  See the file
-// header for the algorithm; the per-row phases are:
+// One CTA per sentence, one warp per beam row (slot r = b*K + i); the rows
+// exchange their candidate lists through shared memory (one barrier), so
+// there are no global atomics or fences.  Per row:
 //   1. log-softmax statistics: combine the output GEMM's per-32-column
-//      (max, sum exp) partials, or reduce the row itself;
+//      (max, sum exp) partials (staged in shared memory), or reduce the row;
 //   2. candidate columns: with partials, only 32-column groups whose max can
-//      reach the top K (exact pruning, margin covers fp32/fp64 rounding);
-//      otherwise every active column;
+//      reach the top K (exact pruning: the margin covers the fp32 rounding
+//      of (x - max) - lse and the fp64 rounding of s_r + lp, so ties are
+//      never lost); otherwise every active column;
 //   3. per-lane top-K of float64 keys s_r + lp (first-max argmax of lp at the
 //      final step), merged across the warp with shuffles;
-//   4. the last row of a sentence to arrive merges the <= K row lists in
-//      lexsort order and routes EOS / survivors (search.py:363-393).
+// then warp 0 merges the <= K row lists in lexsort order (score desc, token
+// asc, parent asc) and routes EOS / survivors (search.py:363-393).
 template <int MAXK>
-__global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__restrict__ logits,
-                                                               int ld, int lp_in, skb_beam_state st) {
-  extern __shared__ uint8_t beam_smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+__global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict__ logits, int ld,
+                                                          int lp_in, skb_beam_state st) {
+  extern __shared__ __align__(16) uint8_t beam_smem[];
+  BeamSmem<MAXK> &sm = *reinterpret_cast<BeamSmem<MAXK> *>(beam_smem);
+  float2 *part_s = reinterpret_cast<float2 *>(beam_smem + sizeof(BeamSmem<MAXK>));
+  const int lane = threadIdx.x & 31, i = threadIdx.x >> 5;
   const int K = st.K, U = st.U;
   const int R = st.B * K;
-  const int r = blockIdx.x * BEAM_WARPS + wib;
-  if (r >= R) return;
-  const int b = r / K, i = r % K;
+  const int b = blockIdx.x;
+  const int r = b * K + i;
   const int t = *st.step;
   const int nf = st.n_factors;
+  const int G = (U + 31) >> 5;
+  if (st.done[b]) return;
+  const int nalive = st.n_alive[b];
+  const int plen = st.prefix_len[b];
+  const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
+  const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
 
-  const bool live = !st.done[b] && i < st.n_alive[b];
-  if (live) {
+  if (i < nalive) {
     const float *row = logits + (size_t)r * ld;
     const unsigned *mask = st.mask ? st.mask + (size_t)b * ((U + 31) >> 5) : nullptr;
-    const int plen = st.prefix_len[b];
-    const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
-    const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
     const bool do_topk = fcol < 0;
     const bool need_argmax = final_force;
     const int kk = K < MAXK ? K : MAXK;
     const double s_r = st.score[r];
     const bool use_part = !lp_in && st.lse_part != nullptr;
-    const float2 *part = use_part ? reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld
-                                  : nullptr;
-    const int G = (U + 31) >> 5;
+    const bool staged = use_part && st.stage_partials;
+    const float2 *gpart = use_part ? reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld
+                                   : nullptr;
+    const float2 *part = staged ? part_s + (size_t)i * G : gpart;
 
     // ---- 1. statistics (and the K-th largest group maximum for pruning)
     float mx = 0.f, lse = 0.f, T = -INFINITY;
     if (use_part) {
+      if (staged) {  // stage the row's partials: 16-byte loads, all in flight
+        const float4 *src = reinterpret_cast<const float4 *>(gpart);
+        float4 *dst = reinterpret_cast<float4 *>(part_s + (size_t)i * G);
+        const int n4 = G >> 1;
+        for (int q0 = lane; q0 < n4; q0 += 32 * 8) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q0 + 32 * u < n4) v[u] = __ldcs(src + q0 + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (q0 + 32 * u < n4) dst[q0 + 32 * u] = v[u];
+        }
+        if ((G & 1) && lane == 0) part_s[(size_t)i * G + G - 1] = gpart[G - 1];
+        __syncwarp();
+      }
       float gv[MAXK];
 #pragma unroll
       for (int j = 0; j < MAXK; ++j) gv[j] = -INFINITY;
@@ -218,11 +249,6 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
       }
     };
     if (use_part && st.prune && (do_topk || need_argmax)) {
-      // exact pruning: T <= K-th largest logit and lp, s_r + lp are monotone
-      // in x, so every column that can enter the top K by (key desc, col
-      // asc) has x >= T - delta (delta covers the float32 rounding of
-      // (x - max) - lse and the float64 rounding of s_r + lp, so ties are
-      // never lost); the first-max argmax lies within delta of the max.
       const float thr_top = do_topk ? (T == -INFINITY ? -INFINITY
                                        : T - (4e-6f * (fabsf(T) + fabsf(mx) + fabsf(lse) + 1.0f) +
                                               (float)(1e-15 * (fabs(s_r) + 1.0))))
@@ -230,14 +256,46 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
       const float thr_arg =
           need_argmax ? mx - 4e-6f * (2.0f * fabsf(mx) + fabsf(lse) + 1.0f) : INFINITY;
       const float thr = fminf(thr_top, thr_arg);
+      // collect candidate groups in increasing order (ballot per 32 groups)
+      int ncg = 0;
+      bool overflow = false;
       for (int g0 = 0; g0 < G; g0 += 32) {
         const int g = g0 + lane;
         unsigned cand = __ballot_sync(0xffffffffu, g < G && part[g].x >= thr);
-        while (cand) {
-          const int gg = g0 + __ffs(cand) - 1;
-          cand &= cand - 1;
-          const int c = (gg << 5) + lane;  // lane = column: coalesced 128 B
-          if (c < U) visit(c, __ldcs(row + c));
+        const int n = __popc(cand);
+        if (ncg + n > 64) {
+          overflow = true;
+          break;
+        }
+        if ((cand >> lane) & 1u) sm.cg[i][ncg + __popc(cand & ((1u << lane) - 1u))] = g;
+        ncg += n;
+      }
+      __syncwarp();
+      if (!overflow) {
+        // lane = column inside the group: one coalesced 128-byte segment per
+        // group; 8 groups' loads in flight before visiting them in order
+        for (int q0 = 0; q0 < ncg; q0 += 8) {
+          float xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = q0 + u < ncg ? (sm.cg[i][q0 + u] << 5) + lane : U;
+            xv[u] = c < U ? __ldcs(row + c) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = q0 + u < ncg ? (sm.cg[i][q0 + u] << 5) + lane : U;
+            if (c < U) visit(c, xv[u]);
+          }
+        }
+      } else {
+        for (int g0 = 0; g0 < G; g0 += 32) {
+          const int g = g0 + lane;
+          unsigned cand = __ballot_sync(0xffffffffu, g < G && part[g].x >= thr);
+          while (cand) {
+            const int c = ((g0 + __ffs(cand) - 1) << 5) + lane;
+            cand &= cand - 1;
+            if (c < U) visit(c, __ldcs(row + c));
+          }
         }
       }
     } else if (do_topk || need_argmax) {
@@ -263,17 +321,17 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
         acol = oc;
       }
     }
-    if (lane == 0) st.row_argmax[r] = acol;
+    if (lane == 0) sm.arg[i] = acol;
     if (!do_topk) {
       if (lane == 0) {
         const float x = row[fcol];
         const float lp = lp_in ? x : (x - mx) - lse;
         // forced steps: float32 key fl32(fl32(s) + lp) (NEP 50 promotion)
         const float key32 = (float)s_r + lp;
-        st.cand_score[(size_t)r * K] = (double)key32;
-        st.cand_lp[(size_t)r * K] = lp;
-        st.cand_col[(size_t)r * K] = fcol;
-        st.cand_cnt[r] = 1;
+        sm.key[i][0] = (double)key32;
+        sm.lp[i][0] = lp;
+        sm.col[i][0] = fcol;
+        sm.cnt[i] = 1;
       }
     } else {
       int cnt = 0;
@@ -294,9 +352,9 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
         const float blp = __shfl_sync(0xffffffffu, tl[0], bl);
         if (bc == INT_MAX) break;
         if (lane == 0) {
-          st.cand_score[(size_t)r * K + j] = bk;
-          st.cand_lp[(size_t)r * K + j] = blp;
-          st.cand_col[(size_t)r * K + j] = bc;
+          sm.key[i][j] = bk;
+          sm.lp[i][j] = blp;
+          sm.col[i][j] = bc;
         }
         ++cnt;
         if (lane == bl) {
@@ -311,7 +369,7 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
           tc[MAXK - 1] = INT_MAX;
         }
       }
-      if (lane == 0) st.cand_cnt[r] = cnt;
+      if (lane == 0) sm.cnt[i] = cnt;
     }
     // factor choices of this row (search.py:261-272): prefix override at
     // t - 1, else first-max of the factor logits
@@ -342,51 +400,25 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
       }
       if (lane == 0) st.fac_choice[(size_t)r * nf + k] = choice;
     }
-  } else if (lane == 0) {
-    st.cand_cnt[r] = 0;
   }
+  __syncthreads();
+  if (i != 0) return;
 
-  // ---- 4. arrival: the last row of the sentence merges
-  __threadfence();
-  __syncwarp();
-  unsigned prev = 0;
-  if (lane == 0) prev = atomicAdd(&st.counter[b], 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != (unsigned)(K - 1)) return;
-  __threadfence();
+  // ---- warp 0: merge the row lists.  K rounds of a warp argmax over the
+  // row-list heads in the exact order (score desc, token asc, parent asc);
+  // columns are sorted by token.
   const int base = b * K;
-  if (__ldcg(st.done + b)) {
-    if (lane == 0) st.counter[b] = 0;
-    return;
-  }
-  const int nalive = __ldcg(st.n_alive + b);
-  // per-warp staging area: K*K (key, lp, col) + per-row (count, score, argmax)
-  double *m_key = reinterpret_cast<double *>(beam_smem) + (size_t)wib * K * K;
-  float *m_lp = reinterpret_cast<float *>(reinterpret_cast<double *>(beam_smem) + (size_t)BEAM_WARPS * K * K) +
-                (size_t)wib * K * K;
-  int *m_col = reinterpret_cast<int *>(reinterpret_cast<float *>(
-                   reinterpret_cast<double *>(beam_smem) + (size_t)BEAM_WARPS * K * K) +
-               (size_t)BEAM_WARPS * K * K) + (size_t)wib * K * K;
-  for (int idx = lane; idx < nalive * K; idx += 32) {
-    const size_t g = (size_t)base * K + idx;
-    m_key[idx] = __ldcg(st.cand_score + g);
-    m_lp[idx] = __ldcg(st.cand_lp + g);
-    m_col[idx] = __ldcg(st.cand_col + g);
-  }
-  const int my_cnt = lane < nalive ? __ldcg(st.cand_cnt + base + lane) : 0;
-  const double my_s = lane < nalive ? __ldcg(st.score + base + lane) : 0.0;
-  const int my_arg = lane < nalive ? __ldcg(st.row_argmax + base + lane) : 0;
-  __syncwarp();
-  // K rounds of a warp argmax over the row-list heads in the exact order
-  // (score desc, token asc, parent asc); columns are sorted by token.
+  const int my_cnt = lane < nalive ? sm.cnt[lane] : 0;
+  const double my_s = lane < nalive ? st.score[base + lane] : 0.0;
+  const int my_arg = lane < nalive ? sm.arg[lane] : 0;
   int head = 0;
   int npk = 0;
   int pick_q = 0, pick_c = 0;  // lane j keeps pick j
   float pick_lp = 0.f;
   for (int sel = 0; sel < K; ++sel) {
     const bool has = lane < nalive && head < my_cnt;
-    double bk = has ? m_key[lane * K + head] : 0.0;
-    int bc = has ? m_col[lane * K + head] : 0;
+    double bk = has ? sm.key[lane][head] : 0.0;
+    int bc = has ? sm.col[lane][head] : 0;
     int bq = lane;
     bool bh = has;
 #pragma unroll
@@ -404,7 +436,7 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
       }
     }
     if (!bh) break;
-    const float plp = __shfl_sync(0xffffffffu, has ? m_lp[lane * K + head] : 0.f, bq);
+    const float plp = __shfl_sync(0xffffffffu, has ? sm.lp[lane][head] : 0.f, bq);
     if (lane == sel) {
       pick_q = bq;
       pick_c = bc;
@@ -413,15 +445,13 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
     if (lane == bq) ++head;
     npk = sel + 1;
   }
-  // scores and tokens of the picks (lane j = pick j), then sequential routing
+  // scores and tokens of the picks (lane j = pick j)
   const double pick_score = __shfl_sync(0xffffffffu, my_s, pick_q) + (double)pick_lp;
   const int pick_arg = __shfl_sync(0xffffffffu, my_arg, pick_q);
   const int pick_tok = (lane < npk) ? (st.col_token ? st.col_token[pick_c] : pick_c) : -1;
-  const int plen = st.prefix_len[b];
-  const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
   const int steps = t + 1;
   const double pen = st.len_pen[steps];
-  // survivor rank of each pick (exclusive prefix count of non-EOS picks)
+  // survivors take new rows in rank order
   const unsigned surv = __ballot_sync(0xffffffffu, lane < npk && pick_tok != EOS);
   const int n_new = __popc(surv);
   if (lane < npk && pick_tok != EOS) {
@@ -433,7 +463,7 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
     st.tok_hist[(size_t)t * R + slot] = pick_tok;
     st.par_hist[(size_t)t * R + slot] = pick_q;
     for (int k = 0; k < nf; ++k) {
-      const int f = __ldcg(st.fac_choice + (size_t)rr * nf + k);
+      const int f = st.fac_choice[(size_t)rr * nf + k];
       st.ftok_next[(size_t)k * R + slot] = f;
       st.fac_hist[((size_t)t * nf + k) * R + slot] = f;
     }
@@ -443,20 +473,11 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
     st.parent[base + lane] = base;
     for (int k = 0; k < nf; ++k) st.ftok_next[(size_t)k * R + base + lane] = PAD;
   }
-  // finished hypotheses in rank order: the first maximum of logprob/steps^a
-  const unsigned fin = __ballot_sync(0xffffffffu, lane < npk && pick_tok == EOS);
-  if (lane == 0) {
-    st.n_alive[b] = n_new;
-    st.counter[b] = 0;
-    if (n_new == 0) {
-      st.done[b] = 1;
-      atomicAdd(st.n_done, 1);
-    }
-  }
-  // lanes with EOS picks, processed in rank order by shuffling to lane 0
-  unsigned f = fin;
-  int best_steps = __shfl_sync(0xffffffffu, lane == 0 ? st.best_steps[b] : 0, 0);
-  double best_norm = __shfl_sync(0xffffffffu, lane == 0 ? st.best_norm[b] : 0.0, 0);
+  // finished hypotheses in rank order: keep the first maximum of
+  // logprob / steps^alpha (search.py:394)
+  unsigned f = __ballot_sync(0xffffffffu, lane < npk && pick_tok == EOS);
+  int best_steps = st.best_steps[b];
+  double best_norm = st.best_norm[b];
   while (f) {
     const int j = __ffs(f) - 1;
     f &= f - 1;
@@ -475,8 +496,15 @@ __global__ void __launch_bounds__(BEAM_WARPS * 32) k_beam_step(const float *__re
         st.best_forced[b] = final_force && ar != c;
         st.best_parent[b] = q;
         for (int k = 0; k < nf; ++k)
-          st.best_fac[(size_t)b * nf + k] = __ldcg(st.fac_choice + (size_t)(base + q) * nf + k);
+          st.best_fac[(size_t)b * nf + k] = st.fac_choice[(size_t)(base + q) * nf + k];
       }
+    }
+  }
+  if (lane == 0) {
+    st.n_alive[b] = n_new;
+    if (n_new == 0) {
+      st.done[b] = 1;
+      atomicAdd(st.n_done, 1);
     }
   }
 }
@@ -524,31 +552,33 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
   if (!st || st->B <= 0 || st->K <= 0 || st->U <= 0)
     return fail(SKB_ERR_SHAPE, "beam_step: bad state");
   if (st->K > 32) return fail(SKB_ERR_CONFIG, "beam size %d exceeds 32", st->K);
-  const int R = st->B * st->K;
   cudaStream_t s = as_stream(stream);
-  const int grid = (R + BEAM_WARPS - 1) / BEAM_WARPS;
-  const size_t smem = (size_t)BEAM_WARPS * st->K * st->K * (sizeof(double) + sizeof(float) + sizeof(int));
-  if (smem > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_beam_step<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-  }
-  if (st->K <= 1)
-    k_beam_step<1><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
-  else if (st->K <= 2)
-    k_beam_step<2><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
-  else if (st->K <= 4)
-    k_beam_step<4><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
-  else if (st->K <= 5)
-    k_beam_step<5><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
-  else if (st->K <= 8)
-    k_beam_step<8><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
-  else if (st->K <= 16)
-    k_beam_step<16><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
+  skb_beam_state sv = *st;
+  // stage the fused partials in shared memory when K rows x G groups fit
+  const int G = (sv.U + 31) / 32;
+  const size_t part_bytes = (size_t)sv.K * G * sizeof(float2);
+  sv.stage_partials = (sv.lse_part != nullptr && part_bytes <= 160 * 1024) ? 1 : 0;
+  auto go = [&](auto kern_ptr, size_t base_smem, int threads) {
+    const size_t smem = base_smem + (sv.stage_partials ? part_bytes : 0);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern_ptr<<<sv.B, threads, smem, s>>>(logits, ld_logits, lp_in, sv);
+  };
+  const int th = sv.K * 32;
+  if (sv.K <= 1)
+    go(k_beam_step<1>, sizeof(BeamSmem<1>), th);
+  else if (sv.K <= 2)
+    go(k_beam_step<2>, sizeof(BeamSmem<2>), th);
+  else if (sv.K <= 4)
+    go(k_beam_step<4>, sizeof(BeamSmem<4>), th);
+  else if (sv.K <= 5)
+    go(k_beam_step<5>, sizeof(BeamSmem<5>), th);
+  else if (sv.K <= 8)
+    go(k_beam_step<8>, sizeof(BeamSmem<8>), th);
+  else if (sv.K <= 16)
+    go(k_beam_step<16>, sizeof(BeamSmem<16>), th);
   else
-    k_beam_step<32><<<grid, BEAM_WARPS * 32, smem, s>>>(logits, ld_logits, lp_in, *st);
+    go(k_beam_step<32>, sizeof(BeamSmem<32>), th);
   SKB_CHECK_LAUNCH("k_beam_step");
   return SKB_OK;
 }

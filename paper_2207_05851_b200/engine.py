@@ -315,7 +315,7 @@ class BeamBatch:
             self.done.data_ptr(), self.score.data_ptr(), sb.tok.data_ptr(), sb.ftok.data_ptr(),
             sb.parent.data_ptr(), self.tok_hist.data_ptr(), self.par_hist.data_ptr(),
             self.fac_hist.data_ptr(), sb.fac.data_ptr() if nf else None, sb.fac.stride(0),
-            model.fac_off.data_ptr(), sb.lse_part.data_ptr(), sb.lse_part.shape[1] // 2, 1,
+            model.fac_off.data_ptr(), sb.lse_part.data_ptr(), sb.lse_part.shape[1] // 2, 1, 0,
             self.cand_score.data_ptr(), self.cand_lp.data_ptr(),
             self.cand_col.data_ptr(), self.cand_cnt.data_ptr(), self.row_argmax.data_ptr(),
             self.fac_choice.data_ptr(), self.counter.data_ptr(), self.best_norm.data_ptr(),

@@ -416,7 +416,7 @@ class ProtocolSearch:
                          b["ftok"].data_ptr(), b["parent"].data_ptr(), b["tok_hist"].data_ptr(),
                          b["par_hist"].data_ptr(), b["fac_hist"].data_ptr(),
                          facl.data_ptr() if nf else None, facl.stride(0), fac_off.data_ptr(),
-                         None, 0, 0, b["cand_score"].data_ptr(), b["cand_lp"].data_ptr(),
+                         None, 0, 0, 0, b["cand_score"].data_ptr(), b["cand_lp"].data_ptr(),
                          b["cand_col"].data_ptr(), b["cand_cnt"].data_ptr(),
                          b["row_argmax"].data_ptr(), b["fac_choice"].data_ptr(),
                          b["counter"].data_ptr(), b["best_norm"].data_ptr(),

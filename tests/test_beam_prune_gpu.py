@@ -36,7 +36,7 @@ def _state(B, K, U, logits, prune, lse_part, mask=None, t=3, max_len=40):
                      b["done"].data_ptr(), b["score"].data_ptr(), b["tok"].data_ptr(),
                      b["ftok"].data_ptr(), b["parent"].data_ptr(), b["tok_hist"].data_ptr(),
                      b["par_hist"].data_ptr(), b["fac_hist"].data_ptr(), None, 1, None,
-                     lse_part.data_ptr(), lse_part.shape[1] // 2, prune,
+                     lse_part.data_ptr(), lse_part.shape[1] // 2, prune, 0,
                      b["cand_score"].data_ptr(), b["cand_lp"].data_ptr(), b["cand_col"].data_ptr(),
                      b["cand_cnt"].data_ptr(), b["row_argmax"].data_ptr(),
                      b["fac_choice"].data_ptr(), b["counter"].data_ptr(), b["best_norm"].data_ptr(),
