@@ -255,6 +255,10 @@ int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, int *step, v
 int skb_beam_finalize(const skb_beam_state *st, int *tokens_out, int *factors_out,
                       void *stream);
 
+/* Debug: copy the beam kernel's per-row phase timestamps (only in builds
+ * with -DSKB_PROFILE_PHASES; SKB_ERR_UNSUPPORTED otherwise). */
+int skb_debug_beam_prof(unsigned long long *host_buf_4096x10);
+
 /* out[r] = max over positions l < len[b] of enc[b, l, :] (model.py:496-500). */
 int skb_masked_maxpool(int B, int L, int d, const float *enc, const int *lengths, float *out,
                        void *stream);

@@ -69,6 +69,7 @@ SIGNATURES = {
     "skb_convert": [C.c_longlong, vp, i32, vp, i32, vp],
     "skb_nvs_mask": [i32, i32, vp, i32, C.c_float, vp, vp],
     "skb_set_device": [i32],
+    "skb_debug_beam_prof": [vp],
 }
 
 _lib = None

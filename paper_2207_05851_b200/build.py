@@ -51,7 +51,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         obj = objdir / (src.stem + ".o")
         if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_t):
             return obj, ""
-        cmd = [cc, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("SKB_NVCC_EXTRA", "").split()
+        cmd = [cc, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{r.stderr}")

@@ -120,6 +120,21 @@ __device__ __forceinline__ float warp_kth(float (&v)[MAXK], int K) {
   return last;
 }
 
+// Optional phase timestamps (build with SKB_NVCC_EXTRA=-DSKB_PROFILE_PHASES)
+#ifdef SKB_PROFILE_PHASES
+__device__ unsigned long long g_tprof[4096 * 10];
+#define TP(k)                                                                         \
+  do {                                                                                \
+    unsigned long long _t;                                                            \
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t));                             \
+    if (lane == 0 && r < 4096) g_tprof[r * 10 + (k)] = _t;                            \
+  } while (0)
+#else
+#define TP(k) \
+  do {        \
+  } while (0)
+#endif
+
 // Shared-memory layout of one sentence CTA (K warps).
 template <int MAXK>
 struct BeamSmem {
@@ -149,7 +164,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
                                                           int lp_in, skb_beam_state st) {
   extern __shared__ __align__(16) uint8_t beam_smem[];
   BeamSmem<MAXK> &sm = *reinterpret_cast<BeamSmem<MAXK> *>(beam_smem);
-  float2 *part_s = reinterpret_cast<float2 *>(beam_smem + sizeof(BeamSmem<MAXK>));
+  float2 *part_s = reinterpret_cast<float2 *>(beam_smem + ((sizeof(BeamSmem<MAXK>) + 15) & ~size_t(15)));
   const int lane = threadIdx.x & 31, i = threadIdx.x >> 5;
   const int K = st.K, U = st.U;
   const int R = st.B * K;
@@ -158,6 +173,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
   const int t = *st.step;
   const int nf = st.n_factors;
   const int G = (U + 31) >> 5;
+  TP(0);
   if (st.done[b]) return;
   const int nalive = st.n_alive[b];
   const int plen = st.prefix_len[b];
@@ -178,12 +194,16 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
     const float2 *part = staged ? part_s + (size_t)i * G : gpart;
 
     // ---- 1. statistics (and the K-th largest group maximum for pruning)
+    TP(1);
     float mx = 0.f, lse = 0.f, T = -INFINITY;
     if (use_part) {
       if (staged) {  // stage the row's partials: 16-byte loads, all in flight
         const float4 *src = reinterpret_cast<const float4 *>(gpart);
         float4 *dst = reinterpret_cast<float4 *>(part_s + (size_t)i * G);
-        const int n4 = G >> 1;
+        const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+        const int n4 = al ? (G >> 1) : 0;
+        if (!al)
+          for (int g = lane; g < G; g += 32) part_s[(size_t)i * G + g] = gpart[g];
         for (int q0 = lane; q0 < n4; q0 += 32 * 8) {
           float4 v[8];
 #pragma unroll
@@ -193,9 +213,10 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
           for (int u = 0; u < 8; ++u)
             if (q0 + 32 * u < n4) dst[q0 + 32 * u] = v[u];
         }
-        if ((G & 1) && lane == 0) part_s[(size_t)i * G + G - 1] = gpart[G - 1];
+        if (al && (G & 1) && lane == 0) part_s[(size_t)i * G + G - 1] = gpart[G - 1];
         __syncwarp();
       }
+      TP(2);
       float gv[MAXK];
 #pragma unroll
       for (int j = 0; j < MAXK; ++j) gv[j] = -INFINITY;
@@ -224,6 +245,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
       lse = logf(warp_sum(sum));
     }
 
+    TP(3);
     // ---- 2./3. candidates -> per-lane top-K and first-max argmax
     double tk[MAXK];
     float tl[MAXK];
@@ -311,6 +333,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
         for (int c = lane; c < U; c += 32) visit(c, row[c]);
       }
     }
+    TP(4);
     // first max of lp across the warp (ties -> lowest column)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -401,7 +424,9 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
       if (lane == 0) st.fac_choice[(size_t)r * nf + k] = choice;
     }
   }
+  TP(5);
   __syncthreads();
+  TP(6);
   if (i != 0) return;
 
   // ---- warp 0: merge the row lists.  K rounds of a warp argmax over the
@@ -507,6 +532,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
       atomicAdd(st.n_done, 1);
     }
   }
+  TP(7);
 }
 
 // ------------------------------------------------------------- reorder
@@ -559,7 +585,7 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
   const size_t part_bytes = (size_t)sv.K * G * sizeof(float2);
   sv.stage_partials = (sv.lse_part != nullptr && part_bytes <= 160 * 1024) ? 1 : 0;
   auto go = [&](auto kern_ptr, size_t base_smem, int threads) {
-    const size_t smem = base_smem + (sv.stage_partials ? part_bytes : 0);
+    const size_t smem = ((base_smem + 15) & ~size_t(15)) + (sv.stage_partials ? part_bytes : 0);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern_ptr<<<sv.B, threads, smem, s>>>(logits, ld_logits, lp_in, sv);
@@ -581,6 +607,16 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
     go(k_beam_step<32>, sizeof(BeamSmem<32>), th);
   SKB_CHECK_LAUNCH("k_beam_step");
   return SKB_OK;
+}
+
+extern "C" int skb_debug_beam_prof(unsigned long long *host) {
+#ifdef SKB_PROFILE_PHASES
+  return cudaMemcpyFromSymbol(host, skb::g_tprof, sizeof(unsigned long long) * 4096 * 10) == cudaSuccess
+             ? 0 : 3;
+#else
+  (void)host;
+  return SKB_ERR_UNSUPPORTED;
+#endif
 }
 
 extern "C" int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, int *step,

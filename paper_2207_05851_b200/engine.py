@@ -59,7 +59,8 @@ class StepBuffers:
         self.f = torch.zeros(R, c.ff_dim, device=dev, dtype=cdt)
         self.logits = torch.zeros(R, U, device=dev)
         # fused log-softmax partials: (max, sum exp) per 32-column group
-        self.lse_part = torch.zeros(R, 2 * ((U + 31) // 32), device=dev)
+        G = (U + 31) // 32
+        self.lse_part = torch.zeros(R, 2 * (G + (G & 1)), device=dev)  # rows 16-byte aligned
         self.mask = None          # [B, words] active-column bits (restricted vocab)
         self.group = 1            # rows per sentence group (beam size)
         self.fac = torch.zeros(R, int(model.fac_off[-1].item()) if nf else 1, device=dev)
