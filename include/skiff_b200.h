@@ -147,11 +147,15 @@ int skb_encoder_attention(int B, int L, int H, int dh, const void *qkv, int ld_q
  * row r attends over positions 0..t (t = *step) of its hypothesis.  New k,v
  * (from qkv) are stored at cache slot (r, t); earlier positions p < t are
  * read from slot anc[(t&1)][r][p] (ancestor table) — the beam
- * reorder never moves cache bytes.  kc/vc: [R_cap, S_max, H*dh] cache_dtype.
+ * reorder never moves cache bytes.  kc/vc: [R_cap, H, S_max, dh] cache_dtype.
+ * rows_per_group G > 1 promises that rows [g*G, g*G+G) only reference slots
+ * in that range (beam rows of one sentence): one CTA per (group, head) then
+ * stages the group's cache tiles in shared memory.
  */
 int skb_self_attention_step(int R, int H, int dh, const void *qkv, int ld_qkv, int qkv_dtype,
                             void *kc, void *vc, int cache_dtype, int S_max, const int *anc,
-                            const int *step, void *ctx, int ldc, int ctx_dtype, void *stream);
+                            const int *step, int rows_per_group, void *ctx, int ldc,
+                            int ctx_dtype, void *stream);
 
 /*
  * Cross-attention for one step (model.py:568-573): q [R, ldq]; row r reads

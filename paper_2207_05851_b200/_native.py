@@ -57,8 +57,8 @@ SIGNATURES = {
     "skb_embed_target": [i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp],
     "skb_embed_source": [i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],
     "skb_encoder_attention": [i32, i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp],
-    "skb_self_attention_step": [i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp, vp, vp, i32,
-                                i32, vp],
+    "skb_self_attention_step": [i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp, vp, i32, vp,
+                                i32, i32, vp],
     "skb_cross_attention_step": [i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp,
                                  vp, i32, vp, i32, i32, vp],
     "skb_gather_rows": [i32, i32, vp, i32, vp, vp, i32, i32, vp],

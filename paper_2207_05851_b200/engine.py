@@ -92,7 +92,7 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
         else:
             kern.gemm(sb.h, Ly.wqkv, sb.qkv)
             kern.self_attention_step(sb.qkv, sb.kc[li], sb.vc[li], sb.anc, sb.step, sb.ctx,
-                                     R, H, dh, sb.S_max)
+                                     R, H, dh, sb.S_max, sb.group)
             kern.gemm(sb.ctx, Ly.wo, sb.x, N.EPI_RESID)
         kern.layernorm(sb.x, *Ly.ln_cross, sb.h)
         kern.gemm(sb.h, Ly.wq_c, sb.q)

@@ -87,10 +87,10 @@ def encoder_attention(qkv, lengths, ctx, B, L, H, dh):
     _count()
 
 
-def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max):
+def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max, group=1):
     N.call("skb_self_attention_step", R, H, dh, qkv.data_ptr(), qkv.stride(0), dcode(qkv),
            kc.data_ptr(), vc.data_ptr(), dcode(kc), S_max, anc.data_ptr(), step.data_ptr(),
-           ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+           group, ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
     _count()
 
 
