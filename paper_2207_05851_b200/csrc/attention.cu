@@ -9,9 +9,7 @@
 //    preallocated cache at slot (row, t) and the t earlier positions are read
 //    through the ancestor table, so the beam reorder never copies cache bytes
 //    (SURVEY §8a10).  Cache layout [slot][head][position][d_h] keeps the
-//    positions of one (slot, head) contiguous.  With beam groups, one CTA
-//    per (sentence, head) streams the sentence's K slots into shared memory
-//    and each warp attends for one beam row from there.
+//    positions of one (slot, head) contiguous.
 //  * cross-attention: one warp per (row, head) over the sentence's encoder
 //    memory; all beam rows of a sentence read the same K/V (L2-resident).
 // Scores are q.k * (1/sqrt(d_h)) in fp32 (kernels.py:512-514).
@@ -365,27 +363,39 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
   float o8[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) o8[u] = 0.f;
+  // ancestor slots of the first chunk; later chunks are prefetched while the
+  // current one computes, and K and V of a chunk are loaded together, so a
+  // chunk costs one memory round trip
+  int sl[ITER];
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int p = it * KPI + grp;
+    sl[it] = p <= t ? (p == t ? r : __ldg(arow + p)) : -1;
+  }
   for (int p0 = 0; p0 <= t; p0 += 32) {
-    size_t off[ITER];
-    float sc[ITER];
+    uint4 kk[ITER], vv[ITER];
 #pragma unroll
     for (int it = 0; it < ITER; ++it) {
       const int p = p0 + it * KPI + grp;
-      off[it] = (size_t)-1;
-      if (p <= t) {
-        const int slot = p == t ? r : __ldg(arow + p);
-        off[it] = (((size_t)slot * H + h) * S_max + p) * DH + sub * 8;
+      if (sl[it] >= 0) {
+        const size_t off = (((size_t)sl[it] * H + h) * S_max + p) * DH + sub * 8;
+        kk[it] = *reinterpret_cast<const uint4 *>(kc + off);
+        vv[it] = *reinterpret_cast<const uint4 *>(vc + off);
+      } else {
+        kk[it] = vv[it] = make_uint4(0, 0, 0, 0);
       }
     }
-    uint4 kv4[ITER];
+    int sn[ITER];
 #pragma unroll
-    for (int it = 0; it < ITER; ++it)
-      kv4[it] = off[it] != (size_t)-1 ? *reinterpret_cast<const uint4 *>(kc + off[it])
-                                      : make_uint4(0, 0, 0, 0);
+    for (int it = 0; it < ITER; ++it) {
+      const int p = p0 + 32 + it * KPI + grp;
+      sn[it] = p <= t ? (p == t ? r : __ldg(arow + p)) : -1;
+    }
+    float sc[ITER];
     float cmax = -INFINITY;
 #pragma unroll
     for (int it = 0; it < ITER; ++it) {
-      const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kv4[it]);
+      const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kk[it]);
       float a = 0.f;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
       }
 #pragma unroll
       for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      sc[it] = off[it] != (size_t)-1 ? a * scale : -INFINITY;
+      sc[it] = sl[it] >= 0 ? a * scale : -INFINITY;
       cmax = fmaxf(cmax, sc[it]);
     }
 #pragma unroll
@@ -415,12 +425,8 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
 #pragma unroll
     for (int u = 0; u < 8; ++u) o8[u] *= corr;
 #pragma unroll
-    for (int it = 0; it < ITER; ++it)
-      kv4[it] = off[it] != (size_t)-1 ? *reinterpret_cast<const uint4 *>(vc + off[it])
-                                      : make_uint4(0, 0, 0, 0);
-#pragma unroll
     for (int it = 0; it < ITER; ++it) {
-      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&kv4[it]);
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv[it]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float2 f = __bfloat1622float2(vp[u]);
@@ -428,175 +434,10 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
         o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
       }
     }
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) sl[it] = sn[it];
   }
   // reduce the KPI key groups; lanes of group 0 own the output
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) o8[u] += __shfl_xor_sync(0xffffffffu, o8[u], o);
-  if (grp == 0) {
-    const float inv = 1.0f / l_run;
-    const size_t ob = (size_t)r * ldc + h * DH + sub * 8;
-    if (ctx_dtype == SKB_BF16) {
-      uint4 w;
-      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        __nv_bfloat162 pr = __floats2bfloat162_rn(o8[2 * u] * inv, o8[2 * u + 1] * inv);
-        wp[u] = *reinterpret_cast<uint32_t *>(&pr);
-      }
-      *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(ctx) + ob) = w;
-    } else {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) reinterpret_cast<float *>(ctx)[ob + u] = o8[u] * inv;
-    }
-  }
-}
-
-// --------------------------- decoder self-attention, beam-grouped (bf16)
-// One CTA per (sentence b, head h), one warp per beam row i < G.  Every
-// ancestor slot of a beam row lies in the sentence's slot range
-// [b*G, b*G+G), so positions [p0, p0+PT) of all G slots are streamed into
-// shared memory (coalesced 16-byte loads: slot-major, positions contiguous)
-// and each warp attends over them through its ancestor table; position t is
-// the row's own fresh k/v (registers).  Online softmax over PT-sized tiles.
-template <int DH>
-__global__ void __launch_bounds__(256) k_self_attn_grouped(
-    int R, int H, int G, const __nv_bfloat16 *qkv, int ld_qkv, __nv_bfloat16 *kc,
-    __nv_bfloat16 *vc, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
-    int ctx_dtype) {
-  constexpr int PT = 32;           // positions per shared-memory tile
-  constexpr int LPK = DH / 8;      // lanes per key row (one uint4 each)
-  constexpr int KPI = 32 / LPK;    // keys per warp instruction
-  constexpr int ITER = PT / KPI;
-  extern __shared__ __align__(16) uint8_t sa_smem[];
-  uint4 *Ks = reinterpret_cast<uint4 *>(sa_smem);           // [G][PT][LPK]
-  uint4 *Vs = Ks + (size_t)G * PT * LPK;
-  const int b = blockIdx.x, h = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
-  const int D = H * DH;
-  const int t = *step;
-  const int r = b * G + warp;
-  const bool row_ok = warp < G && r < R;
-  const int sub = lane % LPK, grp = lane / LPK;
-  // ---- this row's q (8 dims per lane) and fresh k/v -> cache slot (r, t)
-  float q8[8], k8[8], v8[8];
-  if (row_ok) {
-    const size_t base = (size_t)r * ld_qkv + h * DH + sub * 8;
-    const uint4 qv = *reinterpret_cast<const uint4 *>(qkv + base);
-    const uint4 kv = *reinterpret_cast<const uint4 *>(qkv + base + D);
-    const uint4 vv = *reinterpret_cast<const uint4 *>(qkv + base + 2 * D);
-    const __nv_bfloat162 *qp = reinterpret_cast<const __nv_bfloat162 *>(&qv);
-    const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kv);
-    const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float2 a = __bfloat1622float2(qp[u]), c = __bfloat1622float2(kp[u]),
-                   e = __bfloat1622float2(vp[u]);
-      q8[2 * u] = a.x; q8[2 * u + 1] = a.y;
-      k8[2 * u] = c.x; k8[2 * u + 1] = c.y;
-      v8[2 * u] = e.x; v8[2 * u + 1] = e.y;
-    }
-    if (grp == 0) {
-      const size_t cs = (((size_t)r * H + h) * S_max + t) * DH + sub * 8;
-      *reinterpret_cast<uint4 *>(kc + cs) = kv;
-      *reinterpret_cast<uint4 *>(vc + cs) = vv;
-    }
-  }
-  const int *arow = anc + ((size_t)(t & 1) * R + (row_ok ? r : 0)) * S_max;
-  float m_run = -INFINITY, l_run = 0.f;
-  float o8[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) o8[u] = 0.f;
-  // the own position t first (it is never staged)
-  if (row_ok) {
-    float a = 0.f;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a = fmaf(q8[u], k8[u], a);
-#pragma unroll
-    for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    m_run = a * scale;
-    l_run = 1.f;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) o8[u] = grp == 0 ? v8[u] : 0.f;
-  }
-  for (int p0 = 0; p0 < t; p0 += PT) {
-    const int np = min(PT, t - p0);
-    __syncthreads();  // previous tile consumed
-    // ---- stage positions [p0, p0+np) of the G slots (K and V)
-    const int per_mat = G * np * LPK;
-    for (int idx = threadIdx.x; idx < per_mat; idx += nthr) {
-      const int s = idx / (np * LPK);
-      const int rem = idx % (np * LPK);
-      const int p = rem / LPK, c = rem % LPK;
-      const int slot = b * G + s;
-      if (slot < R) {
-        const size_t off = (((size_t)slot * H + h) * S_max + p0 + p) * DH + c * 8;
-        Ks[((size_t)s * PT + p) * LPK + c] = *reinterpret_cast<const uint4 *>(kc + off);
-        Vs[((size_t)s * PT + p) * LPK + c] = *reinterpret_cast<const uint4 *>(vc + off);
-      }
-    }
-    __syncthreads();
-    if (!row_ok) continue;
-    // ---- scores for this tile (KPI keys per instruction)
-    float sc[ITER];
-    int sl[ITER];
-    float cmax = -INFINITY;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int p = it * KPI + grp;
-      sl[it] = p < np ? __ldg(arow + p0 + p) - b * G : -1;
-    }
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int p = it * KPI + grp;
-      float a = 0.f;
-      if (sl[it] >= 0) {
-        const uint4 kk = Ks[((size_t)sl[it] * PT + p) * LPK + sub];
-        const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kk);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 f = __bfloat1622float2(kp[u]);
-          a = fmaf(q8[2 * u], f.x, a);
-          a = fmaf(q8[2 * u + 1], f.y, a);
-        }
-      }
-#pragma unroll
-      for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      sc[it] = sl[it] >= 0 ? a * scale : -INFINITY;
-      cmax = fmaxf(cmax, sc[it]);
-    }
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    const float mnew = fmaxf(m_run, cmax);
-    const float corr = expf(m_run - mnew);
-    float psum = 0.f;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      sc[it] = sc[it] == -INFINITY ? 0.f : expf(sc[it] - mnew);
-      psum += sc[it];
-    }
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
-    l_run = l_run * corr + psum;
-    m_run = mnew;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) o8[u] *= corr;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      if (sl[it] < 0) continue;
-      const int p = it * KPI + grp;
-      const uint4 vv = Vs[((size_t)sl[it] * PT + p) * LPK + sub];
-      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 f = __bfloat1622float2(vp[u]);
-        o8[2 * u] = fmaf(sc[it], f.x, o8[2 * u]);
-        o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
-      }
-    }
-  }
-  if (!row_ok) return;
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
@@ -663,30 +504,7 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
   if (R < 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "self_attention_step: shape");
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "self_attention_step: head dim %d", dh);
   if (R == 0) return SKB_OK;
-  const int G = rows_per_group > 0 ? rows_per_group : 1;
-  if (G > 1 && G <= 8 && cache_dtype == SKB_BF16 && qkv_dtype == SKB_BF16 &&
-      (dh == 32 || dh == 64 || dh == 128) && ld_qkv % 8 == 0 &&
-      (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (reinterpret_cast<uintptr_t>(kc) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(vc) & 15) == 0) {
-    dim3 grid((R + G - 1) / G, H);
-    const size_t smem = (size_t)2 * G * 32 * dh * sizeof(__nv_bfloat16);
-    auto *qb = reinterpret_cast<const __nv_bfloat16 *>(qkv);
-    auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
-    auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
-    const float sc = attn_scale(dh);
-    cudaStream_t s = as_stream(stream);
-    if (dh == 64)
-      k_self_attn_grouped<64><<<grid, 32 * G, smem, s>>>(R, H, G, qb, ld_qkv, k, v, S_max, anc, step,
-                                                         sc, ctx, ldc, ctx_dtype);
-    else if (dh == 32)
-      k_self_attn_grouped<32><<<grid, 32 * G, smem, s>>>(R, H, G, qb, ld_qkv, k, v, S_max, anc, step,
-                                                         sc, ctx, ldc, ctx_dtype);
-    else
-      k_self_attn_grouped<128><<<grid, 32 * G, smem, s>>>(R, H, G, qb, ld_qkv, k, v, S_max, anc,
-                                                          step, sc, ctx, ldc, ctx_dtype);
-    SKB_CHECK_LAUNCH("k_self_attn_grouped");
-    return SKB_OK;
-  }
+  (void)rows_per_group;  // beam rows of a sentence share ancestor slots through L1/L2
   if (cache_dtype == SKB_BF16 && (dh == 32 || dh == 64 || dh == 128) && ld_qkv % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (reinterpret_cast<uintptr_t>(kc) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(vc) & 15) == 0) {
