@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(256) k_encoder_attention(int B, int L, int H, 
                                                            const void *qkv, int ld_qkv, int qkv_dtype,
                                                            const int *lengths, float scale,
                                                            void *ctx, int ldc, int ctx_dtype) {
+  PDL_ENTRY();
   const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l = blockIdx.y * 8 + warp;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(128) k_self_attention_step(
     int R, int H, int dh, const void *qkv, int ld_qkv, int qkv_dtype, void *kc, void *vc,
     int cache_dtype, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
     int ctx_dtype) {
+  PDL_ENTRY();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 4 + warp;
   __shared__ float qs[4][MAX_DH];
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(128) k_cross_attention_step(
     int R, int H, int dh, const void *q, int ldq, int q_dtype, const void *kv, int ld_kv,
     int kv_dtype, int koff, int voff, int L, const int *row_sent, const int *lengths, float scale,
     void *ctx, int ldc, int ctx_dtype) {
+  PDL_ENTRY();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 4 + warp;
   __shared__ float qs[4][MAX_DH];
@@ -223,6 +226,7 @@ __global__ void __launch_bounds__(256) k_attn_smem(
     int R, int G, int H, int dh, const void *q, int ldq, int q_dtype, int qoff, const void *kv,
     int ld_kv, int kv_dtype, int koff, int voff, int L, const int *row_sent, const int *lengths,
     float scale, void *ctx, int ldc, int ctx_dtype) {
+  PDL_ENTRY();
   extern __shared__ float sm[];
   const int g = blockIdx.x, h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -318,6 +322,7 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
     int R, int H, const void *qkv, int ld_qkv, int qkv_dtype, __nv_bfloat16 *kc,
     __nv_bfloat16 *vc, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
     int ctx_dtype) {
+  PDL_ENTRY();
   constexpr int LPK = DH / 8;      // lanes per key row
   constexpr int KPI = 32 / LPK;    // keys per warp instruction
   constexpr int ITER = 32 / KPI;   // = LPK instructions per 32-position chunk
@@ -483,7 +488,7 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
       }
       const int D = H * dh;
       dim3 g2(B, H);
-      k_attn_smem<<<g2, 32 * nw, smem, as_stream(stream)>>>(
+      launch_k(k_attn_smem, g2, 32 * nw, smem, as_stream(stream), 
           B * L, L, H, dh, qkv, ld_qkv, qkv_dtype, 0, qkv, ld_qkv, qkv_dtype, D, 2 * D, L, nullptr,
           lengths, attn_scale(dh), ctx, ldc, ctx_dtype);
       SKB_CHECK_LAUNCH("k_attn_smem(encoder)");
@@ -491,7 +496,7 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
     }
   }
   dim3 grid(B * H, (L + 7) / 8);
-  k_encoder_attention<<<grid, 256, 0, as_stream(stream)>>>(B, L, H, dh, qkv, ld_qkv, qkv_dtype,
+  launch_k(k_encoder_attention, grid, 256, 0, as_stream(stream), B, L, H, dh, qkv, ld_qkv, qkv_dtype,
                                                            lengths, attn_scale(dh), ctx, ldc, ctx_dtype);
   SKB_CHECK_LAUNCH("k_encoder_attention");
   return SKB_OK;
@@ -513,19 +518,19 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
     auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
     const float sc = attn_scale(dh);
     if (dh == 64)
-      k_self_attn_vec<64><<<grid, 128, 0, as_stream(stream)>>>(R, H, qkv, ld_qkv, qkv_dtype, k, v,
+      launch_k(k_self_attn_vec<64>, grid, 128, 0, as_stream(stream), R, H, qkv, ld_qkv, qkv_dtype, k, v,
                                                                S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     else if (dh == 32)
-      k_self_attn_vec<32><<<grid, 128, 0, as_stream(stream)>>>(R, H, qkv, ld_qkv, qkv_dtype, k, v,
+      launch_k(k_self_attn_vec<32>, grid, 128, 0, as_stream(stream), R, H, qkv, ld_qkv, qkv_dtype, k, v,
                                                                S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     else
-      k_self_attn_vec<128><<<grid, 128, 0, as_stream(stream)>>>(R, H, qkv, ld_qkv, qkv_dtype, k, v,
+      launch_k(k_self_attn_vec<128>, grid, 128, 0, as_stream(stream), R, H, qkv, ld_qkv, qkv_dtype, k, v,
                                                                 S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     SKB_CHECK_LAUNCH("k_self_attn_vec");
     return SKB_OK;
   }
   const int warps = R * H;
-  k_self_attention_step<<<(warps + 3) / 4, 128, 0, as_stream(stream)>>>(
+  launch_k(k_self_attention_step, (warps + 3) / 4, 128, 0, as_stream(stream), 
       R, H, dh, qkv, ld_qkv, qkv_dtype, kc, vc, cache_dtype, S_max, anc, step, attn_scale(dh), ctx,
       ldc, ctx_dtype);
   SKB_CHECK_LAUNCH("k_self_attention_step");
@@ -551,7 +556,7 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
         attr = true;
       }
       dim3 g2((R + G - 1) / G, H);
-      k_attn_smem<<<g2, 32 * nw, smem, as_stream(stream)>>>(R, G, H, dh, q, ldq, q_dtype, 0, kv,
+      launch_k(k_attn_smem, g2, 32 * nw, smem, as_stream(stream), R, G, H, dh, q, ldq, q_dtype, 0, kv,
                                                             ld_kv, kv_dtype, koff, voff, L, row_sent,
                                                             lengths, attn_scale(dh), ctx, ldc,
                                                             ctx_dtype);
@@ -560,7 +565,7 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
     }
   }
   const int warps = R * H;
-  k_cross_attention_step<<<(warps + 3) / 4, 128, 0, as_stream(stream)>>>(
+  launch_k(k_cross_attention_step, (warps + 3) / 4, 128, 0, as_stream(stream), 
       R, H, dh, q, ldq, q_dtype, kv, ld_kv, kv_dtype, koff, voff, L, row_sent, lengths,
       attn_scale(dh), ctx, ldc, ctx_dtype);
   SKB_CHECK_LAUNCH("k_cross_attention_step");

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/skiff_b200.h"
 
@@ -26,6 +27,41 @@ int fail(int code, const char *fmt, ...);
   } while (0)
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------- programmatic dependent launch
+// Every kernel of the decode step is launched with programmatic stream
+// serialization: the next kernel's CTAs are scheduled while the current one
+// drains, run their prologue (barrier init, TMEM alloc, descriptor and
+// weight prefetch), and block in griddepcontrol.wait until the predecessor
+// grid has completed and its writes are visible.  Kernels therefore touch no
+// predecessor-produced memory before pdl_wait().  SKB_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#define PDL_ENTRY()        \
+  do {                     \
+    ::skb::pdl_wait();     \
+    ::skb::pdl_trigger();  \
+  } while (0)
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t stream, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------- element access
 __device__ __forceinline__ float load_f(const void *p, int dtype, size_t i) {

@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(256) k_layernorm(int rows, int d, const float 
                                                    int ldx, const float *__restrict__ gain,
                                                    const float *__restrict__ bias, float eps,
                                                    void *out, int ldo, int out_dtype) {
+  PDL_ENTRY();
   const int warp = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const float *xr = x + (size_t)warp * ldx;
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(256) k_layernorm_reg(int rows, const float *__
                                                        int ldx, const float *__restrict__ gain,
                                                        const float *__restrict__ bias, float eps,
                                                        void *out, int ldo, int out_dtype) {
+  PDL_ENTRY();
   constexpr int d = NV * 128;
   const int warp = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -121,6 +123,7 @@ __global__ void k_embed_target(int rows, int d, const int *__restrict__ tok,
                                const int *__restrict__ step, int n_factors,
                                const int *__restrict__ ftok, const float *const *__restrict__ ftables,
                                float *__restrict__ x) {
+  PDL_ENTRY();
   const int r = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows || c >= d) return;
@@ -144,6 +147,7 @@ __global__ void k_embed_source(int B, int L, int d, int ds, const int *__restric
                                const float *__restrict__ E, const float *__restrict__ pe,
                                SrcFactors f, const int *__restrict__ fids,
                                const float *const *__restrict__ ftables, float *__restrict__ x) {
+  PDL_ENTRY();
   const int row = blockIdx.y;  // b*L + l
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= B * L || c >= d) return;
@@ -167,6 +171,7 @@ __global__ void k_embed_source(int B, int L, int d, int ds, const int *__restric
 __global__ void k_gather_rows(int n, int w, const uint8_t *__restrict__ table, size_t ld_bytes,
                               const int *__restrict__ idx, uint8_t *__restrict__ out,
                               size_t ldo_bytes, int row_bytes) {
+  PDL_ENTRY();
   const int i = blockIdx.x;
   if (i >= n) return;
   const uint8_t *src = table + (size_t)idx[i] * ld_bytes;
@@ -184,6 +189,7 @@ __global__ void k_gather_rows(int n, int w, const uint8_t *__restrict__ table, s
 // model.py:496-500 (kernels.py masked_max): max over unpadded positions.
 __global__ void k_masked_maxpool(int B, int L, int d, const float *__restrict__ enc,
                                  const int *__restrict__ lengths, float *__restrict__ out) {
+  PDL_ENTRY();
   const int b = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || c >= d) return;
@@ -208,15 +214,15 @@ extern "C" int skb_layernorm(int rows, int d, const float *x, int ldx, const flo
   const int blocks = (rows + 7) / 8;
   cudaStream_t s = as_stream(stream);
   if (aligned && d == 1024)
-    k_layernorm_reg<8><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+    launch_k(k_layernorm_reg<8>, blocks, 256, 0, s, rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   else if (aligned && d == 512)
-    k_layernorm_reg<4><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+    launch_k(k_layernorm_reg<4>, blocks, 256, 0, s, rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   else if (aligned && d == 256)
-    k_layernorm_reg<2><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+    launch_k(k_layernorm_reg<2>, blocks, 256, 0, s, rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   else if (aligned && d == 2048)
-    k_layernorm_reg<16><<<blocks, 256, 0, s>>>(rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+    launch_k(k_layernorm_reg<16>, blocks, 256, 0, s, rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   else
-    k_layernorm<<<blocks, 256, 0, s>>>(rows, d, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+    launch_k(k_layernorm, blocks, 256, 0, s, rows, d, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   SKB_CHECK_LAUNCH("k_layernorm");
   return SKB_OK;
 }
@@ -227,7 +233,7 @@ extern "C" int skb_embed_target(int rows, int d, const int *tok, const float *E,
   if (rows < 0 || d <= 0) return fail(SKB_ERR_SHAPE, "embed_target: rows=%d d=%d", rows, d);
   if (rows == 0) return SKB_OK;
   dim3 grid((d + 255) / 256, rows);
-  k_embed_target<<<grid, 256, 0, as_stream(stream)>>>(rows, d, tok, E, pe, step, n_factors, ftok,
+  launch_k(k_embed_target, grid, 256, 0, as_stream(stream), rows, d, tok, E, pe, step, n_factors, ftok,
                                                       ftables, x);
   SKB_CHECK_LAUNCH("k_embed_target");
   return SKB_OK;
@@ -253,7 +259,7 @@ extern "C" int skb_embed_source(int B, int L, int d, int ds, const int *ids, con
   }
   if (off != d) return fail(SKB_ERR_CONFIG, "embed_source: concat widths do not fill d");
   dim3 grid((d + 255) / 256, B * L);
-  k_embed_source<<<grid, 256, 0, as_stream(stream)>>>(B, L, d, ds, ids, E, pe, f, fids, ftables, x);
+  launch_k(k_embed_source, grid, 256, 0, as_stream(stream), B, L, d, ds, ids, E, pe, f, fids, ftables, x);
   SKB_CHECK_LAUNCH("k_embed_source");
   return SKB_OK;
 }
@@ -263,7 +269,7 @@ extern "C" int skb_gather_rows(int n, int w, const void *table, int ld_table, co
   if (n < 0 || w <= 0) return fail(SKB_ERR_SHAPE, "gather_rows: n=%d w=%d", n, w);
   if (n == 0) return SKB_OK;
   const size_t es = dtype == SKB_F32 ? 4 : 2;
-  k_gather_rows<<<n, 128, 0, as_stream(stream)>>>(n, w, (const uint8_t *)table, ld_table * es, idx,
+  launch_k(k_gather_rows, n, 128, 0, as_stream(stream), n, w, (const uint8_t *)table, ld_table * es, idx,
                                                   (uint8_t *)out, ld_out * es, (int)(w * es));
   SKB_CHECK_LAUNCH("k_gather_rows");
   return SKB_OK;
@@ -273,7 +279,7 @@ extern "C" int skb_masked_maxpool(int B, int L, int d, const float *enc, const i
                                   float *out, void *stream) {
   if (B <= 0 || L <= 0 || d <= 0) return fail(SKB_ERR_SHAPE, "masked_maxpool: bad shape");
   dim3 grid((d + 255) / 256, B);
-  k_masked_maxpool<<<grid, 256, 0, as_stream(stream)>>>(B, L, d, enc, lengths, out);
+  launch_k(k_masked_maxpool, grid, 256, 0, as_stream(stream), B, L, d, enc, lengths, out);
   SKB_CHECK_LAUNCH("k_masked_maxpool");
   return SKB_OK;
 }
@@ -281,6 +287,7 @@ extern "C" int skb_masked_maxpool(int B, int L, int d, const float *enc, const i
 // ----------------------------------------------------- dtype conversion
 namespace skb {
 __global__ void k_convert(size_t n, const void *src, int sdt, void *dst, int ddt) {
+  PDL_ENTRY();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     store_f(dst, ddt, i, load_f(src, sdt, i));
@@ -289,6 +296,7 @@ __global__ void k_convert(size_t n, const void *src, int sdt, void *dst, int ddt
 // NVS selection (model.py:511-517): bit c of row b set iff
 // sigmoid(logit[b, c]) > threshold (threshold rounded to float32).
 __global__ void k_nvs_mask(int B, int V, const float *logits, int ld, float thr, unsigned *mask) {
+  PDL_ENTRY();
   const int b = blockIdx.y;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int words = (V + 31) >> 5;
@@ -304,7 +312,7 @@ extern "C" int skb_convert(long long n, const void *src, int src_dtype, void *ds
   if (n == 0) return SKB_OK;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_convert<<<blocks, 256, 0, as_stream(stream)>>>((size_t)n, src, src_dtype, dst, dst_dtype);
+  launch_k(k_convert, blocks, 256, 0, as_stream(stream), (size_t)n, src, src_dtype, dst, dst_dtype);
   SKB_CHECK_LAUNCH("k_convert");
   return SKB_OK;
 }
@@ -313,7 +321,7 @@ extern "C" int skb_nvs_mask(int B, int V, const float *logits, int ld, float thr
                             unsigned *mask, void *stream) {
   if (B <= 0 || V <= 0) return fail(SKB_ERR_SHAPE, "nvs_mask: bad shape");
   dim3 grid((V + 255) / 256, B);
-  k_nvs_mask<<<grid, 256, 0, as_stream(stream)>>>(B, V, logits, ld, threshold, mask);
+  launch_k(k_nvs_mask, grid, 256, 0, as_stream(stream), B, V, logits, ld, threshold, mask);
   SKB_CHECK_LAUNCH("k_nvs_mask");
   return SKB_OK;
 }

@@ -1,6 +1,8 @@
 // Thread-local error message + status plumbing for the C ABI.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace skb {
 
 static thread_local char g_err[512] = "";
@@ -18,6 +20,15 @@ int fail(int code, const char *fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
   return code;
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SKB_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 }  // namespace skb

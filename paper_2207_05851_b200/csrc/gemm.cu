@@ -381,6 +381,23 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // PDL prologue: the weight (B) tiles of the first pipeline stages do
+      // not depend on the previous kernel, so they are fetched while it
+      // drains; activations (A) only after griddepcontrol.wait.
+      int pre = 0;
+      int pm0 = 0, pn0 = 0;
+      if ((int)blockIdx.x < num_units) {
+        int tile, split, kb0, kb1;
+        decode(blockIdx.x, pm0, pn0, tile, split, kb0, kb1);
+        pre = min(C::STAGES, kb1 - kb0);
+        for (int q = 0; q < pre; ++q) {
+          uint8_t *sa = smem + q * C::STAGE_BYTES;
+          mbar_expect_tx(&full[q], C::STAGE_BYTES);
+          tma_load_2d(sa + C::A_BYTES, &tmB, (kb0 + q) * BK, pn0, &full[q]);
+        }
+      }
+      pdl_wait();
+      pdl_trigger();
       int it = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
         int m0, n0, tile, split, kb0, kb1;
@@ -388,15 +405,22 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
           uint8_t *sa = smem + s * C::STAGE_BYTES;
+          if (it < pre) {  // B already in flight for this stage
+            tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
+            continue;
+          }
+          mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
           tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
           tma_load_2d(sa + C::A_BYTES, &tmB, kb * BK, n0, &full[s]);
         }
       }
+    } else {
+      pdl_wait();
     }
   } else if (warp == 1) {
+    pdl_wait();
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
       int it = 0, local = 0;
@@ -426,6 +450,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---- epilogue warps 2..5
+    pdl_wait();
     const int quarter = warp & 3;
     const bool vec_ok = ep.kind != SKB_EPI_SSRU && (ep.ldo % 8 == 0) &&
                         ((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0);
@@ -613,7 +638,7 @@ static int launch(int M, int N, int K, const void *A, int lda, const void *W, in
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
   const int nsm = num_sms();
   const int grid = tiles < nsm ? tiles : nsm;
-  k_gemm_tc<BN><<<grid, 192, C::SMEM, st>>>(ma, mb, M, N, K, ep);
+  launch_k(k_gemm_tc<BN>, grid, 192, C::SMEM, st, ma, mb, M, N, K, ep);
   SKB_CHECK_LAUNCH("k_gemm_tc");
   return SKB_OK;
 }
@@ -627,6 +652,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_gemm_simt(int M, int N, int K, const T *__restrict__ A,
                                                    int lda, const T *__restrict__ W, int ldw,
                                                    EpiArgs ep) {
+  PDL_ENTRY();
   constexpr int TM = 64, TN = 64, TK = 16;
   __shared__ float As[TK][TM + 4];
   __shared__ float Ws[TK][TN + 4];
@@ -726,9 +752,9 @@ static int gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, 
                      int ldw, const EpiArgs &ep, cudaStream_t st) {
   dim3 grid((N + 63) / 64, (M + 63) / 64);
   if (in_dtype == SKB_F32)
-    k_gemm_simt<float><<<grid, 256, 0, st>>>(M, N, K, (const float *)A, lda, (const float *)W, ldw, ep);
+    launch_k(k_gemm_simt<float>, grid, 256, 0, st, M, N, K, (const float *)A, lda, (const float *)W, ldw, ep);
   else
-    k_gemm_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(M, N, K, (const __nv_bfloat16 *)A, lda,
+    launch_k(k_gemm_simt<__nv_bfloat16>, grid, 256, 0, st, M, N, K, (const __nv_bfloat16 *)A, lda,
                                                      (const __nv_bfloat16 *)W, ldw, ep);
   SKB_CHECK_LAUNCH("k_gemm_simt");
   return SKB_OK;

@@ -162,6 +162,7 @@ struct BeamSmem {
 template <int MAXK>
 __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict__ logits, int ld,
                                                           int lp_in, skb_beam_state st) {
+  PDL_ENTRY();
   extern __shared__ __align__(16) uint8_t beam_smem[];
   BeamSmem<MAXK> &sm = *reinterpret_cast<BeamSmem<MAXK> *>(beam_smem);
   float2 *part_s = reinterpret_cast<float2 *>(beam_smem + ((sizeof(BeamSmem<MAXK>) + 15) & ~size_t(15)));
@@ -537,6 +538,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
 
 // ------------------------------------------------------------- reorder
 __global__ void k_beam_reorder(int R, int S_max, int *anc, const int *parent, const int *step) {
+  PDL_ENTRY();
   const int r = blockIdx.y;
   const int t = *step;
   const int p = parent[r];
@@ -547,10 +549,12 @@ __global__ void k_beam_reorder(int R, int S_max, int *anc, const int *parent, co
     dst[pos] = pos == t ? p : src[pos];
 }
 
-__global__ void k_step_advance(int *step) { *step += 1; }
+__global__ void k_step_advance(int *step) {
+  PDL_ENTRY(); *step += 1; }
 
 // ------------------------------------------------------------ finalize
 __global__ void k_beam_finalize(skb_beam_state st, int *tokens_out, int *factors_out) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= st.B) return;
   const int K = st.K, R = st.B * K, nf = st.n_factors;
@@ -588,7 +592,7 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
     const size_t smem = ((base_smem + 15) & ~size_t(15)) + (sv.stage_partials ? part_bytes : 0);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern_ptr<<<sv.B, threads, smem, s>>>(logits, ld_logits, lp_in, sv);
+    launch_k(kern_ptr, sv.B, threads, smem, s, logits, ld_logits, lp_in, sv);
   };
   const int th = sv.K * 32;
   if (sv.K <= 1)
@@ -624,9 +628,9 @@ extern "C" int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, i
   if (R <= 0 || S_max <= 0) return fail(SKB_ERR_SHAPE, "beam_reorder: bad shape");
   cudaStream_t s = as_stream(stream);
   dim3 grid((S_max + 127) / 128, R);
-  k_beam_reorder<<<grid, 128, 0, s>>>(R, S_max, anc, parent, step);
+  launch_k(k_beam_reorder, grid, 128, 0, s, R, S_max, anc, parent, step);
   SKB_CHECK_LAUNCH("k_beam_reorder");
-  k_step_advance<<<1, 1, 0, s>>>(step);
+  launch_k(k_step_advance, 1, 1, 0, s, step);
   SKB_CHECK_LAUNCH("k_step_advance");
   return SKB_OK;
 }
@@ -634,7 +638,7 @@ extern "C" int skb_beam_reorder(int R, int S_max, int *anc, const int *parent, i
 extern "C" int skb_beam_finalize(const skb_beam_state *st, int *tokens_out, int *factors_out,
                                  void *stream) {
   if (!st || st->B <= 0) return fail(SKB_ERR_SHAPE, "beam_finalize: bad state");
-  k_beam_finalize<<<(st->B + 127) / 128, 128, 0, as_stream(stream)>>>(*st, tokens_out, factors_out);
+  launch_k(k_beam_finalize, (st->B + 127) / 128, 128, 0, as_stream(stream), *st, tokens_out, factors_out);
   SKB_CHECK_LAUNCH("k_beam_finalize");
   return SKB_OK;
 }
