@@ -818,7 +818,15 @@ extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int ld
     return rounds * (bytes + 96.0 * 1024);  // + fixed per-unit overhead
   };
   int best_s = 1;
-  if (can_split) {
+  // Split-K is opt-in (SKB_GEMM_SPLITK=1): measured on B200 at the decode
+  // shapes, the partial-tile round trip through L2 costs more than the extra
+  // SMs gain (tools/bench_gemm.py sweep, profiles/r1_gemm_sweep.txt).
+  static int splitk_on = -1;
+  if (splitk_on < 0) {
+    const char *e = getenv("SKB_GEMM_SPLITK");
+    splitk_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (can_split && splitk_on) {
     const int ss[6] = {1, 2, 3, 4, 6, 8};
     double best = 1e30;
     for (int si = 0; si < 6; ++si) {
