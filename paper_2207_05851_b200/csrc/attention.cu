@@ -468,6 +468,174 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
 
 static float attn_scale(int dh) { return (float)(1.0 / sqrt((double)dh)); }
 
+// ------------------------- grouped attention, bf16 K/V in shared memory
+// Same contract as k_attn_smem for bf16 operands with d_h in {32,64,128}:
+// the (sentence, head) K/V slice is copied raw (cp.async, 16 B) into shared
+// memory, and each warp serves one query row with DH/8 lanes per key (one
+// 16-byte LDS of K or V each, 32*8/DH keys per instruction), online softmax
+// over 32-key chunks.
+template <int DH>
+__global__ void __launch_bounds__(256) k_attn_smem_vec(
+    int R, int G, int H, const __nv_bfloat16 *q, int ldq, const __nv_bfloat16 *kv, int ld_kv,
+    int koff, int voff, int L, const int *row_sent, const int *lengths, float scale, void *ctx,
+    int ldc, int ctx_dtype) {
+  PDL_ENTRY();
+  constexpr int LPK = DH / 8;
+  constexpr int KPI = 32 / LPK;
+  constexpr int ITER = 32 / KPI;
+  extern __shared__ __align__(16) uint8_t av_smem[];
+  uint4 *Ks = reinterpret_cast<uint4 *>(av_smem);   // [L][LPK]
+  uint4 *Vs = Ks + (size_t)L * LPK;
+  const int g = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int row0 = g * G;
+  const int b = row_sent ? row_sent[row0] : g;
+  const int len = lengths[b];
+  for (int idx = threadIdx.x; idx < len * LPK; idx += blockDim.x) {
+    const int j = idx / LPK, c = idx - j * LPK;
+    const size_t kr = (size_t)(b * L + j) * ld_kv + h * DH + c * 8;
+    const uint32_t dk = static_cast<uint32_t>(__cvta_generic_to_shared(Ks + idx));
+    const uint32_t dv = static_cast<uint32_t>(__cvta_generic_to_shared(Vs + idx));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dk), "l"(kv + kr + koff) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dv), "l"(kv + kr + voff) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int sub = lane % LPK, grp = lane / LPK;
+  for (int i = warp; i < G; i += nw) {
+    const int r = row0 + i;
+    if (r >= R) break;
+    float q8[8];
+    {
+      const uint4 qv = *reinterpret_cast<const uint4 *>(q + (size_t)r * ldq + h * DH + sub * 8);
+      const __nv_bfloat162 *qp = reinterpret_cast<const __nv_bfloat162 *>(&qv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(qp[u]);
+        q8[2 * u] = f.x * scale;  // fold 1/sqrt(d_h) into q (one multiply per dim)
+        q8[2 * u + 1] = f.y * scale;
+      }
+    }
+    float m_run = -INFINITY, l_run = 0.f;
+    float o8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o8[u] = 0.f;
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      float sc[ITER];
+      float cmax = -INFINITY;
+#pragma unroll
+      for (int it = 0; it < ITER; ++it) {
+        const int j = j0 + it * KPI + grp;
+        float a = 0.f;
+        if (j < len) {
+          const uint4 kk = Ks[(size_t)j * LPK + sub];
+          const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kk);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 f = __bfloat1622float2(kp[u]);
+            a = fmaf(q8[2 * u], f.x, a);
+            a = fmaf(q8[2 * u + 1], f.y, a);
+          }
+        }
+#pragma unroll
+        for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        sc[it] = j < len ? a : -INFINITY;
+        cmax = fmaxf(cmax, sc[it]);
+      }
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      const float mnew = fmaxf(m_run, cmax);
+      const float corr = m_run == -INFINITY ? 0.f : expf(m_run - mnew);
+      float psum = 0.f;
+#pragma unroll
+      for (int it = 0; it < ITER; ++it) {
+        sc[it] = sc[it] == -INFINITY ? 0.f : expf(sc[it] - mnew);
+        psum += sc[it];
+      }
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+      l_run = l_run * corr + psum;
+      m_run = mnew;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o8[u] *= corr;
+#pragma unroll
+      for (int it = 0; it < ITER; ++it) {
+        const int j = j0 + it * KPI + grp;
+        if (j >= len) continue;
+        const uint4 vv = Vs[(size_t)j * LPK + sub];
+        const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = __bfloat1622float2(vp[u]);
+          o8[2 * u] = fmaf(sc[it], f.x, o8[2 * u]);
+          o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) o8[u] += __shfl_xor_sync(0xffffffffu, o8[u], o);
+    if (grp == 0) {
+      const float inv = 1.0f / l_run;
+      const size_t ob = (size_t)r * ldc + h * DH + sub * 8;
+      if (ctx_dtype == SKB_BF16) {
+        uint4 w;
+        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          __nv_bfloat162 pr = __floats2bfloat162_rn(o8[2 * u] * inv, o8[2 * u + 1] * inv);
+          wp[u] = *reinterpret_cast<uint32_t *>(&pr);
+        }
+        *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(ctx) + ob) = w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) reinterpret_cast<float *>(ctx)[ob + u] = o8[u] * inv;
+      }
+    }
+  }
+}
+
+// Dispatch helper for the grouped attention (cross and encoder).
+static bool attn_vec_ok(int dh, int q_dtype, int kv_dtype, const void *q, int ldq, const void *kv,
+                        int ld_kv, int koff, int voff, int qoff) {
+  return (dh == 32 || dh == 64 || dh == 128) && q_dtype == SKB_BF16 && kv_dtype == SKB_BF16 &&
+         ldq % 8 == 0 && ld_kv % 8 == 0 && koff % 8 == 0 && voff % 8 == 0 && qoff % 8 == 0 &&
+         ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv)) & 15) == 0;
+}
+
+static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, int qoff,
+                           const void *kv, int ld_kv, int koff, int voff, int L, const int *row_sent,
+                           const int *lengths, float scale, void *ctx, int ldc, int ctx_dtype,
+                           cudaStream_t st) {
+  const int nw = G < 8 ? G : 8;
+  const size_t smem = (size_t)2 * L * dh * sizeof(__nv_bfloat16);
+  if (smem > 200 * 1024) return -1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_smem_vec<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_attn_smem_vec<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_attn_smem_vec<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid((R + G - 1) / G, H);
+  auto *qb = reinterpret_cast<const __nv_bfloat16 *>(q) + qoff;
+  auto *kb = reinterpret_cast<const __nv_bfloat16 *>(kv);
+  if (dh == 64)
+    launch_k(k_attn_smem_vec<64>, grid, 32 * nw, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
+             row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+  else if (dh == 32)
+    launch_k(k_attn_smem_vec<32>, grid, 32 * nw, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
+             row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+  else
+    launch_k(k_attn_smem_vec<128>, grid, 32 * nw, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff,
+             L, row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+  return 0;
+}
+
+
+
 }  // namespace skb
 
 using namespace skb;
@@ -477,6 +645,12 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
                                      int ctx_dtype, void *stream) {
   if (B <= 0 || L <= 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "encoder_attention: shape");
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "encoder_attention: head dim %d > %d", dh, MAX_DH);
+  if (attn_vec_ok(dh, qkv_dtype, qkv_dtype, qkv, ld_qkv, qkv, ld_qkv, H * dh, 2 * H * dh, 0) &&
+      launch_attn_vec(B * L, L, H, dh, qkv, ld_qkv, 0, qkv, ld_qkv, H * dh, 2 * H * dh, L, nullptr,
+                      lengths, attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream)) == 0) {
+    SKB_CHECK_LAUNCH("k_attn_smem_vec(encoder)");
+    return SKB_OK;
+  }
   {
     const int nw = L < 8 ? L : 8;
     const size_t smem = ((size_t)2 * L * (dh + 1) + (size_t)nw * dh) * sizeof(float);
@@ -546,6 +720,12 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "cross_attention_step: head dim %d", dh);
   if (R == 0) return SKB_OK;
   const int G = rows_per_group > 0 ? rows_per_group : 1;
+  if (attn_vec_ok(dh, q_dtype, kv_dtype, q, ldq, kv, ld_kv, koff, voff, 0) &&
+      launch_attn_vec(R, G, H, dh, q, ldq, 0, kv, ld_kv, koff, voff, L, row_sent, lengths,
+                      attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream)) == 0) {
+    SKB_CHECK_LAUNCH("k_attn_smem_vec(cross)");
+    return SKB_OK;
+  }
   {
     const int nw = G < 8 ? G : 8;
     const size_t smem = ((size_t)2 * L * (dh + 1) + (size_t)nw * dh) * sizeof(float);
