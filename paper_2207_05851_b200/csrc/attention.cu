@@ -16,6 +16,8 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace skb {
 
 constexpr int MAX_DH = 128;
@@ -597,6 +599,186 @@ __global__ void __launch_bounds__(256) k_attn_smem_vec(
   }
 }
 
+// ------------------- grouped attention on tensor cores (mma.sync, bf16)
+// One warp computes 16 query rows x one head with m16n8k16 MMAs: S = Q K^T
+// over 64-key chunks (fp32 accumulators), online softmax on the C fragments,
+// then O += P V with P re-used in registers as the A operand and V fetched
+// transposed by ldmatrix.  The (sentence, head) K/V slice is staged in
+// shared memory once (cp.async, rows padded to DH+8 bf16 = conflict-free).
+// Used for cross-attention (16 beam rows of a sentence per warp) and the
+// encoder (L query rows of a sentence, 16 per warp).
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4],
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&p);
+}
+
+template <int DH>
+__global__ void __launch_bounds__(128) k_attn_mma(
+    int R, int G, int H, const __nv_bfloat16 *q, int ldq, const __nv_bfloat16 *kv, int ld_kv,
+    int koff, int voff, int L, const int *row_sent, const int *lengths, float scale, void *ctx,
+    int ldc, int ctx_dtype) {
+  PDL_ENTRY();
+  constexpr int LD = DH + 8;        // padded smem row (bf16)
+  constexpr int KC = 64;            // keys per chunk
+  extern __shared__ __align__(16) uint8_t am_smem[];
+  __nv_bfloat16 *Ks = reinterpret_cast<__nv_bfloat16 *>(am_smem);      // [Lp][LD]
+  const int Lp = (L + KC - 1) / KC * KC;
+  __nv_bfloat16 *Vs = Ks + (size_t)Lp * LD;
+  const int g = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int row0 = g * G;
+  const int b = row_sent ? row_sent[row0] : g;
+  const int len = lengths[b];
+  const int CP = DH / 8;  // 16-byte chunks per row
+  for (int idx = threadIdx.x; idx < Lp * CP; idx += blockDim.x) {
+    const int j = idx / CP, c = idx - j * CP;
+    __nv_bfloat16 *dk = Ks + (size_t)j * LD + c * 8;
+    __nv_bfloat16 *dv = Vs + (size_t)j * LD + c * 8;
+    if (j < len) {
+      const size_t kr = (size_t)(b * L + j) * ld_kv + h * DH + c * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(dk))),
+                   "l"(kv + kr + koff)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(dv))),
+                   "l"(kv + kr + voff)
+                   : "memory");
+    } else {  // zero padding keys (masked below; V must be finite)
+      *reinterpret_cast<uint4 *>(dk) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4 *>(dv) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int gq = lane >> 2, tq = lane & 3;  // fragment row group / thread-in-group
+  for (int rt = warp * 16; rt < G; rt += nw * 16) {
+    // ---- Q fragments (A operand, row-major): rows rt+gq and rt+gq+8
+    uint32_t qa[DH / 16][4];
+    const int ra = row0 + rt + gq, rb = ra + 8;
+    const bool va = rt + gq < G && ra < R, vb = rt + gq + 8 < G && rb < R;
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      const int c0 = ks * 16 + tq * 2;
+      const __nv_bfloat16 *qa_p = q + (size_t)ra * ldq + h * DH;
+      const __nv_bfloat16 *qb_p = q + (size_t)rb * ldq + h * DH;
+      qa[ks][0] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0) : 0u;
+      qa[ks][1] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0) : 0u;
+      qa[ks][2] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0 + 8) : 0u;
+      qa[ks][3] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0 + 8) : 0u;
+    }
+    float o[DH / 8][4];
+#pragma unroll
+    for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+    for (int j0 = 0; j0 < len; j0 += KC) {
+      // ---- S = Q K^T for 64 keys (8 n-tiles)
+      float sc[KC / 8][4];
+#pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt) {
+        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+        const __nv_bfloat16 *krow = Ks + (size_t)(j0 + nt * 8 + gq) * LD;
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t *>(krow + ks * 16 + tq * 2);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t *>(krow + ks * 16 + tq * 2 + 8);
+          mma_bf16_16816(sc[nt], qa[ks], b0, b1);
+        }
+      }
+      // ---- scale, mask, online softmax (rows gq and gq+8; 4 lanes share a row)
+      float cm_a = -INFINITY, cm_b = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = j0 + nt * 8 + tq * 2 + e < len;
+          sc[nt][e] = ok ? sc[nt][e] * scale : -INFINITY;
+          sc[nt][2 + e] = ok ? sc[nt][2 + e] * scale : -INFINITY;
+          cm_a = fmaxf(cm_a, sc[nt][e]);
+          cm_b = fmaxf(cm_b, sc[nt][2 + e]);
+        }
+#pragma unroll
+      for (int o2 = 1; o2 < 4; o2 <<= 1) {
+        cm_a = fmaxf(cm_a, __shfl_xor_sync(0xffffffffu, cm_a, o2));
+        cm_b = fmaxf(cm_b, __shfl_xor_sync(0xffffffffu, cm_b, o2));
+      }
+      const float mn_a = fmaxf(m_a, cm_a), mn_b = fmaxf(m_b, cm_b);
+      const float cr_a = m_a == -INFINITY ? 0.f : expf(m_a - mn_a);
+      const float cr_b = m_b == -INFINITY ? 0.f : expf(m_b - mn_b);
+      float ps_a = 0.f, ps_b = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < KC / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          sc[nt][e] = sc[nt][e] == -INFINITY ? 0.f : expf(sc[nt][e] - mn_a);
+          sc[nt][2 + e] = sc[nt][2 + e] == -INFINITY ? 0.f : expf(sc[nt][2 + e] - mn_b);
+          ps_a += sc[nt][e];
+          ps_b += sc[nt][2 + e];
+        }
+#pragma unroll
+      for (int o2 = 1; o2 < 4; o2 <<= 1) {
+        ps_a += __shfl_xor_sync(0xffffffffu, ps_a, o2);
+        ps_b += __shfl_xor_sync(0xffffffffu, ps_b, o2);
+      }
+      l_a = l_a * cr_a + ps_a;
+      l_b = l_b * cr_b + ps_b;
+      m_a = mn_a;
+      m_b = mn_b;
+#pragma unroll
+      for (int n = 0; n < DH / 8; ++n) {
+        o[n][0] *= cr_a; o[n][1] *= cr_a;
+        o[n][2] *= cr_b; o[n][3] *= cr_b;
+      }
+      // ---- O += P V: P's C fragments become A fragments (16 keys per k-step)
+#pragma unroll
+      for (int kk = 0; kk < KC / 16; ++kk) {
+        uint32_t pa[4];
+        pa[0] = pack_bf16(sc[2 * kk][0], sc[2 * kk][1]);
+        pa[1] = pack_bf16(sc[2 * kk][2], sc[2 * kk][3]);
+        pa[2] = pack_bf16(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+        pa[3] = pack_bf16(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+        // V rows (keys) j0+16kk .. +15, transposed by ldmatrix into B frags
+        const int vrow = j0 + kk * 16 + (lane & 15);
+#pragma unroll
+        for (int n = 0; n < DH / 8; ++n) {
+          const uint32_t addr = static_cast<uint32_t>(
+              __cvta_generic_to_shared(Vs + (size_t)vrow * LD + n * 8));
+          uint32_t b0, b1;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                       : "=r"(b0), "=r"(b1)
+                       : "r"(addr));
+          mma_bf16_16816(o[n], pa, b0, b1);
+        }
+      }
+    }
+    // ---- normalise and store rows gq, gq+8
+    const float ia = 1.0f / l_a, ib = 1.0f / l_b;
+#pragma unroll
+    for (int n = 0; n < DH / 8; ++n) {
+      const int c = h * DH + n * 8 + tq * 2;
+      if (ctx_dtype == SKB_BF16) {
+        __nv_bfloat16 *cb = reinterpret_cast<__nv_bfloat16 *>(ctx);
+        if (va) *reinterpret_cast<uint32_t *>(cb + (size_t)ra * ldc + c) = pack_bf16(o[n][0] * ia, o[n][1] * ia);
+        if (vb) *reinterpret_cast<uint32_t *>(cb + (size_t)rb * ldc + c) = pack_bf16(o[n][2] * ib, o[n][3] * ib);
+      } else {
+        float *cf = reinterpret_cast<float *>(ctx);
+        if (va) { cf[(size_t)ra * ldc + c] = o[n][0] * ia; cf[(size_t)ra * ldc + c + 1] = o[n][1] * ia; }
+        if (vb) { cf[(size_t)rb * ldc + c] = o[n][2] * ib; cf[(size_t)rb * ldc + c + 1] = o[n][3] * ib; }
+      }
+    }
+  }
+}
+
 // Dispatch helper for the grouped attention (cross and encoder).
 static bool attn_vec_ok(int dh, int q_dtype, int kv_dtype, const void *q, int ldq, const void *kv,
                         int ld_kv, int koff, int voff, int qoff) {
@@ -609,6 +791,40 @@ static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, 
                            const void *kv, int ld_kv, int koff, int voff, int L, const int *row_sent,
                            const int *lengths, float scale, void *ctx, int ldc, int ctx_dtype,
                            cudaStream_t st) {
+  {
+    // tensor-core path: one warp per 16 query rows
+    const int Lp = (L + 63) / 64 * 64;
+    const size_t smem = (size_t)2 * Lp * (dh + 8) * sizeof(__nv_bfloat16);
+    static int use_mma = -1;
+    if (use_mma < 0) {
+      const char *e = getenv("SKB_ATTN_MMA");
+      use_mma = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (use_mma && smem <= 200 * 1024 && (dh == 64 || dh == 128 || dh == 32)) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_attn_mma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_attn_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_attn_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      const int tiles = (G + 15) / 16;
+      const int nwm = tiles < 4 ? tiles : 4;
+      dim3 grid((R + G - 1) / G, H);
+      auto *qb = reinterpret_cast<const __nv_bfloat16 *>(q) + qoff;
+      auto *kb = reinterpret_cast<const __nv_bfloat16 *>(kv);
+      if (dh == 64)
+        launch_k(k_attn_mma<64>, grid, 32 * nwm, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
+                 row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+      else if (dh == 128)
+        launch_k(k_attn_mma<128>, grid, 32 * nwm, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
+                 row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+      else
+        launch_k(k_attn_mma<32>, grid, 32 * nwm, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
+                 row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+      return 0;
+    }
+  }
   const int nw = G < 8 ? G : 8;
   const size_t smem = (size_t)2 * L * dh * sizeof(__nv_bfloat16);
   if (smem > 200 * 1024) return -1;
