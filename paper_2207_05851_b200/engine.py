@@ -170,14 +170,236 @@ def nvs_active_sets(model: Model, enc, len_d, B, L, threshold, jobs) -> list[np.
     return out
 
 
+class DecodeWorkspace:
+    """Every device buffer, the initial-state image and the captured CUDA
+    graphs (encoder; 1 and CHUNK decode steps) for one batch shape.  Reused
+    by every BeamBatch of the same shape: a new batch costs one pinned H2D
+    copy of its inputs, two D2D state resets and graph replays."""
+
+    CHUNK = 8
+
+    def __init__(self, model: Model, B: int, L: int, S_max: int, K: int, P: int, U: int,
+                 alpha: float, restricted: bool):
+        c = model.config
+        dev = model.device
+        nf, nsf = len(c.target_factor_specs), len(c.source_factor_specs)
+        self.model, self.B, self.L, self.S_max, self.K, self.P, self.U = model, B, L, S_max, K, P, U
+        self.nf, self.nsf, self.restricted = nf, nsf, restricted
+        R = B * K
+        self.R = R
+        nf1 = max(nf, 1)
+        # ---- per-batch inputs: one int32 arena filled by one H2D copy
+        self.in_sizes = dict(ids=B * L, fids=max(nsf, 1) * B * L, lengths=B, max_len=B,
+                             prefix_len=B, prefix_col=B * P, prefix_fac=B * nf1 * P,
+                             col_token=U if restricted else 1,
+                             mask=B * ((U + 31) // 32) if restricted else 1)
+        tot = sum(self.in_sizes.values())
+        self.in_host = torch.zeros(tot, dtype=I32, pin_memory=True)
+        self.in_dev = torch.zeros(tot, dtype=I32, device=dev)
+        self.inp = {}
+        off = 0
+        for k, n in self.in_sizes.items():
+            self.inp[k] = self.in_dev[off:off + n]
+            off += n
+        self.inp_host = {}
+        off = 0
+        for k, n in self.in_sizes.items():
+            self.inp_host[k] = self.in_host[off:off + n]
+            off += n
+        # ---- decode state: int32 / float64 arenas reset from init images
+        st_sizes = dict(n_alive=B, done=B, counter=B, best_steps=B, best_forced=B, best_parent=B,
+                        best_fac=B * nf1, n_done=1, step=1, tok=R, ftok=nf1 * R, parent=R)
+        self.st = {}
+        tot = sum(st_sizes.values())
+        self.st_i32 = torch.zeros(tot, dtype=I32, device=dev)
+        off = 0
+        for k, n in st_sizes.items():
+            self.st[k] = self.st_i32[off:off + n]
+            off += n
+        self.st_f64 = torch.zeros(R + 2 * B, dtype=torch.float64, device=dev)
+        self.st["score"] = self.st_f64[:R]
+        self.st["best_norm"] = self.st_f64[R:R + B]
+        self.st["best_logprob"] = self.st_f64[R + B:]
+        self.st["n_alive"].fill_(1)
+        self.st["tok"].fill_(BOS_ID)
+        self.st["ftok"].fill_(SHIFT_ID)
+        self.st["parent"].copy_(torch.arange(R, dtype=I32, device=dev))
+        self.init_i32 = self.st_i32.clone()
+        self.init_f64 = self.st_f64.clone()
+        # ---- step buffers (tok/ftok/parent/step alias the state arena)
+        self.row_sent = torch.arange(R, dtype=I32, device=dev) // K
+        D2 = 2 * c.d_model * c.decoder_layers
+        ckv = torch.empty(B * L, max(D2, 1), device=dev, dtype=model.cdt)
+        E_out = torch.empty(U, c.d_model, device=dev, dtype=model.cdt) if restricted \
+            else model.E_trg_c
+        self.sb = StepBuffers(model, R, B, L, S_max, U, E_out, ckv, self.inp["lengths"],
+                              self.row_sent)
+        sb = self.sb
+        sb.step, sb.tok, sb.parent = self.st["step"], self.st["tok"], self.st["parent"]
+        sb.ftok = self.st["ftok"].view(nf1, R)
+        sb.group = K
+        sb.mask = self.inp["mask"].view(B, -1) if restricted else None
+        self.enc_bufs = model.encoder_buffers(B * L)
+        self.len_pen = torch.tensor([float(s) ** alpha if s > 0 else 1.0 for s in range(S_max + 1)],
+                                    dtype=torch.float64, device=dev)
+
+        def z(n, dt=I32):
+            return torch.zeros(n, dtype=dt, device=dev)
+
+        self.tok_hist = z(S_max * R)
+        self.par_hist = z(S_max * R)
+        self.fac_hist = z(S_max * nf1 * R)
+        self.cand_score = z(R * K, torch.float64)
+        self.cand_lp = z(R * K, torch.float32)
+        self.cand_col = z(R * K)
+        self.cand_cnt = z(R)
+        self.row_argmax = z(R)
+        self.fac_choice = z(R * nf1)
+        self.tokens_out = z(B * S_max).view(B, S_max)
+        self.factors_out = z(B * nf1 * S_max).view(B, nf1, S_max)
+        self.out_host = torch.zeros(B * S_max + B * nf1 * S_max + 2 * B, dtype=I32,
+                                    pin_memory=True)
+        self.eos_col = None
+        self.state = None
+        self.graph_enc = self.graph_1 = self.graph_n = None
+        self.launches_enc = self.launches_step = 0
+
+    def bind_state(self, eos_col: int) -> None:
+        model, sb, st, nf = self.model, self.sb, self.st, self.nf
+        self.eos_col = eos_col
+        self.state = N.BeamState(
+            self.B, self.K, self.U, self.S_max, nf, self.len_pen.data_ptr(), st["step"].data_ptr(),
+            N.ptr(self.inp["col_token"]) if self.restricted else None,
+            N.ptr(self.inp["mask"]) if self.restricted else None, eos_col,
+            self.inp["max_len"].data_ptr(), self.inp["prefix_len"].data_ptr(),
+            self.inp["prefix_col"].data_ptr(), self.P,
+            self.inp["prefix_fac"].data_ptr() if nf else None, st["n_alive"].data_ptr(),
+            st["done"].data_ptr(), st["score"].data_ptr(), st["tok"].data_ptr(),
+            st["ftok"].data_ptr(), st["parent"].data_ptr(), self.tok_hist.data_ptr(),
+            self.par_hist.data_ptr(), self.fac_hist.data_ptr(),
+            sb.fac.data_ptr() if nf else None, sb.fac.stride(0), model.fac_off.data_ptr(),
+            sb.lse_part.data_ptr(), sb.lse_part.shape[1] // 2, 1, 0,
+            self.cand_score.data_ptr(), self.cand_lp.data_ptr(), self.cand_col.data_ptr(),
+            self.cand_cnt.data_ptr(), self.row_argmax.data_ptr(), self.fac_choice.data_ptr(),
+            st["counter"].data_ptr(), st["best_norm"].data_ptr(), st["best_logprob"].data_ptr(),
+            st["best_steps"].data_ptr(), st["best_forced"].data_ptr(),
+            st["best_parent"].data_ptr(), st["best_fac"].data_ptr(), st["n_done"].data_ptr())
+
+    # ---------------------------------------------------------------- work
+    def encode(self):
+        """Encoder + all layers' cross K/V (model.py:414-430, 527-531)."""
+        m = self.model
+        enc = m.encode_device(self.inp["ids"], self.inp["fids"].view(max(self.nsf, 1), -1)
+                              if self.nsf else None, self.inp["lengths"], self.B, self.L,
+                              self.enc_bufs)
+        if m.config.decoder_layers:
+            m.cross_kv_device(enc, out=self.sb.ckv, tmp=self.enc_bufs["xc"])
+        if self.restricted:
+            kern.gather_rows(m.E_trg_c, self.inp["col_token"], self.sb.E_out)
+        return enc
+
+    def one_step(self):
+        step_forward(self.model, self.sb)
+        kern.beam_step(self.sb.logits, self.state)
+        kern.beam_reorder(self.sb.anc, self.sb.parent, self.sb.step, self.R, self.S_max)
+
+    def reset(self):
+        self.st_i32.copy_(self.init_i32, non_blocking=True)
+        self.st_f64.copy_(self.init_f64, non_blocking=True)
+
+    def _capture(self, fn, launches_attr):
+        g = torch.cuda.CUDAGraph()
+        before = kern.launches
+        with torch.cuda.graph(g):
+            fn()
+        setattr(self, launches_attr, kern.launches - before)
+        kern.launches = before  # capture does not launch
+        return g
+
+    def run(self, use_graph: bool = True, poll: bool = True) -> int:
+        """Encode + decode S_max steps (stopping early, one chunk late, once
+        every sentence is done).  Returns the number of steps run."""
+        if not use_graph:
+            self.encode()
+            steps = 0
+            while steps < self.S_max:
+                self.one_step()
+                steps += 1
+            return steps
+        if self.graph_enc is None:
+            self.encode()                      # eager once: warms every kernel
+            self.graph_enc = self._capture(self.encode, "launches_enc")
+        else:
+            self.graph_enc.replay()
+            kern.launches += self.launches_enc
+        steps = 0
+        if self.graph_1 is None:
+            self.one_step()                    # step 0 eagerly, then capture
+            steps = 1
+            self.graph_1 = self._capture(self.one_step, "launches_step")
+            if self.S_max >= self.CHUNK:
+                self.graph_n = self._capture(lambda: [self.one_step() for _ in range(self.CHUNK)],
+                                             "launches_chunk")
+        done_host = torch.zeros(1, dtype=I32, pin_memory=True)
+        ev = None
+        while steps < self.S_max:
+            if self.graph_n is not None and self.S_max - steps >= self.CHUNK:
+                self.graph_n.replay()
+                kern.launches += self.launches_chunk
+                steps += self.CHUNK
+            else:
+                self.graph_1.replay()
+                kern.launches += self.launches_step
+                steps += 1
+            if poll and steps < self.S_max:
+                # early exit for finished batches, checked one chunk late so the
+                # host never stalls the GPU pipeline
+                if ev is not None and ev.query() and int(done_host[0]) >= self.B:
+                    break
+                done_host.copy_(self.st["n_done"], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+        return steps
+
+    def collect(self) -> tuple:
+        """Backtrack the best hypotheses; one D2H copy of everything."""
+        B, S, nf1 = self.B, self.S_max, max(self.nf, 1)
+        kern.beam_finalize(self.state, self.tokens_out, self.factors_out)
+        h = self.out_host
+        h[:B * S].copy_(self.tokens_out.view(-1), non_blocking=True)
+        h[B * S:B * S + B * nf1 * S].copy_(self.factors_out.view(-1), non_blocking=True)
+        h[B * S + B * nf1 * S:B * S + B * nf1 * S + B].copy_(self.st["best_steps"],
+                                                              non_blocking=True)
+        h[B * S + B * nf1 * S + B:].copy_(self.st["best_forced"], non_blocking=True)
+        lp = self.st["best_logprob"].to("cpu", non_blocking=False)
+        arr = h.numpy()
+        toks = arr[:B * S].reshape(B, S)
+        facs = arr[B * S:B * S + B * nf1 * S].reshape(B, nf1, S)
+        steps = arr[B * S + B * nf1 * S:B * S + B * nf1 * S + B]
+        forced = arr[B * S + B * nf1 * S + B:]
+        return toks, facs, steps, forced, lp.numpy()
+
+
+_WS_CACHE: dict = {}
+_WS_MAX = 4
+
+
+def _workspace(model, key, *args):
+    ws = _WS_CACHE.get((id(model), key))
+    if ws is None:
+        if len(_WS_CACHE) >= _WS_MAX:
+            _WS_CACHE.pop(next(iter(_WS_CACHE)))
+        ws = DecodeWorkspace(model, *args)
+        _WS_CACHE[(id(model), key)] = ws
+    return ws
+
+
 class BeamBatch:
-    """Device state of one batched beam (or greedy, K=1) run.
+    """One batched beam (or greedy, K=1) run over a cached DecodeWorkspace.
 
-    Construction does the host work and stages every input on the device
-    (ids, lengths, prefixes, restriction masks, buffers); `run()` is pure
-    device work: encoder, cross K/V, the captured decode loop, finalize."""
-
-    GRAPH_POLL = 8
+    Construction does the host work and stages every input on the device;
+    `run()` is device work: encoder, cross K/V, the captured decode loop,
+    finalize, one D2H copy of the results."""
 
     def __init__(self, model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
                  nvs_threshold: float | None = None, use_graph: bool = True):
@@ -189,17 +411,49 @@ class BeamBatch:
         self.use_graph = use_graph
         self.nvs_threshold = nvs_threshold
         c = model.config
-        dev = model.device
-        nf = len(c.target_factor_specs)
+        nf, nsf = len(c.target_factor_specs), len(c.source_factor_specs)
         self.nf = nf
         B = len(jobs)
         L = max(len(j.src_ids) for j in jobs)
-        self.B, self.L = B, L
-        # ---- source ids (padded), staged on the device
-        ids = np.zeros((B, L), dtype=np.int32)
+        self.B, self.L, self.R = B, L, B * beam
+        max_len = np.array([2 * len(j.src_ids) + 10 for j in jobs], dtype=np.int32)
+        self.S_max = int(max_len.max())
+        self.P = max(1, max(len(j.prefix_ids) for j in jobs))
+        self._max_len = max_len
+        self.ws = None
+        self.steps_run = 0
+        if nvs_threshold is None:
+            self._prepare([j.active_ids for j in jobs])
+
+    # restricted vocabulary (search.py:235-242): union U + per-chunk bitmask
+    def _prepare(self, actives):
+        model, c = self.model, self.model.config
+        B, L, K, P, nf, jobs = self.B, self.L, self.K, self.P, self.nf, self.jobs
         nsf = len(c.source_factor_specs)
-        fids = np.zeros((max(nsf, 1), B, L), dtype=np.int32)
-        lengths = np.zeros(B, dtype=np.int32)
+        restricted = any(a is not None for a in actives)
+        V = c.trg_vocab_size
+        if restricted:
+            actives = [a if a is not None else np.arange(V, dtype=np.int64) for a in actives]
+            U_ids = np.unique(np.concatenate(actives)).astype(np.int64)
+            U = int(U_ids.size)
+        else:
+            U = V
+        key = (B, L, self.S_max, K, P, U, self.alpha, restricted)
+        ws = _workspace(model, key, B, L, self.S_max, K, P, U, self.alpha, restricted)
+        self.ws = ws
+        # this batch's inputs: own pinned staging + own device copy (several
+        # batches of one shape can be staged before any of them runs)
+        self.in_host = torch.zeros_like(ws.in_host, pin_memory=True)
+        h = {}
+        off = 0
+        for k, n in ws.in_sizes.items():
+            h[k] = self.in_host[off:off + n]
+            off += n
+        ids = h["ids"].numpy().reshape(B, L)
+        ids[:] = 0
+        fids = h["fids"].numpy().reshape(max(nsf, 1), B, L)
+        fids[:] = 0
+        lengths = h["lengths"].numpy()
         for b, j in enumerate(jobs):
             n = len(j.src_ids)
             ids[b, :n] = j.src_ids
@@ -208,188 +462,99 @@ class BeamBatch:
                 fids[k, b, :n] = j.src_factor_ids[k]
         if (ids < 0).any() or (ids >= c.src_vocab_size).any():
             raise ShapeError(f"ids out of range [0, {c.src_vocab_size}) for embedding table")
-        self.h2d_bytes = ids.nbytes + lengths.nbytes + (fids.nbytes if nsf else 0)
-        self.ids_d = torch.from_numpy(ids.reshape(-1)).to(dev)
-        self.fids_d = torch.from_numpy(fids.reshape(max(nsf, 1), -1)).to(dev) if nsf else None
-        self.len_d = torch.from_numpy(lengths).to(dev)
-        # ---- per-chunk limits
-        max_len = np.array([2 * len(j.src_ids) + 10 for j in jobs], dtype=np.int32)
-        self.S_max = int(max_len.max())
-        self.max_len = torch.from_numpy(max_len).to(dev)
-        self.prefix_len = torch.tensor([len(j.prefix_ids) for j in jobs], dtype=I32, device=dev)
-        self.R = B * beam
-        self.row_sent = torch.arange(self.R, dtype=I32, device=dev) // beam
-        self.len_pen = torch.tensor([float(s) ** alpha if s > 0 else 1.0
-                                     for s in range(self.S_max + 1)],
-                                    dtype=torch.float64, device=dev)
-        self.sb = None
-        if nvs_threshold is None:
-            self._setup_vocab([j.active_ids for j in jobs])
-        self.graph = None
-        self.steps_run = 0
-        self.launches_per_step = 0
-
-    def _setup_vocab(self, actives):
-        """Restricted output vocabulary (search.py:235-242) as the union U of
-        the chunks' active sets plus a per-chunk column bitmask; then every
-        buffer of the decode loop."""
-        model, c, dev = self.model, self.model.config, self.model.device
-        B, K, nf, jobs = self.B, self.K, self.nf, self.jobs
-        restricted = any(a is not None for a in actives)
-        V = c.trg_vocab_size
+        h["max_len"].numpy()[:] = self._max_len
+        h["prefix_len"].numpy()[:] = [len(j.prefix_ids) for j in jobs]
+        pcol = h["prefix_col"].numpy().reshape(B, P)
+        pcol[:] = -1
+        pfac = h["prefix_fac"].numpy().reshape(B, max(nf, 1), P)
+        pfac[:] = -1
+        col_of = None
         if restricted:
-            actives = [a if a is not None else np.arange(V, dtype=np.int64) for a in actives]
-            U_ids = np.unique(np.concatenate(actives)).astype(np.int64)
-            U = int(U_ids.size)
-            mask = np.zeros((B, (U + 31) // 32), dtype=np.uint32)
+            h["col_token"].numpy()[:] = U_ids.astype(np.int32)
+            mask = h["mask"].numpy().view(np.uint32).reshape(B, -1)
+            mask[:] = 0
             for b, a in enumerate(actives):
                 cols = np.searchsorted(U_ids, a)
-                np.bitwise_or.at(mask[b], cols >> 5,
-                                 (np.uint32(1) << (cols & 31).astype(np.uint32)))
-            self.col_token = torch.from_numpy(U_ids.astype(np.int32)).to(dev)
-            self.mask = torch.from_numpy(mask.view(np.int32)).to(dev)
-            E_out = torch.empty(U, c.d_model, device=dev, dtype=model.cdt)
-            self._gather_E = True
+                np.bitwise_or.at(mask[b], cols >> 5, (np.uint32(1) << (cols & 31).astype(np.uint32)))
             col_of = {int(t): i for i, t in enumerate(U_ids)}
-        else:
-            U = V
-            self.col_token = self.mask = None
-            E_out = model.E_trg_c
-            self._gather_E = False
-            col_of = None
-        self.U = U
-        eos_col = col_of[EOS_ID] if restricted else EOS_ID
-        P = max(1, max(len(j.prefix_ids) for j in jobs))
-        prefix_col = np.full((B, P), -1, dtype=np.int32)
-        prefix_fac = np.full((B, max(nf, 1), P), -1, dtype=np.int32)
         for b, j in enumerate(jobs):
             for t, tok in enumerate(j.prefix_ids):
                 if restricted:
                     if tok not in col_of:
                         raise ConfigError(f"token id {tok} missing from the restricted vocabulary")
-                    prefix_col[b, t] = col_of[tok]
+                    pcol[b, t] = col_of[tok]
                 else:
-                    prefix_col[b, t] = tok
+                    pcol[b, t] = tok
             for k, stream in enumerate(j.prefix_factor_ids[:nf]):
-                prefix_fac[b, k, :len(stream)] = stream
-        R, S_max = self.R, self.S_max
-        D2 = 2 * c.d_model * c.decoder_layers
-        ckv = torch.empty(B * self.L, max(D2, 1), device=dev, dtype=model.cdt)
-        self.sb = StepBuffers(model, R, B, self.L, S_max, U, E_out, ckv, self.len_d,
-                              self.row_sent)
-        sb = self.sb
-        sb.group = K
-        sb.mask = self.mask
+                pfac[b, k, :len(stream)] = stream
+        eos_col = col_of[EOS_ID] if restricted else EOS_ID
+        self.eos_col = eos_col
+        self.h2d_bytes = self.in_host.numel() * 4
+        self.in_dev = self.in_host.to(model.device, non_blocking=True)
 
-        def z(n, dt=I32):
-            return torch.zeros(n, dtype=dt, device=dev)
+    # the attributes bench.py / tests read
+    @property
+    def sb(self):
+        return self.ws.sb
 
-        self.prefix_col = torch.from_numpy(prefix_col).to(dev)
-        self.prefix_fac = torch.from_numpy(prefix_fac).to(dev)
-        self.n_alive = torch.ones(B, dtype=I32, device=dev)
-        self.done = z(B)
-        self.score = z(R, torch.float64)
-        self.tok_hist = z(S_max * R)
-        self.par_hist = z(S_max * R)
-        self.fac_hist = z(S_max * max(nf, 1) * R)
-        self.cand_score = z(R * K, torch.float64)
-        self.cand_lp = z(R * K, torch.float32)
-        self.cand_col = z(R * K)
-        self.cand_cnt = z(R)
-        self.row_argmax = z(R)
-        self.fac_choice = z(R * max(nf, 1))
-        self.counter = z(B)
-        self.best_norm = z(B, torch.float64)
-        self.best_logprob = z(B, torch.float64)
-        self.best_steps = z(B)
-        self.best_forced = z(B)
-        self.best_parent = z(B)
-        self.best_fac = z(B * max(nf, 1))
-        self.n_done = z(1)
-        self.tokens_out = z(B * S_max).view(B, S_max)
-        self.factors_out = z(B * max(nf, 1) * S_max).view(B, max(nf, 1), S_max)
-        self.state = N.BeamState(
-            B, K, U, S_max, nf, self.len_pen.data_ptr(), sb.step.data_ptr(),
-            N.ptr(self.col_token), N.ptr(self.mask), eos_col, self.max_len.data_ptr(),
-            self.prefix_len.data_ptr(), self.prefix_col.data_ptr(), P,
-            self.prefix_fac.data_ptr() if nf else None, self.n_alive.data_ptr(),
-            self.done.data_ptr(), self.score.data_ptr(), sb.tok.data_ptr(), sb.ftok.data_ptr(),
-            sb.parent.data_ptr(), self.tok_hist.data_ptr(), self.par_hist.data_ptr(),
-            self.fac_hist.data_ptr(), sb.fac.data_ptr() if nf else None, sb.fac.stride(0),
-            model.fac_off.data_ptr(), sb.lse_part.data_ptr(), sb.lse_part.shape[1] // 2, 1, 0,
-            self.cand_score.data_ptr(), self.cand_lp.data_ptr(),
-            self.cand_col.data_ptr(), self.cand_cnt.data_ptr(), self.row_argmax.data_ptr(),
-            self.fac_choice.data_ptr(), self.counter.data_ptr(), self.best_norm.data_ptr(),
-            self.best_logprob.data_ptr(), self.best_steps.data_ptr(),
-            self.best_forced.data_ptr(), self.best_parent.data_ptr(), self.best_fac.data_ptr(),
-            self.n_done.data_ptr())
+    @property
+    def state(self):
+        return self.ws.state
 
-    def _encode(self):
-        """Encoder + all layers' cross K/V (model.py:414-430, 527-531)."""
-        m = self.model
-        nsf = len(m.config.source_factor_specs)
-        enc = m.encode_device(self.ids_d, self.fids_d if nsf else None, self.len_d,
-                              self.B, self.L)
-        if self.nvs_threshold is not None:
-            self._setup_vocab(nvs_active_sets(m, enc, self.len_d, self.B, self.L,
-                                              self.nvs_threshold, self.jobs))
-        if m.config.decoder_layers:
-            m.cross_kv_device(enc, out=self.sb.ckv)
-        if self._gather_E:
-            kern.gather_rows(m.E_trg_c, self.col_token, self.sb.E_out)
+    @property
+    def done(self):
+        return self.ws.st["done"]
 
-    # ------------------------------------------------------------- stepping
-    def _one_step(self):
-        step_forward(self.model, self.sb)
-        kern.beam_step(self.sb.logits, self.state)
-        kern.beam_reorder(self.sb.anc, self.sb.parent, self.sb.step, self.R, self.S_max)
+    @property
+    def n_alive(self):
+        return self.ws.st["n_alive"]
+
+    @property
+    def n_done(self):
+        return self.ws.st["n_done"]
+
+    @property
+    def tokens_out(self):
+        return self.ws.tokens_out
 
     def run(self) -> list[ChunkResult]:
-        self._encode()
-        before = kern.launches
-        self._one_step()                      # step 0 eagerly (also warms every kernel)
-        self.launches_per_step = kern.launches - before
-        self.steps_run = 1
-        remaining = self.S_max - 1
-        host_done = torch.zeros(1, dtype=I32, pin_memory=True)
-        if remaining > 0 and self.use_graph:
-            self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph):
-                self._one_step()
-            kern.launches -= self.launches_per_step  # capture does not launch
-        while remaining > 0:
-            n = min(self.GRAPH_POLL, remaining)
-            for _ in range(n):
-                if self.graph is not None:
-                    self.graph.replay()
-                    kern.launches += self.launches_per_step
-                else:
-                    self._one_step()
-            remaining -= n
-            self.steps_run += n
-            if remaining > 0:
-                host_done.copy_(self.n_done, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                if int(host_done[0]) >= self.B:
-                    break
+        if self.ws is None:  # NVS: the active sets come from the encoder output
+            m, c = self.model, self.model.config
+            nsf = len(c.source_factor_specs)
+            ids = np.zeros((self.B, self.L), dtype=np.int32)
+            fids = np.zeros((max(nsf, 1), self.B, self.L), dtype=np.int32)
+            lengths = np.zeros(self.B, dtype=np.int32)
+            for b, j in enumerate(self.jobs):
+                ids[b, :len(j.src_ids)] = j.src_ids
+                lengths[b] = len(j.src_ids)
+                for k in range(nsf):
+                    fids[k, b, :len(j.src_ids)] = j.src_factor_ids[k]
+            dev = m.device
+            len_d = torch.from_numpy(lengths).to(dev)
+            enc = m.encode_device(torch.from_numpy(ids.reshape(-1)).to(dev),
+                                  torch.from_numpy(fids.reshape(max(nsf, 1), -1)).to(dev)
+                                  if nsf else None, len_d, self.B, self.L)
+            self._prepare(nvs_active_sets(m, enc, len_d, self.B, self.L, self.nvs_threshold,
+                                          self.jobs))
+        ws = self.ws
+        if ws.state is None or ws.eos_col != self.eos_col:
+            ws.bind_state(self.eos_col)
+            ws.graph_1 = ws.graph_n = None  # the step graph bakes eos_col in
+        ws.in_dev.copy_(self.in_dev, non_blocking=True)   # device-resident inputs
+        ws.reset()
+        self.steps_run = ws.run(self.use_graph)
         return self.collect()
 
     def collect(self) -> list[ChunkResult]:
-        c = self.model.config
-        nf = len(c.target_factor_specs)
-        B = self.B
-        kern.beam_finalize(self.state, self.tokens_out, self.factors_out)
-        toks, facs = self.tokens_out.cpu().numpy(), self.factors_out.cpu().numpy()
-        steps = self.best_steps.cpu().numpy()
-        lp = self.best_logprob.cpu().numpy()
-        forced = self.best_forced.cpu().numpy()
+        toks, facs, steps, forced, lp = self.ws.collect()
+        nf = self.nf
         out = []
-        for b in range(B):
+        for b in range(self.B):
             s = int(steps[b])
             if s <= 0:
                 raise RuntimeError("device search finished without a hypothesis")
-            out.append(ChunkResult([int(x) for x in toks[b, :s - 1]],
-                                   [[int(x) for x in facs[b, k, :s]] for k in range(nf)],
+            out.append(ChunkResult(toks[b, :s - 1].tolist(),
+                                   [facs[b, k, :s].tolist() for k in range(nf)],
                                    float(lp[b]), s, bool(forced[b])))
         return out
 

@@ -170,8 +170,18 @@ class Model:
             self.w_nvs, self.b_nvs = cw(p["nvs.w"]), f32(p["nvs.b"])
 
     # ------------------------------------------------------------ encoder
+    def encoder_buffers(self, n: int) -> dict:
+        """Preallocated encoder work buffers for n = B*L positions."""
+        c, dev, cdt = self.config, self.device, self.cdt
+        d = c.d_model
+        return dict(x=torch.empty(n, d, device=dev), h=torch.empty(n, d, device=dev, dtype=cdt),
+                    qkv=torch.empty(n, 3 * d, device=dev, dtype=cdt),
+                    ctx=torch.empty(n, d, device=dev, dtype=cdt),
+                    f=torch.empty(n, c.ff_dim, device=dev, dtype=cdt),
+                    xc=torch.empty(n, d, device=dev, dtype=cdt))
+
     def encode_device(self, ids: torch.Tensor, fids: torch.Tensor | None, lengths: torch.Tensor,
-                      B: int, L: int) -> torch.Tensor:
+                      B: int, L: int, bufs: dict | None = None) -> torch.Tensor:
         """Batched pre-norm encoder (model.py:414-430), no final LN.
         ids [B*L] int32 (padded), fids [n_factors, B*L] int32, lengths [B]
         int32.  Returns enc fp32 [B*L, d]."""
@@ -179,17 +189,15 @@ class Model:
         d, H, dh = c.d_model, c.heads, c.head_dim
         n = B * L
         dev, cdt = self.device, self.cdt
-        x = torch.empty(n, d, device=dev)
+        bufs = bufs or self.encoder_buffers(n)
+        x = bufs["x"]
         specs = c.source_factor_specs
         kern.embed_source(ids, self.E_src, self.pe_src, [s.dim for s in specs],
                           [0 if s.combine == "sum" else 1 for s in specs], fids,
                           self.src_ftab_ptrs, x, B, L, d)
         if not self.enc:
             return x
-        h = torch.empty(n, d, device=dev, dtype=cdt)
-        qkv = torch.empty(n, 3 * d, device=dev, dtype=cdt)
-        ctx = torch.empty(n, d, device=dev, dtype=cdt)
-        f = torch.empty(n, c.ff_dim, device=dev, dtype=cdt)
+        h, qkv, ctx, f = bufs["h"], bufs["qkv"], bufs["ctx"], bufs["f"]
         for Ly in self.enc:
             kern.layernorm(x, *Ly.ln1, h)
             kern.gemm(h, Ly.wqkv, qkv)
@@ -200,13 +208,14 @@ class Model:
             kern.gemm(f, Ly.w2, x, N.EPI_RESID, Ly.b2)
         return x
 
-    def cross_kv_device(self, enc: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def cross_kv_device(self, enc: torch.Tensor, out: torch.Tensor | None = None,
+                        tmp: torch.Tensor | None = None) -> torch.Tensor:
         """All decoder layers' cross K|V in one GEMM (model.py:527-531)."""
         n, d = enc.shape
         if self.cdt == torch.float32:
             a = enc
         else:
-            a = torch.empty(n, d, device=self.device, dtype=self.cdt)
+            a = tmp if tmp is not None else torch.empty(n, d, device=self.device, dtype=self.cdt)
             kern.convert(enc, a)
         if out is None:
             out = torch.empty(n, self.w_ckv.shape[0], device=self.device, dtype=self.cdt)
