@@ -99,6 +99,11 @@ int skb_tc_available(void);
 int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
              int ldw, const skb_epilogue *epi, void *stream);
 
+/* Force the tcgen05 tile configuration of later skb_gemm calls (tests and
+ * tuning): N-tile width bn in {64,128,256}, multicast cluster size cs in
+ * {1,2,4}, split-K factor; 0 = choose automatically. */
+int skb_gemm_force(int bn, int cs, int splits);
+
 /* Same, forcing the SIMT path (for parity tests of the tcgen05 path). */
 int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
                   int ldw, const skb_epilogue *epi, void *stream);

@@ -53,6 +53,7 @@ SIGNATURES = {
     "skb_tc_available": [],
     "skb_gemm": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
     "skb_gemm_simt": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
+    "skb_gemm_force": [i32, i32, i32],
     "skb_layernorm": [i32, i32, vp, i32, vp, vp, C.c_float, vp, i32, i32, vp],
     "skb_embed_target": [i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp],
     "skb_embed_source": [i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],

@@ -283,6 +283,34 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, int c0, int c1,
+                                               uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -311,6 +339,12 @@ __device__ __forceinline__ float2 group_stats_fast(const EpiArgs &e, int m, int 
 }
 
 // Persistent, warp-specialised tcgen05 GEMM.
+// With CS > 1 the CTAs run as clusters of CS along N: the CS CTAs of a
+// cluster work on the same M tile (CS adjacent N tiles) and each loads only
+// BM/CS rows of every A (activation) k-block, multicast by TMA into all CS
+// CTAs' shared memory — A's L2->SM traffic drops CS-fold.  A stage is
+// refilled only after every CTA of the cluster has released it (the MMA
+// commit arrives on all CS empty barriers).
 //   warp 0      : TMA producer (one elected lane) over all tiles of this CTA
 //   warp 1      : MMA issuer (one lane): K loop into one of two TMEM
 //                 accumulators, tcgen05.commit -> smem slot free / tile done
@@ -319,7 +353,7 @@ __device__ __forceinline__ float2 group_stats_fast(const EpiArgs &e, int m, int 
 // Tiles are visited M-fastest so the CTAs working at the same time share the
 // weight (B) tile: each weight byte comes from HBM once, the small
 // activation matrix stays L2-resident.
-template <int BN>
+template <int BN, int CS>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               int M, int N, int K, EpiArgs ep) {
@@ -337,17 +371,32 @@ __global__ void __launch_bounds__(192, 1)
   const int mt = (M + BM - 1) / BM;
   const int num_tiles = mt * ((N + BN - 1) / BN);
   const int nk = (K + BK - 1) / BK;
-  const int S = ep.splits;
+  const int S = CS > 1 ? 1 : ep.splits;
   const int kps = (nk + S - 1) / S;  // k-blocks per split
-  const int num_units = num_tiles * S;
+  const int nt = (N + BN - 1) / BN;
+  const int num_units = CS > 1 ? ((nt + CS - 1) / CS) * mt : num_tiles * S;
+  const int rank = CS > 1 ? (int)cluster_rank() : 0;
+  const int u_first = CS > 1 ? (int)blockIdx.x / CS : (int)blockIdx.x;
+  const int u_step = CS > 1 ? (int)gridDim.x / CS : (int)gridDim.x;
+  constexpr uint16_t CMASK = (uint16_t)((1u << CS) - 1u);
+  constexpr int A_SLICE = BM / CS;  // rows of each A k-block this CTA loads
   __shared__ int last_flag[2];
+  (void)num_tiles;
   // unit u -> (tile, split): M fastest, then split, then N, so concurrently
-  // running CTAs share both the weight tile and its K slice.
+  // running CTAs share both the weight tile and its K slice.  In cluster
+  // mode a unit is (M tile, group of CS N tiles); this CTA takes N tile
+  // group*CS + rank.
   auto decode = [&](int u, int &m0, int &n0, int &tile, int &split, int &kb0, int &kb1) {
     const int mb = u % mt;
     const int rest = u / mt;
-    split = rest % S;
-    const int nb = rest / S;
+    int nb;
+    if (CS > 1) {
+      split = 0;
+      nb = rest * CS + rank;
+    } else {
+      split = rest % S;
+      nb = rest / S;
+    }
     m0 = mb * BM;
     n0 = nb * BN;
     tile = nb * mt + mb;
@@ -358,7 +407,7 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);  // every CTA of the cluster releases the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -378,6 +427,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (CS > 1) cluster_sync_all();  // peers' barriers exist before any multicast
 
   if (warp == 0) {
     if (lane == 0) {
@@ -386,9 +436,9 @@ __global__ void __launch_bounds__(192, 1)
       // drains; activations (A) only after griddepcontrol.wait.
       int pre = 0;
       int pm0 = 0, pn0 = 0;
-      if ((int)blockIdx.x < num_units) {
+      if (u_first < num_units) {
         int tile, split, kb0, kb1;
-        decode(blockIdx.x, pm0, pn0, tile, split, kb0, kb1);
+        decode(u_first, pm0, pn0, tile, split, kb0, kb1);
         pre = min(C::STAGES, kb1 - kb0);
         for (int q = 0; q < pre; ++q) {
           uint8_t *sa = smem + q * C::STAGE_BYTES;
@@ -399,7 +449,13 @@ __global__ void __launch_bounds__(192, 1)
       pdl_wait();
       pdl_trigger();
       int it = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      auto load_a = [&](uint8_t *sa, int kb, int m0, uint64_t *bar) {
+        if (CS > 1)  // my slice of the A tile, into every CTA of the cluster
+          tma_load_2d_mc(sa + rank * A_SLICE * 128, &tmA, kb * BK, m0 + rank * A_SLICE, bar, CMASK);
+        else
+          tma_load_2d(sa, &tmA, kb * BK, m0, bar);
+      };
+      for (int u = u_first; u < num_units; u += u_step) {
         int m0, n0, tile, split, kb0, kb1;
         decode(u, m0, n0, tile, split, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -407,12 +463,13 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t ph = (it / C::STAGES) & 1;
           uint8_t *sa = smem + s * C::STAGE_BYTES;
           if (it < pre) {  // B already in flight for this stage
-            tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
+            if (CS > 1) mbar_wait(&empty[s], ph ^ 1);  // (passes: fresh barriers)
+            load_a(sa, kb, m0, &full[s]);
             continue;
           }
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
+          load_a(sa, kb, m0, &full[s]);
           tma_load_2d(sa + C::A_BYTES, &tmB, kb * BK, n0, &full[s]);
         }
       }
@@ -424,7 +481,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
       int it = 0, local = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++local) {
+      for (int u = u_first; u < num_units; u += u_step, ++local) {
         int m0, n0, tile, split, kb0, kb1;
         decode(u, m0, n0, tile, split, kb0, kb1);
         const int acc = local & 1;
@@ -443,7 +500,10 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
             umma_bf16(d, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty[s]);
+          if (CS > 1)
+            umma_commit_mc(&empty[s], CMASK);  // release the stage in every CTA
+          else
+            umma_commit(&empty[s]);
         }
         umma_commit(&tfull[acc]);
       }
@@ -456,7 +516,7 @@ __global__ void __launch_bounds__(192, 1)
                         ((reinterpret_cast<uintptr_t>(ep.out) & 15) == 0);
     int local = 0;
     const int erow = quarter * 32 + lane;  // row within the tile
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++local) {
+    for (int u = u_first; u < num_units; u += u_step, ++local) {
       int m0, n0, tile, split, kb0, kb1;
       decode(u, m0, n0, tile, split, kb0, kb1);
       const int acc = local & 1;
@@ -535,6 +595,8 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   __syncthreads();
+  // no peer may still multicast into / arrive on this CTA's shared memory
+  if (CS > 1) cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -620,27 +682,69 @@ static int make_map(CUtensorMap *out, const void *ptr, int rows, int cols, int l
   return SKB_OK;
 }
 
-template <int BN>
+template <int BN, int CS>
 static int launch(int M, int N, int K, const void *A, int lda, const void *W, int ldw,
                   EpiArgs ep, cudaStream_t st, int splits = 1) {
-  ep.splits = splits;
   using C = Cfg<BN>;
+  ep.splits = CS > 1 ? 1 : splits;
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, A, M, K, lda, BM);
+  int rc = make_map(&ma, A, M, K, lda, BM / CS);
   if (rc) return rc;
   rc = make_map(&mb, W, N, K, ldw, BN);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_gemm_tc<BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
+  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
   const int nsm = num_sms();
-  const int grid = tiles < nsm ? tiles : nsm;
-  launch_k(k_gemm_tc<BN>, grid, 192, C::SMEM, st, ma, mb, M, N, K, ep);
+  int grid;
+  if (CS > 1) {
+    const int clusters = ((nt + CS - 1) / CS) * mt;
+    const int maxc = nsm / CS;
+    grid = (clusters < maxc ? clusters : maxc) * CS;
+  } else {
+    const int tiles = mt * nt * ep.splits;
+    grid = tiles < nsm ? tiles : nsm;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CS > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CS;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, CS>, ma, mb, M, N, K, ep);
   SKB_CHECK_LAUNCH("k_gemm_tc");
   return SKB_OK;
+}
+
+// tile-config overrides (tests / tuning): env SKB_GEMM_BN|CS|SPLITS at load,
+// or skb_gemm_force() at run time; 0 = automatic
+int g_force_bn = -1, g_force_cs = 0, g_force_s = 0;
+void init_forces() {
+  if (g_force_bn >= 0) return;
+  const char *e = getenv("SKB_GEMM_BN");
+  g_force_bn = e ? atoi(e) : 0;
+  e = getenv("SKB_GEMM_CS");
+  g_force_cs = e ? atoi(e) : 0;
+  e = getenv("SKB_GEMM_SPLITS");
+  g_force_s = e ? atoi(e) : 0;
 }
 
 }  // namespace tc
@@ -772,6 +876,14 @@ extern "C" int skb_tc_available(void) {
   return (major == 10 && minor == 0 && tc::encode_fn() != nullptr) ? 1 : 0;
 }
 
+extern "C" int skb_gemm_force(int bn, int cs, int splits) {
+  tc::init_forces();
+  tc::g_force_bn = bn;
+  tc::g_force_cs = cs;
+  tc::g_force_s = splits;
+  return SKB_OK;
+}
+
 extern "C" int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda,
                              const void *W, int ldw, const skb_epilogue *epi, void *stream) {
   int rc = check_args(in_dtype, M, N, K, A, W, epi);
@@ -802,13 +914,8 @@ extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int ld
   const int nk = (K + tc::BK - 1) / tc::BK;
   const int nsm = tc::num_sms();
   const bool can_split = epi->splitk_ws != nullptr && epi->splitk_counters != nullptr;
-  static int force_bn = -1, force_s = -1;
-  if (force_bn < 0) {
-    const char *e = getenv("SKB_GEMM_BN");
-    force_bn = e ? atoi(e) : 0;
-    const char *f = getenv("SKB_GEMM_SPLITS");
-    force_s = f ? atoi(f) : 0;
-  }
+  tc::init_forces();
+  const int force_bn = tc::g_force_bn, force_s = tc::g_force_s;
   const int bns[3] = {256, 128, 64};
   auto cost = [&](long m, int bn, int sp) {
     const long tiles = ((m + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn) * sp;
@@ -842,24 +949,41 @@ extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int ld
     }
   }
   if (force_s) best_s = force_s;
-  int best_bn = 128;
+  // Tile width BN and multicast cluster size CS (A shared by CS N tiles):
+  // per-CTA bytes (BM/CS + BN) x K, units in ceil(CTAs / SMs) rounds.
+  const int force_cs = tc::g_force_cs;
+  int best_bn = 128, best_cs = 1;
   double best = 1e30;
   for (int bi = 0; bi < 3; ++bi) {
     const int bn = bns[bi];
     if (force_bn && bn != force_bn) continue;
-    const double c = cost(M, bn, best_s);
-    if (c < best * 0.97) {
-      best = c;
-      best_bn = bn;
+    const int css[3] = {1, 2, 4};
+    for (int ci = 0; ci < 3; ++ci) {
+      const int cs = css[ci];
+      if (force_cs && cs != force_cs) continue;
+      if (cs > 1 && best_s > 1) continue;
+      const long ntl = (N + bn - 1) / bn;
+      const long ctas = ((M + tc::BM - 1) / tc::BM) * ((ntl + cs - 1) / cs) * cs * best_s;
+      const long rounds = (ctas + nsm - 1) / nsm;
+      const double kb = (double)((nk + best_s - 1) / best_s) * tc::BK;
+      const double bytes = ((double)tc::BM / cs + bn) * kb * 2.0 +
+                           (best_s > 1 ? 2.0 * tc::BM * bn * 4 : 0.0);
+      const double c = rounds * (bytes + 96.0 * 1024);
+      if (c < best * 0.97) {
+        best = c;
+        best_bn = bn;
+        best_cs = cs;
+      }
     }
   }
-  if (best_s > 1) {
-    const long nt = (long)((M + tc::BM - 1) / tc::BM) * ((N + best_bn - 1) / best_bn);
-    if (nt > epi->splitk_counters_n ||
-        (long long)nt * best_s * tc::BM * best_bn > epi->splitk_ws_elems)
-      return fail(SKB_ERR_CONFIG, "gemm: split-K workspace too small (M=%d N=%d)", M, N);
-  }
-  if (best_bn == 256) return tc::launch<256>(M, N, K, A, lda, W, ldw, ep, st, best_s);
-  if (best_bn == 128) return tc::launch<128>(M, N, K, A, lda, W, ldw, ep, st, best_s);
-  return tc::launch<64>(M, N, K, A, lda, W, ldw, ep, st, best_s);
+#define SKB_GEMM_GO(BNV)                                                               \
+  do {                                                                                 \
+    if (best_cs == 4) return tc::launch<BNV, 4>(M, N, K, A, lda, W, ldw, ep, st, 1);    \
+    if (best_cs == 2) return tc::launch<BNV, 2>(M, N, K, A, lda, W, ldw, ep, st, 1);    \
+    return tc::launch<BNV, 1>(M, N, K, A, lda, W, ldw, ep, st, best_s);                 \
+  } while (0)
+  if (best_bn == 256) SKB_GEMM_GO(256);
+  if (best_bn == 128) SKB_GEMM_GO(128);
+  SKB_GEMM_GO(64);
+#undef SKB_GEMM_GO
 }

@@ -191,3 +191,27 @@ def test_splitk_resid_deterministic_and_batch_invariant(M, Nn, K):
     _run("skb_gemm", N.BF16, A[:1], W, _splitk_epi(N.EPI_RESID, x1, Nn, N.F32, bias))
     torch.cuda.synchronize()
     assert torch.equal(x1[0], outs[0][0])
+
+
+@pytest.mark.parametrize("bn,cs", [(64, 2), (64, 4), (128, 2), (128, 4), (256, 4), (256, 2)])
+@pytest.mark.parametrize("M,Nn,K", [(640, 1024, 1024), (300, 3072, 512), (77, 1000, 256),
+                                    (640, 32000, 1024)])
+def test_cluster_multicast_configs(bn, cs, M, Nn, K):
+    """TMA multicast of A across a cluster of CS N-tiles: every forced tile
+    configuration gives the same (bitwise) result as the default one."""
+    g = torch.Generator(device="cuda").manual_seed(M + Nn + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    x0 = torch.randn(M, Nn, device="cuda", generator=g)
+    outs = []
+    for cfg in ((bn, 1, 1), (bn, cs, 1)):
+        N.call("skb_gemm_force", *cfg)
+        x = x0.clone()
+        _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_RESID, x, Nn, N.F32, bias))
+        outs.append(x)
+    N.call("skb_gemm_force", 0, 0, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    ref = x0.double() + A.double() @ W.double().T + bias.double()
+    assert (outs[1].double() - ref).abs().max().item() <= 2e-3 * K ** 0.5

@@ -45,4 +45,5 @@ for name, (m, Nn, K) in SHAPES.items():
     res[name] = dict(us=round(ms * 1e3, 2), tflops=round(2 * m * Nn * K / ms / 1e9, 1),
                      err=round(err, 4))
 print(json.dumps({"BN": os.environ.get("SKB_GEMM_BN", "auto"),
+                  "CS": os.environ.get("SKB_GEMM_CS", "auto"),
                   "S": os.environ.get("SKB_GEMM_SPLITS", "auto"), **res}))
