@@ -104,6 +104,13 @@ int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int lda, const vo
  * {1,2,4}, split-K factor; 0 = choose automatically. */
 int skb_gemm_force(int bn, int cs, int splits);
 
+/* Select the swap-AB decode GEMM (weights on the MMA M side, one tile per
+ * CTA, whole-smem TMA ring, K split across a cluster with a DSMEM
+ * reduction): mode 0 = automatic (M <= 1024), 1 = never, 2 = always;
+ * na = activation rows per tile (multiple of 16, <= 256), cs = cluster
+ * K-split; 0 = choose automatically. */
+int skb_gemm_force_sw(int mode, int na, int cs);
+
 /* Same, forcing the SIMT path (for parity tests of the tcgen05 path). */
 int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
                   int ldw, const skb_epilogue *epi, void *stream);
@@ -267,6 +274,11 @@ int skb_beam_finalize(const skb_beam_state *st, int *tokens_out, int *factors_ou
 /* Debug: copy the beam kernel's per-row phase timestamps (only in builds
  * with -DSKB_PROFILE_PHASES; SKB_ERR_UNSUPPORTED otherwise). */
 int skb_debug_beam_prof(unsigned long long *host_buf_4096x10);
+
+/* Debug: per-CTA %globaltimer stamps of the last swap-AB GEMM launch
+ * (entry, pre-wait, post-wait, first stage, last MMA, accumulator ready,
+ * exit, smid) — builds with -DSKB_GEMM_TRACE only. */
+int skb_debug_gemm_trace(unsigned long long *host_buf_1024x8);
 
 /* out[r] = max over positions l < len[b] of enc[b, l, :] (model.py:496-500). */
 int skb_masked_maxpool(int B, int L, int d, const float *enc, const int *lengths, float *out,

@@ -54,6 +54,7 @@ SIGNATURES = {
     "skb_gemm": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
     "skb_gemm_simt": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
     "skb_gemm_force": [i32, i32, i32],
+    "skb_gemm_force_sw": [i32, i32, i32],
     "skb_layernorm": [i32, i32, vp, i32, vp, vp, C.c_float, vp, i32, i32, vp],
     "skb_embed_target": [i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp],
     "skb_embed_source": [i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],
@@ -71,6 +72,7 @@ SIGNATURES = {
     "skb_nvs_mask": [i32, i32, vp, i32, C.c_float, vp, vp],
     "skb_set_device": [i32],
     "skb_debug_beam_prof": [vp],
+    "skb_debug_gemm_trace": [vp],
 }
 
 _lib = None

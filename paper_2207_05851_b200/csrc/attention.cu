@@ -317,19 +317,21 @@ __global__ void __launch_bounds__(256) k_attn_smem(
 // position (each lane moves one 16-byte uint4 = 8 bf16 of K or V), so a warp
 // reads 32/LPK full 128-byte rows per instruction.  Positions p < t come
 // from slot anc[t&1][r][p]; the new k/v are written to slot (r, t) first.
-// grid (ceil(R/4), H): the 4 warps of a CTA are 4 consecutive rows of one
-// head — beam rows of a sentence share ancestor slots, which then hit L1.
-template <int DH>
-__global__ void __launch_bounds__(128) k_self_attn_vec(
+// grid (ceil(R/G), H): the G warps of a CTA are the G beam rows of one
+// sentence (same head) — they share ancestor slots, which then hit L1.
+// CH positions per chunk keep the K/V registers small (<= 64 registers,
+// >= 32 resident warps per SM) so enough chunks are in flight per SM.
+template <int DH, int CH>
+__global__ void __launch_bounds__(256, 3) k_self_attn_vec(
     int R, int H, const void *qkv, int ld_qkv, int qkv_dtype, __nv_bfloat16 *kc,
     __nv_bfloat16 *vc, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
     int ctx_dtype) {
   PDL_ENTRY();
   constexpr int LPK = DH / 8;      // lanes per key row
   constexpr int KPI = 32 / LPK;    // keys per warp instruction
-  constexpr int ITER = 32 / KPI;   // = LPK instructions per 32-position chunk
+  constexpr int ITER = CH / KPI;   // warp instructions per CH-position chunk
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 4 + warp, h = blockIdx.y;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp, h = blockIdx.y;
   if (r >= R) return;
   const int D = H * DH;
   const int t = *step;
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
     const int p = it * KPI + grp;
     sl[it] = p <= t ? (p == t ? r : __ldg(arow + p)) : -1;
   }
-  for (int p0 = 0; p0 <= t; p0 += 32) {
+  for (int p0 = 0; p0 <= t; p0 += CH) {
     uint4 kk[ITER], vv[ITER];
 #pragma unroll
     for (int it = 0; it < ITER; ++it) {
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(128) k_self_attn_vec(
     int sn[ITER];
 #pragma unroll
     for (int it = 0; it < ITER; ++it) {
-      const int p = p0 + 32 + it * KPI + grp;
+      const int p = p0 + CH + it * KPI + grp;
       sn[it] = p <= t ? (p == t ? r : __ldg(arow + p)) : -1;
     }
     float sc[ITER];
@@ -899,23 +901,23 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
   if (R < 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "self_attention_step: shape");
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "self_attention_step: head dim %d", dh);
   if (R == 0) return SKB_OK;
-  (void)rows_per_group;  // beam rows of a sentence share ancestor slots through L1/L2
   if (cache_dtype == SKB_BF16 && (dh == 32 || dh == 64 || dh == 128) && ld_qkv % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (reinterpret_cast<uintptr_t>(kc) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(vc) & 15) == 0) {
-    dim3 grid((R + 3) / 4, H);
+    const int G = (rows_per_group >= 1 && rows_per_group <= 8) ? rows_per_group : 4;
+    dim3 grid((R + G - 1) / G, H);
     auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
     auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
     const float sc = attn_scale(dh);
     if (dh == 64)
-      launch_k(k_self_attn_vec<64>, grid, 128, 0, as_stream(stream), R, H, qkv, ld_qkv, qkv_dtype, k, v,
-                                                               S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+      launch_k(k_self_attn_vec<64, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
+               qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     else if (dh == 32)
-      launch_k(k_self_attn_vec<32>, grid, 128, 0, as_stream(stream), R, H, qkv, ld_qkv, qkv_dtype, k, v,
-                                                               S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+      launch_k(k_self_attn_vec<32, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
+               qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     else
-      launch_k(k_self_attn_vec<128>, grid, 128, 0, as_stream(stream), R, H, qkv, ld_qkv, qkv_dtype, k, v,
-                                                                S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+      launch_k(k_self_attn_vec<128, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
+               qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     SKB_CHECK_LAUNCH("k_self_attn_vec");
     return SKB_OK;
   }

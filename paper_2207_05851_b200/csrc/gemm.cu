@@ -749,6 +749,588 @@ void init_forces() {
 
 }  // namespace tc
 
+// ================================================ swap-AB decode GEMM (sw)
+// The decode step's GEMMs have few activation rows (M = batch x beam, 640 at
+// the benchmark) against wide weight matrices.  Laid out the usual way
+// (activations on the MMA M side) they give only ceil(M/128) x N/BN tiles,
+// far fewer than 148 SMs, each streaming a long K.  This kernel swaps the
+// operands: the weight tile (128 output columns n) is the MMA A operand and
+// an Na-row activation tile is the MMA B operand (Na = 16..256, a multiple
+// of 16), so D^T[n, m] accumulates in TMEM with lane = n, column = m.  Na is
+// chosen so that (N/128) x (M/Na) x CS fills the SMs, and every CTA runs a
+// single tile with the WHOLE shared memory as a TMA ring: most of the K
+// range is in flight at once, and the weight k-blocks (which do not depend
+// on the previous kernel) are all requested before griddepcontrol.wait.
+// Long-K shapes split K across a cluster of CS CTAs; the fp32 partial tiles
+// are reduced through distributed shared memory in rank order
+// (deterministic, no L2 round trip, no atomics), each CTA finishing 1/CS of
+// the tile.  CS is chosen from (N, K) alone, so a row's result does not
+// depend on the batch size (test_search.py:400-405).
+namespace sw {
+
+#ifdef SKB_GEMM_TRACE
+__device__ unsigned long long g_trace[1024 * 8];
+__device__ int g_dbg;
+#define SW_STAMP(slot)                                                                    \
+  do {                                                                                    \
+    unsigned long long _t;                                                                \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                \
+    const int _c = blockIdx.x + blockIdx.y * gridDim.x;                                   \
+    if (_c < 1024) g_trace[_c * 8 + (slot)] = _t;                                         \
+  } while (0)
+#else
+#define SW_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+
+constexpr int W_BYTES = 128 * tc::BK * 2;  // 16 KB weight k-block
+constexpr int SMEM_MAX = 232448;          // 227 KB opt-in
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+// Epilogue of one element (m, n).  Lanes of a warp hold consecutive n for
+// the same m, so every store is coalesced.  The kernel is instantiated per
+// epilogue kind and cluster size: each variant carries only its own code (a
+// decode step runs ~40 different kernels back to back, so every launch
+// starts with a cold instruction cache and code size is latency).
+template <int KIND>
+__device__ __forceinline__ void epi_one(const EpiArgs &e, int m, int n, float v, float bn) {
+  const size_t o = (size_t)m * e.ldo + n;
+  if (KIND == SKB_EPI_RESID) {
+    float *x = reinterpret_cast<float *>(e.out) + o;
+    *x = *x + (v + bn);
+    return;
+  }
+  float t = v + bn;
+  if (KIND == SKB_EPI_RELU) t = fmaxf(t, 0.f);
+  if (e.out_dtype == SKB_F32)
+    reinterpret_cast<float *>(e.out)[o] = t;
+  else
+    reinterpret_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16_rn(t);
+}
+
+// SSRU cell (model.py:268-272) on the lane pair (2j, 2j+1) = (W_f h, W h);
+// called by all 32 lanes (the partner value comes by shuffle).
+__device__ __forceinline__ void epi_ssru(const EpiArgs &e, const float *cprev, float *cnext,
+                                         int m, int n, float v, float bn, bool ok) {
+  const float w = __shfl_xor_sync(0xffffffffu, v, 1);
+  if (!ok || (n & 1)) return;
+  const int j = n >> 1;
+  const int srow = e.src_row ? e.src_row[m] : m;
+  const float f = sigmoid_ref(v + bn);
+  const float cp = cprev ? cprev[(size_t)srow * e.ld_state + j] : 0.f;
+  const float c = f * cp + (1.0f - f) * w;
+  cnext[(size_t)m * e.ld_state + j] = c;
+  float *xp = reinterpret_cast<float *>(e.out) + (size_t)m * e.ldo + j;
+  *xp = *xp + fmaxf(c, 0.f);
+}
+
+// 16 consecutive activation rows m0..m0+15 of output column n.
+template <int KIND>
+__device__ __forceinline__ void epi16(const EpiArgs &e, const float *cprev, float *cnext, int M,
+                                      int m0, int n, bool nok, float bn, const float *v) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int m = m0 + i;
+    if (KIND == SKB_EPI_SSRU)
+      epi_ssru(e, cprev, cnext, m, n, v[i], bn, nok && m < M);
+    else if (nok && m < M)
+      epi_one<KIND>(e, m, n, v[i], bn);
+  }
+}
+
+__device__ __forceinline__ void sts4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+// Stage 16 outputs (activation rows mloc..mloc+15, output column `row` of
+// the tile) into the shared-memory tile [rows][128] that one TMA store (or
+// TMA reduce-add, for the residual) writes out.  Lanes hold consecutive
+// columns, so every st.shared is conflict-free.
+template <int KIND>
+__device__ __forceinline__ void stage16(uint32_t base, bool bf16, int mloc, int row, float bn,
+                                        const float *v) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float t = v[i] + bn;
+    if (KIND == SKB_EPI_RELU) t = fmaxf(t, 0.f);
+    if (bf16) {
+      const __nv_bfloat16 b = __float2bfloat16_rn(t);
+      asm volatile("st.shared.b16 [%0], %1;" ::"r"(base + (uint32_t)((mloc + i) * 128 + row) * 2u),
+                   "h"(*reinterpret_cast<const unsigned short *>(&b))
+                   : "memory");
+    } else {
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(base + (uint32_t)((mloc + i) * 128 + row) * 4u),
+                   "f"(t)
+                   : "memory");
+    }
+  }
+}
+
+// Epilogue warps: make the staged tile visible to the TMA unit, then one
+// thread writes it with a bulk tensor store (x += tile for the residual).
+template <int KIND>
+__device__ __forceinline__ void flush_tile(const CUtensorMap *tmO, uint32_t base, int c0, int c1,
+                                           bool leader) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (leader) {
+    if (KIND == SKB_EPI_RESID)
+      asm volatile(
+          "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+              reinterpret_cast<uint64_t>(tmO)),
+          "r"(c0), "r"(c1), "r"(base)
+          : "memory");
+    else
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                       reinterpret_cast<uint64_t>(tmO)),
+                   "r"(c0), "r"(c1), "r"(base)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+//   warp 0 : TMA producer (one lane)   warp 1 : MMA issuer (one lane)
+//   warps 2..5 : epilogue, TMEM lane quarter = warp % 4
+// grid (weight tiles x activation tiles, CS), cluster (1, CS): the CS CTAs
+// of a cluster share the output tile and split K.
+template <int KIND, int CS>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_sw(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+              const __grid_constant__ CUtensorMap tmO, int M, int N, int K, int Na, int stages,
+              int stg_off, int tma_out, EpiArgs ep) {
+  using namespace tc;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int SB = W_BYTES + Na * 128;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + stages * SB);
+  uint64_t *empty = full + stages;
+  uint64_t *tfull = empty + stages;
+  uint64_t *rbar = tfull + 1;  // split-K: peers' partial slices landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CS > 1 ? (int)blockIdx.y : 0;
+  const int n_at = (M + Na - 1) / Na;
+  const int at = (int)blockIdx.x % n_at, wt = (int)blockIdx.x / n_at;
+  const int m0 = at * Na, n0 = wt * 128;
+  const int nk = (K + BK - 1) / BK;
+  const int kb0 = rank * nk / CS, kb1 = (rank + 1) * nk / CS;
+  const int nkc = kb1 - kb0;
+  int tcols = 32;
+  while (tcols < Na) tcols <<= 1;
+
+  if (threadIdx.x == 0) {
+    SW_STAMP(0);
+#pragma unroll 1
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(rbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    if (tma_out)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmO)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights first: independent of the previous kernel (PDL prologue)
+      const int pre = nkc < stages ? nkc : stages;
+#pragma unroll 1
+      for (int q = 0; q < pre; ++q) {
+        mbar_expect_tx(&full[q], SB);
+        tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * BK, n0, &full[q]);
+      }
+      pdl_wait();
+      pdl_trigger();
+      SW_STAMP(2);
+#pragma unroll 1
+      for (int q = 0; q < pre; ++q)
+        tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * BK, m0, &full[q]);
+#pragma unroll 1
+      for (int it = pre; it < nkc; ++it) {
+        const int s = it % stages;
+        const uint32_t ph = (it / stages) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t *st = smem + s * SB;
+        mbar_expect_tx(&full[s], SB);
+        tma_load_2d(st, &tmW, (kb0 + it) * BK, n0, &full[s]);
+        tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * BK, m0, &full[s]);
+      }
+    } else {
+      pdl_wait();
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(128, Na);
+#pragma unroll 1
+      for (int it = 0; it < nkc; ++it) {
+        const int s = it % stages;
+        mbar_wait(&full[s], (it / stages) & 1);
+        if (it == 0) SW_STAMP(3);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint8_t *st = smem + s * SB;
+        const uint64_t da = umma_desc_sw128(st);
+        const uint64_t db = umma_desc_sw128(st + W_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (it > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tfull);
+    }
+  }
+  // epilogue state (warps 2..5)
+  const int row = (warp & 3) * 32 + lane;  // weight row within the tile = output column
+  const int n = n0 + row;
+  const bool nok = n < N;
+  const float *cprev = nullptr;
+  float *cnext = nullptr;
+  if (warp >= 2) {
+    pdl_wait();
+    if (KIND == SKB_EPI_SSRU) {
+      cprev = ep.c_prev;
+      cnext = ep.c_next;
+      if (ep.step) {  // decode-loop double buffer selected by step parity
+        const int t = *ep.step;
+        cnext = ep.c_next + (t & 1) * ep.state_stride;
+        cprev = t == 0 ? nullptr : ep.c_next + ((t + 1) & 1) * ep.state_stride;
+      }
+    }
+    mbar_wait(tfull, 0);
+    if (warp == 2 && lane == 0) SW_STAMP(5);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    if (CS == 1) {
+      const float bn = (ep.bias && nok) ? __ldg(ep.bias + n) : 0.f;
+#ifdef SKB_GEMM_TRACE
+      const int dbg = g_dbg;
+#else
+      constexpr int dbg = 0;
+#endif
+      const uint32_t stg = smem_u32(smem) + (uint32_t)stg_off;
+      const bool bf16 = ep.out_dtype == SKB_BF16 && KIND != SKB_EPI_RESID;
+#pragma unroll 1
+      for (int c = 0; c < Na && m0 + c < M; c += 16) {
+        float v[16];
+        if (dbg != 2)
+          tmem_ld16(tb + (uint32_t)c, v);
+        else
+          for (int i = 0; i < 16; ++i) v[i] = (float)i;
+        if (dbg == 1) continue;
+        if (KIND != SKB_EPI_SSRU && tma_out)
+          stage16<KIND>(stg, bf16, c, row, bn, v);
+        else
+          epi16<KIND>(ep, cprev, cnext, M, m0 + c, n, nok, bn, v);
+      }
+      if (KIND != SKB_EPI_SSRU && tma_out && dbg != 1)
+        flush_tile<KIND>(&tmO, stg, n0, m0, warp == 2 && lane == 0);
+    } else {
+      // park the fp32 partial in my shared memory: part[m][128] (row-major
+      // in m, so the slice each peer finishes is one contiguous block)
+      const uint32_t pbase = smem_u32(smem) + (uint32_t)row * 4u;
+#pragma unroll 1
+      for (int c = 0; c < Na; c += 16) {
+        float v[16];
+        tmem_ld16(tb + (uint32_t)c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(pbase + (uint32_t)(c + i) * 512u), "f"(v[i])
+                       : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (warp == 2 && lane == 0)  // expect the CS-1 slices the peers push to me
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rbar)),
+                     "r"((uint32_t)((CS - 1) * (Na / CS) * 512))
+                     : "memory");
+    }
+  }
+  __syncwarp();
+  if (warp == 2 && lane == 0) SW_STAMP(1);
+  if (CS > 1) {
+    // split-K reduction, push model: every CTA bulk-copies slice p of its
+    // partial into CTA p's receive slot [my rank] (async copy engine over
+    // the cluster network), then CTA p sums its slice in rank order.
+    const int cpr = Na / CS;  // activation rows finished by this CTA
+    const int c0 = rank * cpr;
+    const uint32_t part = smem_u32(smem);
+    const uint32_t recv = part + (uint32_t)Na * 512u;  // [CS][cpr][128] fp32
+    cluster_sync_all();  // all partials written, every ring drained
+    if (warp == 2 && lane == 0) {
+#pragma unroll 1
+      for (int p = 0; p < CS; ++p) {
+        if (p == rank) continue;
+        const uint32_t dst = mapa(recv + (uint32_t)(rank * cpr) * 512u, (uint32_t)p);
+        const uint32_t bar = mapa(smem_u32(rbar), (uint32_t)p);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "r"(part + (uint32_t)(p * cpr) * 512u), "r"((uint32_t)(cpr * 512)), "r"(bar)
+            : "memory");
+      }
+    }
+    if (warp >= 2) {
+      const float bn = (ep.bias && nok) ? __ldg(ep.bias + n) : 0.f;
+      const uint32_t stg = smem_u32(smem) + (uint32_t)stg_off;
+      const bool bf16 = ep.out_dtype == SKB_BF16 && KIND != SKB_EPI_RESID;
+      mbar_wait(rbar, 0);
+#pragma unroll 1
+      for (int j0 = 0; j0 < cpr && m0 + c0 + j0 < M; j0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int jj = j0 + i < cpr ? j0 + i : cpr - 1;
+          float acc = 0.f;
+#pragma unroll
+          for (int src = 0; src < CS; ++src) {  // fixed rank order: deterministic
+            const uint32_t a = src == rank ? part + (uint32_t)(c0 + jj) * 512u
+                                           : recv + (uint32_t)(src * cpr + jj) * 512u;
+            float x;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(a + (uint32_t)row * 4u) : "memory");
+            acc = src == 0 ? x : acc + x;
+          }
+          v[i] = acc;
+        }
+        if (KIND != SKB_EPI_SSRU && tma_out) {
+          stage16<KIND>(stg, bf16, j0, row, bn, v);
+        } else {
+          const int lim = min(M, m0 + c0 + cpr);  // rows beyond my slice are a peer's
+          epi16<KIND>(ep, cprev, cnext, lim, m0 + c0 + j0, n, nok, bn, v);
+        }
+      }
+      if (KIND != SKB_EPI_SSRU && tma_out)
+        flush_tile<KIND>(&tmO, stg, n0, m0 + c0, warp == 2 && lane == 0);
+    }
+    if (warp == 2 && lane == 0) SW_STAMP(4);
+    cluster_sync_all();  // peers are done reading my shared memory
+  }
+  __syncthreads();
+#ifdef SKB_GEMM_TRACE
+  if (threadIdx.x == 0) {
+    SW_STAMP(6);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int c = blockIdx.x + blockIdx.y * gridDim.x;
+    if (c < 1024) g_trace[c * 8 + 7] = smid;
+  }
+#endif
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+}
+
+// Output tensor map for the TMA-store epilogue: [rows M][cols N] of fp32 or
+// bf16 at pitch ld, box = 128 columns x box_rows rows, no swizzle.
+static int make_map_out(CUtensorMap *out, const void *ptr, int rows, int cols, int ld, bool f32,
+                        int box_rows) {
+  static std::mutex mu;
+  static std::unordered_map<tc::MapKey, CUtensorMap, tc::MapKeyHash> cache;
+  tc::MapKey key{ptr, rows, cols, ld * (f32 ? -1 : 1), box_rows};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return SKB_OK;
+    }
+  }
+  tc::EncodeTiledFn fn = tc::encode_fn();
+  if (!fn) return fail(SKB_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  const int es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * es};
+  cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void *>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SKB_ERR_LAUNCH, "cuTensorMapEncodeTiled(out) failed (%d)", (int)r);
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *out;
+  return SKB_OK;
+}
+
+template <int KIND, int CS>
+static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
+                    const CUtensorMap &mo, int Na, int stages, int stg_off, int tma_out,
+                    size_t smem, EpiArgs ep, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_gemm_sw<KIND, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    attr_set = true;
+  }
+  const int n_wt = (N + 127) / 128, n_at = (M + Na - 1) / Na;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_wt * n_at, CS);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CS > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = CS;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS>, mw, mx, mo, M, N, K, Na, stages, stg_off, tma_out,
+                     ep);
+  SKB_CHECK_LAUNCH("k_gemm_sw");
+  return SKB_OK;
+}
+
+template <int KIND>
+static int launch_k2(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
+                     const CUtensorMap &mo, int Na, int CS, int stages, int stg_off, int tma_out,
+                     size_t smem, EpiArgs ep, cudaStream_t st) {
+  if (CS == 4)
+    return launch_t<KIND, 4>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+  if (CS == 2)
+    return launch_t<KIND, 2>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+  return launch_t<KIND, 1>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+}
+
+static int launch(int M, int N, int K, const void *X, int ldx, const void *W, int ldw, EpiArgs ep,
+                  cudaStream_t st, int Na, int CS) {
+  ep.splits = 1;
+#ifdef SKB_GEMM_TRACE
+  {
+    const char *e = getenv("SKB_SW_DBG");
+    const int d = e ? atoi(e) : 0;
+    cudaMemcpyToSymbol(g_dbg, &d, sizeof(int));
+  }
+#endif
+  if (Na < 16 || Na > 256 || Na % 16 || !(CS == 1 || CS == 2 || CS == 4) ||
+      (CS > 1 && Na % (4 * CS)))
+    return fail(SKB_ERR_CONFIG, "gemm_sw: bad tile Na=%d CS=%d", Na, CS);
+  CUtensorMap mw, mx;
+  int rc = tc::make_map(&mw, W, N, K, ldw, 128);
+  if (rc) return rc;
+  rc = tc::make_map(&mx, X, M, K, ldx, Na);
+  if (rc) return rc;
+  const int SB = W_BYTES + Na * 128;
+  const int nk = (K + tc::BK - 1) / tc::BK;
+  const int nkc = (nk + CS - 1) / CS;
+  // TMA-store epilogue: the output tile is staged in the (drained) ring
+  const bool f32o = ep.kind == SKB_EPI_RESID || ep.out_dtype == SKB_F32;
+  const int es = f32o ? 4 : 2;
+  const int tma_out = ep.kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
+                      ((long)ep.ldo * es) % 16 == 0;
+  const int rows_box = CS == 1 ? Na : Na / CS;
+  const int part_bytes = CS > 1 ? 2 * Na * 512 : 0;  // partial + receive slots
+  const int stg_off = (part_bytes + 1023) & ~1023;
+  const int need = tma_out ? stg_off + ((rows_box + 15) / 16 * 16) * 128 * es : part_bytes;
+  int stages = (SMEM_MAX - 1024 - 512) / SB;
+  if (stages > nkc) stages = nkc;
+  if (stages * SB < need) stages = (need + SB - 1) / SB;
+  if (stages < 1 || stages * SB + 1024 + 512 > SMEM_MAX)
+    return fail(SKB_ERR_UNSUPPORTED, "gemm_sw: Na=%d CS=%d does not fit", Na, CS);
+  const size_t smem = (size_t)stages * SB + 1024 + 512;
+  CUtensorMap mo;
+  if (tma_out) {
+    rc = make_map_out(&mo, ep.out, M, N, ep.ldo, f32o, rows_box);
+    if (rc) return rc;
+  } else {
+    mo = mw;  // unused
+  }
+  switch (ep.kind) {
+    case SKB_EPI_RELU:
+      return launch_k2<SKB_EPI_RELU>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
+    case SKB_EPI_RESID:
+      return launch_k2<SKB_EPI_RESID>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
+    case SKB_EPI_SSRU:
+      return launch_k2<SKB_EPI_SSRU>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
+    default:
+      return launch_k2<SKB_EPI_STORE>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
+  }
+}
+
+// Cluster split CS from (N, K) only (numerics must not depend on M).
+// Measured on B200 at M = 640 (tools/gemm_sweep.py): the bulk-copy
+// reduction costs ~3-4 us, so only long-K shapes (FFN2, K = 4096) gain.
+static int pick_cs(int N, int K) {
+  const int nk = (K + tc::BK - 1) / tc::BK;
+  const int n_wt = (N + 127) / 128;
+  if (nk >= 48 && n_wt <= 16) return 4;
+  return 1;
+}
+
+// Activation tile Na for the actual M: one wave of CTAs over the SMs with
+// the fewest bytes streamed per CTA.
+static int pick_na(int M, int N, int CS) {
+  const int nsm = tc::num_sms();
+  const int n_wt = (N + 127) / 128;
+  const int na_max = CS > 1 ? 160 : 256;  // partial + receive slots must fit in smem
+  int best = 16;
+  double best_c = 1e30;
+  for (int na = 16; na <= na_max; na += 16) {
+    if (CS > 1 && na % (4 * CS)) continue;
+    const long ctas = (long)n_wt * ((M + na - 1) / na) * CS;
+    const long waves = (ctas + nsm - 1) / nsm;
+    const double c = waves * (128.0 + na + 96.0);
+    if (c < best_c * 0.999) {
+      best_c = c;
+      best = na;
+    }
+  }
+  return best;
+}
+
+int g_mode = -1, g_na = 0, g_cs = 0;  // mode: 0 auto, 1 never, 2 always
+void init_mode() {
+  if (g_mode >= 0) return;
+  const char *e = getenv("SKB_GEMM_SW");
+  g_mode = e ? atoi(e) : 0;
+}
+
+}  // namespace sw
+
 // ========================================================== SIMT kernel
 // 64x64 output tile, BK=16, 256 threads, 4x4 outputs per thread.  Used for
 // fp32 (parity) mode and for shapes TMA cannot describe.
@@ -884,6 +1466,26 @@ extern "C" int skb_gemm_force(int bn, int cs, int splits) {
   return SKB_OK;
 }
 
+extern "C" int skb_gemm_force_sw(int mode, int na, int cs) {
+  sw::init_mode();
+  sw::g_mode = mode;
+  sw::g_na = na;
+  sw::g_cs = cs;
+  return SKB_OK;
+}
+
+extern "C" int skb_debug_gemm_trace(unsigned long long *host) {
+#ifdef SKB_GEMM_TRACE
+  cudaMemcpyFromSymbol(host, sw::g_trace, sizeof(sw::g_trace));
+  static unsigned long long zeros[1024 * 8];
+  cudaMemcpyToSymbol(sw::g_trace, zeros, sizeof(zeros));  // read-and-clear
+  return SKB_OK;
+#else
+  (void)host;
+  return SKB_ERR_UNSUPPORTED;
+#endif
+}
+
 extern "C" int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda,
                              const void *W, int ldw, const skb_epilogue *epi, void *stream) {
   int rc = check_args(in_dtype, M, N, K, A, W, epi);
@@ -903,6 +1505,13 @@ extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int ld
                       (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
                       (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   if (!tma_ok) return gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, ep, st);
+  // decode-sized M: swap-AB kernel (weights on the MMA M side)
+  sw::init_mode();
+  if (sw::g_mode != 1 && epi->kind != SKB_EPI_LOGITS && (sw::g_mode == 2 || M <= 1024)) {
+    const int cs = sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K);
+    const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);
+    return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs);
+  }
   // Tile width BN and split-K factor S from a bytes-per-SM cost model: every
   // work unit streams (BM + BN) x K/S bf16 operands (plus an fp32 partial
   // round trip when S > 1); units run in ceil(units / SMs) rounds.

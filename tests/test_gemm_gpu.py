@@ -14,6 +14,15 @@ SHAPES = [(3, 48, 16), (5, 40, 32), (130, 64, 4096), (77, 8000, 256), (640, 1024
           (200, 3072, 1024), (640, 32000, 1024), (1, 4096, 1024), (257, 1000, 512)]
 
 
+@pytest.fixture(autouse=True, params=["tc", "sw"])
+def gemm_path(request):
+    """Run every test through both tcgen05 kernels: the M-major persistent
+    kernel (k_gemm_tc) and the swap-AB decode kernel (k_gemm_sw)."""
+    N.call("skb_gemm_force_sw", 1 if request.param == "tc" else 2, 0, 0)
+    yield request.param
+    N.call("skb_gemm_force_sw", 0, 0, 0)
+
+
 def _epi(kind, out, ldo, out_dtype, bias=None, c_prev=None, c_next=None, src_row=None,
          ld_state=0):
     return N.Epilogue(kind, N.ptr(bias), N.ptr(out), ldo, out_dtype, N.ptr(c_prev),
@@ -215,3 +224,65 @@ def test_cluster_multicast_configs(bn, cs, M, Nn, K):
     assert torch.equal(outs[0], outs[1])
     ref = x0.double() + A.double() @ W.double().T + bias.double()
     assert (outs[1].double() - ref).abs().max().item() <= 2e-3 * K ** 0.5
+
+
+@pytest.mark.parametrize("na,cs", [(16, 1), (48, 1), (80, 2), (160, 4), (256, 1), (64, 4),
+                                   (128, 2), (240, 1), (96, 2)])
+@pytest.mark.parametrize("M,Nn,K", [(640, 1024, 1024), (640, 1024, 4096), (5, 3072, 1024),
+                                    (300, 200, 640), (77, 4096, 1024), (1, 2048, 512)])
+def test_swap_ab_configs(gemm_path, na, cs, M, Nn, K):
+    """k_gemm_sw: every (activation tile, cluster K-split) gives the reference
+    result; for a given split the result is bitwise independent of the tile
+    and of M (cluster reduction in rank order)."""
+    if gemm_path != "sw":
+        pytest.skip("swap-AB only")
+    g = torch.Generator(device="cuda").manual_seed(M + Nn + K + na)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    x0 = torch.randn(M, Nn, device="cuda", generator=g)
+    outs = []
+    for n_a in (na, 16):
+        N.call("skb_gemm_force_sw", 2, n_a, cs)
+        x = x0.clone()
+        _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_RESID, x, Nn, N.F32, bias))
+        outs.append(x)
+    x1 = x0[M - 1:].clone()
+    _run("skb_gemm", N.BF16, A[M - 1:], W, _epi(N.EPI_RESID, x1, Nn, N.F32, bias))
+    torch.cuda.synchronize()
+    ref = x0.double() + A.double() @ W.double().T + bias.double()
+    assert (outs[0].double() - ref).abs().max().item() <= 2e-3 * K ** 0.5
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(x1[0], outs[0][M - 1])
+    out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+    N.call("skb_gemm_force_sw", 2, na, cs)
+    _run("skb_gemm", N.BF16, A, W, _epi(N.EPI_RELU, out, Nn, N.BF16, bias))
+    torch.cuda.synchronize()
+    want = torch.relu(A.float() @ W.float().T + bias)
+    assert torch.allclose(out.float(), want, rtol=1e-2, atol=0.005 * K ** 0.5)
+
+
+@pytest.mark.parametrize("na,cs", [(16, 1), (80, 2), (64, 4)])
+def test_swap_ab_ssru_cluster(gemm_path, na, cs):
+    """SSRU cell epilogue through the cluster reduction path."""
+    if gemm_path != "sw":
+        pytest.skip("swap-AB only")
+    M, d = 300, 512
+    g = torch.Generator(device="cuda").manual_seed(21)
+    h = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    Wi = (torch.randn(2 * d, d, device="cuda", generator=g) * 0.05).bfloat16()
+    bi = torch.randn(2 * d, device="cuda", generator=g)
+    bi[1::2] = 0
+    c_prev = torch.randn(M, d, device="cuda", generator=g)
+    src = torch.randint(0, M, (M,), device="cuda", generator=g, dtype=torch.int32)
+    c_next = torch.zeros(M, d, device="cuda")
+    x = torch.randn(M, d, device="cuda", generator=g)
+    x0 = x.clone()
+    N.call("skb_gemm_force_sw", 2, na, cs)
+    _run("skb_gemm", N.BF16, h, Wi, _epi(N.EPI_SSRU, x, d, N.F32, bi, c_prev, c_next, src, d))
+    z = h.double() @ Wi.double().T
+    f = torch.sigmoid(z[:, 0::2] + bi.double()[0::2])
+    c = f * c_prev.double()[src.long()] + (1 - f) * z[:, 1::2]
+    torch.cuda.synchronize()
+    assert (c_next.double() - c).abs().max().item() < 1e-3
+    assert (x.double() - (x0.double() + torch.relu(c))).abs().max().item() < 1e-3

@@ -1,0 +1,26 @@
+"""Launch one swap-AB GEMM shape/config a few times (for ncu captures).
+    python tools/gemm_one.py NAME NA CS [M]"""
+import ctypes as C
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2207_05851_b200 import _native as N  # noqa: E402
+
+shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024),
+          "out_proj": (32000, 1024)}
+name, na, cs = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+M = int(sys.argv[4]) if len(sys.argv) > 4 else 640
+Nn, K = shapes[name]
+A = torch.randn(M, K, device="cuda").bfloat16()
+W = torch.randn(Nn, K, device="cuda").bfloat16()
+out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None, 0,
+                 None, 0, None, 0, 1, None, 0, None, 0)
+N.call("skb_gemm_force_sw", 2 if na >= 0 else 1, max(na, 0), cs)
+for i in range(3):
+    N.call("skb_gemm", N.BF16, M, Nn, K, A.data_ptr(), K, W.data_ptr(), K, C.byref(epi),
+           torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
+print("ok")

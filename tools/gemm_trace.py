@@ -1,0 +1,49 @@
+"""Per-CTA timeline of one swap-AB GEMM launch (build with
+SKB_NVCC_EXTRA=-DSKB_GEMM_TRACE).  Prints, relative to the earliest CTA
+entry: entry, producer pdl-wait done, first stage landed, last MMA issued,
+accumulator ready, exit — min/median/max over CTAs (us)."""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2207_05851_b200 import _native as N  # noqa: E402
+
+M = 640
+shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024)}
+import os
+if os.environ.get("SHAPES"):
+    shapes = {k: shapes[k] for k in os.environ["SHAPES"].split(",")}
+cfgs = [(int(a), int(b)) for a, b in (x.split(",") for x in sys.argv[1:])] or [(0, 0)]
+for name, (Nn, K) in shapes.items():
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    Ws = [torch.randn(Nn, K, device="cuda").bfloat16() for _ in range(8)]
+    out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+    epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None, 0,
+                     None, 0, None, 0, 1, None, 0, None, 0)
+    for na, cs in cfgs:
+        N.call("skb_gemm_force_sw", 2, na, cs)
+        buf = (C.c_ulonglong * (1024 * 8))()
+        for i in range(8):  # warm; the last launch is traced (its weights cold)
+            if i == 7:
+                torch.cuda.synchronize()
+                N.call("skb_debug_gemm_trace", buf)  # clear
+            N.call("skb_gemm", N.BF16, M, Nn, K, A.data_ptr(), K, Ws[i].data_ptr(), K,
+                   C.byref(epi), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        N.call("skb_debug_gemm_trace", buf)
+        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
+        t = t[t[:, 0] > 0]
+        t0 = t[:, 0].min()
+        rel = (t[:, :7] - t0) / 1e3
+        labels = ["entry", "epi1done", "postwait", "stage0", "lastmma/red", "accready", "exit"]
+        print(f"{name} na={na} cs={cs} ctas={len(t)} sms={len(set(t[:, 7]))}")
+        for j, lab in enumerate(labels):
+            col = rel[:, j]
+            col = col[(col > -1e6) & (col < 1e6)]
+            if not len(col):
+                continue
+            print(f"   {lab:9s} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
+N.call("skb_gemm_force_sw", 0, 0, 0)
