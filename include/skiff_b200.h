@@ -277,8 +277,8 @@ int skb_debug_beam_prof(unsigned long long *host_buf_4096x10);
 
 /* Debug: per-CTA %globaltimer stamps of the last swap-AB GEMM launch
  * (entry, pre-wait, post-wait, first stage, last MMA, accumulator ready,
- * exit, smid) — builds with -DSKB_GEMM_TRACE only. */
-int skb_debug_gemm_trace(unsigned long long *host_buf_1024x8);
+ * exit, smid, reduction phases) — builds with -DSKB_GEMM_TRACE only. */
+int skb_debug_gemm_trace(unsigned long long *host_buf_1024x16);
 
 /* out[r] = max over positions l < len[b] of enc[b, l, :] (model.py:496-500). */
 int skb_masked_maxpool(int B, int L, int d, const float *enc, const int *lengths, float *out,

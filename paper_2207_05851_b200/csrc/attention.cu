@@ -470,6 +470,167 @@ __global__ void __launch_bounds__(256, 3) k_self_attn_vec(
   }
 }
 
+// Same mapping as k_self_attn_vec, software-pipelined: the ancestor slots
+// of 32 positions are held one per lane (loaded one 32-block ahead and
+// broadcast by shuffle), and the K/V of chunk c+1 are requested before chunk
+// c is reduced, so a warp keeps two chunks (2 x CH x 256 B) in flight and
+// pays one memory round trip per warp instead of one per chunk.
+template <int DH, int CH>
+__global__ void __launch_bounds__(256, 2) k_self_attn_pf(
+    int R, int H, const void *qkv, int ld_qkv, int qkv_dtype, __nv_bfloat16 *kc,
+    __nv_bfloat16 *vc, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
+    int ctx_dtype) {
+  PDL_ENTRY();
+  constexpr int LPK = DH / 8;      // lanes per key row (16 B each)
+  constexpr int KPI = 32 / LPK;    // keys per warp instruction
+  constexpr int ITER = CH / KPI;   // warp instructions per chunk (K and V each)
+  static_assert(CH <= 32 && 32 % CH == 0, "chunks must tile a 32-position block");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp, h = blockIdx.y;
+  if (r >= R) return;
+  const int D = H * DH;
+  const int t = *step;
+  const int sub = lane % LPK, grp = lane / LPK;
+  const int *arow = anc + ((size_t)(t & 1) * R + r) * S_max;
+  // ancestor slots, one position per lane: blocks 0 and 1 (positions < t)
+  int a_cur = lane < t ? __ldg(arow + lane) : r;
+  int a_nxt = 32 + lane < t ? __ldg(arow + 32 + lane) : r;
+  float q8[8];
+  {
+    const size_t base = (size_t)r * ld_qkv + h * DH + sub * 8;
+    const size_t cslot = (((size_t)r * H + h) * S_max + t) * DH + sub * 8;
+    if (qkv_dtype == SKB_BF16) {
+      const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(qkv);
+      const uint4 qv = *reinterpret_cast<const uint4 *>(src + base);
+      const __nv_bfloat162 *qp = reinterpret_cast<const __nv_bfloat162 *>(&qv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(qp[u]);
+        q8[2 * u] = f.x;
+        q8[2 * u + 1] = f.y;
+      }
+      if (grp == 0) {
+        *reinterpret_cast<uint4 *>(kc + cslot) = *reinterpret_cast<const uint4 *>(src + base + D);
+        *reinterpret_cast<uint4 *>(vc + cslot) = *reinterpret_cast<const uint4 *>(src + base + 2 * D);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q8[u] = load_f(qkv, qkv_dtype, base + u);
+      if (grp == 0)
+        for (int u = 0; u < 8; ++u) {
+          kc[cslot + u] = __float2bfloat16_rn(load_f(qkv, qkv_dtype, base + D + u));
+          vc[cslot + u] = __float2bfloat16_rn(load_f(qkv, qkv_dtype, base + 2 * D + u));
+        }
+    }
+  }
+  __threadfence_block();
+  __syncwarp();
+  // slot of position p of this chunk (block register `ab` holds p & ~31)
+  auto load_chunk = [&](int p0, int ab, uint4 *kk, uint4 *vv) {
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int p = p0 + it * KPI + grp;
+      const int sl = __shfl_sync(0xffffffffu, ab, p & 31);
+      if (p <= t) {
+        const size_t off = (((size_t)sl * H + h) * S_max + p) * DH + sub * 8;
+        kk[it] = *reinterpret_cast<const uint4 *>(kc + off);
+        vv[it] = *reinterpret_cast<const uint4 *>(vc + off);
+      } else {
+        kk[it] = vv[it] = make_uint4(0, 0, 0, 0);
+      }
+    }
+  };
+  float m_run = -INFINITY, l_run = 0.f;
+  float o8[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) o8[u] = 0.f;
+  uint4 kk[ITER], vv[ITER];
+  load_chunk(0, a_cur, kk, vv);
+  for (int p0 = 0; p0 <= t; p0 += CH) {
+    const int pn = p0 + CH;
+    uint4 kn[ITER], vn[ITER];
+    const bool more = pn <= t;
+    const bool newblk = (pn & 31) == 0;
+    if (more) load_chunk(pn, newblk ? a_nxt : a_cur, kn, vn);
+    if (newblk) {  // rotate the ancestor block registers; fetch two blocks ahead
+      a_cur = a_nxt;
+      const int q = pn + 32 + lane;
+      a_nxt = q < t ? __ldg(arow + q) : r;
+    }
+    float sc[ITER];
+    float cmax = -INFINITY;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kk[it]);
+      float a = 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(kp[u]);
+        a = fmaf(q8[2 * u], f.x, a);
+        a = fmaf(q8[2 * u + 1], f.y, a);
+      }
+#pragma unroll
+      for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      sc[it] = (p0 + it * KPI + grp) <= t ? a * scale : -INFINITY;
+      cmax = fmaxf(cmax, sc[it]);
+    }
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    const float mnew = fmaxf(m_run, cmax);
+    const float corr = m_run == -INFINITY ? 0.f : expf(m_run - mnew);
+    float psum = 0.f;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      sc[it] = sc[it] == -INFINITY ? 0.f : expf(sc[it] - mnew);
+      psum += sc[it];
+    }
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+    l_run = l_run * corr + psum;
+    m_run = mnew;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o8[u] *= corr;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv[it]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(vp[u]);
+        o8[2 * u] = fmaf(sc[it], f.x, o8[2 * u]);
+        o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
+      }
+    }
+    if (more) {
+#pragma unroll
+      for (int it = 0; it < ITER; ++it) {
+        kk[it] = kn[it];
+        vv[it] = vn[it];
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int o = LPK; o < 32; o <<= 1) o8[u] += __shfl_xor_sync(0xffffffffu, o8[u], o);
+  if (grp == 0) {
+    const float inv = 1.0f / l_run;
+    const size_t ob = (size_t)r * ldc + h * DH + sub * 8;
+    if (ctx_dtype == SKB_BF16) {
+      uint4 w;
+      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        __nv_bfloat162 pr = __floats2bfloat162_rn(o8[2 * u] * inv, o8[2 * u + 1] * inv);
+        wp[u] = *reinterpret_cast<uint32_t *>(&pr);
+      }
+      *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(ctx) + ob) = w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) reinterpret_cast<float *>(ctx)[ob + u] = o8[u] * inv;
+    }
+  }
+}
+
 static float attn_scale(int dh) { return (float)(1.0 / sqrt((double)dh)); }
 
 // ------------------------- grouped attention, bf16 K/V in shared memory
@@ -909,7 +1070,15 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
     auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
     auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
     const float sc = attn_scale(dh);
-    if (dh == 64)
+    static int pf = -1;
+    if (pf < 0) {
+      const char *e = getenv("SKB_ATTN_PF");
+      pf = e ? atoi(e) : 0;  // measured slower in the decode graph (fewer resident warps)
+    }
+    if (dh == 64 && pf)
+      launch_k(k_self_attn_pf<64, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
+               qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
+    else if (dh == 64)
       launch_k(k_self_attn_vec<64, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
                qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     else if (dh == 32)

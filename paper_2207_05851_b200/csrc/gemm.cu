@@ -769,14 +769,14 @@ void init_forces() {
 namespace sw {
 
 #ifdef SKB_GEMM_TRACE
-__device__ unsigned long long g_trace[1024 * 8];
+__device__ unsigned long long g_trace[1024 * 16];
 __device__ int g_dbg;
 #define SW_STAMP(slot)                                                                    \
   do {                                                                                    \
     unsigned long long _t;                                                                \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                \
     const int _c = blockIdx.x + blockIdx.y * gridDim.x;                                   \
-    if (_c < 1024) g_trace[_c * 8 + (slot)] = _t;                                         \
+    if (_c < 1024) g_trace[_c * 16 + (slot)] = _t;                                         \
   } while (0)
 #else
 #define SW_STAMP(slot) \
@@ -889,11 +889,14 @@ __device__ __forceinline__ void stage16(uint32_t base, bool bf16, int mloc, int 
 
 // Epilogue warps: make the staged tile visible to the TMA unit, then one
 // thread writes it with a bulk tensor store (x += tile for the residual).
-template <int KIND>
+// `before_store` runs on all 128 epilogue threads once the tile is complete
+// in shared memory and before the store is issued.
+template <int KIND, typename F>
 __device__ __forceinline__ void flush_tile(const CUtensorMap *tmO, uint32_t base, int c0, int c1,
-                                           bool leader) {
+                                           bool leader, F before_store) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("bar.sync 1, 128;" ::: "memory");
+  before_store();
   if (leader) {
     if (KIND == SKB_EPI_RESID)
       asm volatile(
@@ -908,6 +911,80 @@ __device__ __forceinline__ void flush_tile(const CUtensorMap *tmO, uint32_t base
                    : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// LOGITS epilogue (model.py:577-581, kernels.py:287-295): partial
+// log-softmax statistics (max, sum exp(x - max)) of every 32-column group of
+// the staged fp32 logit tile, over the row's active columns.  Eight lanes
+// share a group (4 values each, one 16-byte shared load), so a warp reads
+// one whole 512-byte tile row per instruction (conflict-free); the group
+// reductions are fixed shuffle trees (deterministic, M-independent).
+__device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int M, int N, int m0,
+                                             int n0, int rows, int warp_e, int lane) {
+  constexpr int U = 4;  // independent tile rows per iteration (shuffle-latency ILP)
+  const int g = lane >> 3, sub = lane & 7;  // group within the tile row, lane within group
+  const int n = n0 + g * 32;
+  unsigned tail = 0xffffffffu;
+  if (n >= N) tail = 0u;
+  else if (N - n < 32) tail = (1u << (N - n)) - 1u;
+#pragma unroll 1
+  for (int ml0 = warp_e; ml0 < rows && m0 + ml0 < M; ml0 += 4 * U) {
+    float4 f[U];
+    unsigned b4[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ml = ml0 + 4 * u;
+      const int m = m0 + ml;
+      b4[u] = 0u;
+      f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ml < rows && m < M) {
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(f[u].x), "=f"(f[u].y), "=f"(f[u].z), "=f"(f[u].w)
+                     : "r"(stg + (uint32_t)(ml * 128 + lane * 4) * 4u));
+        unsigned bits = tail;
+        if (e.mask && tail) bits &= e.mask[(size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5)];
+        b4[u] = (bits >> (sub * 4)) & 0xfu;
+      }
+    }
+    // branch-free: masked columns become -inf; ex2.approx (SFU) on x - max,
+    // whose log-sum-exp differs from expf's by < 1e-6 relative
+    float mx[U], sm[U], x[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x[u][0] = (b4[u] & 1u) ? f[u].x : -INFINITY;
+      x[u][1] = (b4[u] & 2u) ? f[u].y : -INFINITY;
+      x[u][2] = (b4[u] & 4u) ? f[u].z : -INFINITY;
+      x[u][3] = (b4[u] & 8u) ? f[u].w : -INFINITY;
+      mx[u] = fmaxf(fmaxf(x[u][0], x[u][1]), fmaxf(x[u][2], x[u][3]));
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) mx[u] = fmaxf(mx[u], __shfl_xor_sync(0xffffffffu, mx[u], o));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float ml2 = mx[u] == -INFINITY ? 0.f : mx[u] * 1.4426950408889634f;
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float e2;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(fmaf(x[u][q], 1.4426950408889634f, -ml2)));
+        acc += e2;  // ex2(-inf) = +0 for masked columns
+      }
+      sm[u] = acc;
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) sm[u] += __shfl_xor_sync(0xffffffffu, sm[u], o);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ml = ml0 + 4 * u, m = m0 + ml;
+      if (sub == 0 && n < N && ml < rows && m < M)
+        reinterpret_cast<float2 *>(e.lse_part)[(size_t)m * e.lse_ld + (n >> 5)] =
+            make_float2(mx[u], sm[u]);
+    }
   }
 }
 
@@ -1060,8 +1137,16 @@ __global__ void __launch_bounds__(192, 1)
         else
           epi16<KIND>(ep, cprev, cnext, M, m0 + c, n, nok, bn, v);
       }
-      if (KIND != SKB_EPI_SSRU && tma_out && dbg != 1)
-        flush_tile<KIND>(&tmO, stg, n0, m0, warp == 2 && lane == 0);
+      if (KIND != SKB_EPI_SSRU && tma_out && dbg != 1) {
+        // LOGITS: group statistics from the staged tile, before the store
+        // engine starts reading it
+        flush_tile<KIND>(&tmO, stg, n0, m0, warp == 2 && lane == 0, [&] {
+          if (warp == 3 && lane == 0) SW_STAMP(11);
+          if (KIND == SKB_EPI_LOGITS && dbg != 3)
+            logits_stats(ep, stg, M, N, m0, n0, Na, warp - 2, lane);
+          if (warp == 3 && lane == 0) SW_STAMP(12);
+        });
+      }
     } else {
       // park the fp32 partial in my shared memory: part[m][128] (row-major
       // in m, so the slice each peer finishes is one contiguous block)
@@ -1093,6 +1178,7 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t part = smem_u32(smem);
     const uint32_t recv = part + (uint32_t)Na * 512u;  // [CS][cpr][128] fp32
     cluster_sync_all();  // all partials written, every ring drained
+    if (warp == 2 && lane == 0) SW_STAMP(8);
     if (warp == 2 && lane == 0) {
 #pragma unroll 1
       for (int p = 0; p < CS; ++p) {
@@ -1110,6 +1196,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t stg = smem_u32(smem) + (uint32_t)stg_off;
       const bool bf16 = ep.out_dtype == SKB_BF16 && KIND != SKB_EPI_RESID;
       mbar_wait(rbar, 0);
+      if (warp == 2 && lane == 0) SW_STAMP(9);
 #pragma unroll 1
       for (int j0 = 0; j0 < cpr && m0 + c0 + j0 < M; j0 += 16) {
         float v[16];
@@ -1134,8 +1221,9 @@ __global__ void __launch_bounds__(192, 1)
           epi16<KIND>(ep, cprev, cnext, lim, m0 + c0 + j0, n, nok, bn, v);
         }
       }
+      if (warp == 2 && lane == 0) SW_STAMP(10);
       if (KIND != SKB_EPI_SSRU && tma_out)
-        flush_tile<KIND>(&tmO, stg, n0, m0 + c0, warp == 2 && lane == 0);
+        flush_tile<KIND>(&tmO, stg, n0, m0 + c0, warp == 2 && lane == 0, [] {});
     }
     if (warp == 2 && lane == 0) SW_STAMP(4);
     cluster_sync_all();  // peers are done reading my shared memory
@@ -1147,7 +1235,7 @@ __global__ void __launch_bounds__(192, 1)
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     const int c = blockIdx.x + blockIdx.y * gridDim.x;
-    if (c < 1024) g_trace[c * 8 + 7] = smid;
+    if (c < 1024) g_trace[c * 16 + 7] = smid;
   }
 #endif
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1266,7 +1354,18 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   const int part_bytes = CS > 1 ? 2 * Na * 512 : 0;  // partial + receive slots
   const int stg_off = (part_bytes + 1023) & ~1023;
   const int need = tma_out ? stg_off + ((rows_box + 15) / 16 * 16) * 128 * es : part_bytes;
-  int stages = (SMEM_MAX - 1024 - 512) / SB;
+  // Ring budget: half the SM by default, so the next kernel's CTA (PDL)
+  // can become resident beside this one and prefetch its weights while this
+  // one drains; the per-SM TMA ingest (~80-120 GB/s) is already reached
+  // with ~100 KB in flight.  SKB_SW_SMEM overrides (bytes).
+  static int budget = -1;
+  if (budget < 0) {
+    const char *e = getenv("SKB_SW_SMEM");
+    budget = e ? atoi(e) : 113 * 1024;
+    if (budget > SMEM_MAX) budget = SMEM_MAX;
+  }
+  int stages = (budget - 1024 - 512) / SB;
+  if (stages < 2) stages = 2;
   if (stages > nkc) stages = nkc;
   if (stages * SB < need) stages = (need + SB - 1) / SB;
   if (stages < 1 || stages * SB + 1024 + 512 > SMEM_MAX)
@@ -1286,6 +1385,9 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
       return launch_k2<SKB_EPI_RESID>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
     case SKB_EPI_SSRU:
       return launch_k2<SKB_EPI_SSRU>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
+    case SKB_EPI_LOGITS:
+      if (CS != 1 || !tma_out) return fail(SKB_ERR_CONFIG, "gemm_sw: LOGITS needs CS=1 and TMA output");
+      return launch_t<SKB_EPI_LOGITS, 1>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
     default:
       return launch_k2<SKB_EPI_STORE>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
   }
@@ -1301,19 +1403,22 @@ static int pick_cs(int N, int K) {
   return 1;
 }
 
-// Activation tile Na for the actual M: one wave of CTAs over the SMs with
-// the fewest bytes streamed per CTA.
+// Activation tile Na for the actual M (numerics do not depend on it).  Cost
+// model fitted to the tools/gemm_sweep.py sweep on B200 (M = 64..1280): two
+// CTAs co-reside per SM (113 KB ring), each streams (128 + Na) rows of K,
+// plus a fixed per-CTA cost worth ~160 rows; CTA slots beyond one wave
+// cost proportionally.
 static int pick_na(int M, int N, int CS) {
-  const int nsm = tc::num_sms();
+  const int slots = 2 * tc::num_sms();
   const int n_wt = (N + 127) / 128;
-  const int na_max = CS > 1 ? 160 : 256;  // partial + receive slots must fit in smem
+  const int na_max = CS > 1 ? 80 : 160;  // split-K partial + receive slots fit the ring
   int best = 16;
   double best_c = 1e30;
   for (int na = 16; na <= na_max; na += 16) {
     if (CS > 1 && na % (4 * CS)) continue;
-    const long ctas = (long)n_wt * ((M + na - 1) / na) * CS;
-    const long waves = (ctas + nsm - 1) / nsm;
-    const double c = waves * (128.0 + na + 96.0);
+    const double ctas = (double)n_wt * ((M + na - 1) / na) * CS;
+    const double waves = ctas <= slots ? 1.0 : ctas / slots;
+    const double c = waves * (128.0 + na + 160.0);
     if (c < best_c * 0.999) {
       best_c = c;
       best = na;
@@ -1477,7 +1582,7 @@ extern "C" int skb_gemm_force_sw(int mode, int na, int cs) {
 extern "C" int skb_debug_gemm_trace(unsigned long long *host) {
 #ifdef SKB_GEMM_TRACE
   cudaMemcpyFromSymbol(host, sw::g_trace, sizeof(sw::g_trace));
-  static unsigned long long zeros[1024 * 8];
+  static unsigned long long zeros[1024 * 16];
   cudaMemcpyToSymbol(sw::g_trace, zeros, sizeof(zeros));  // read-and-clear
   return SKB_OK;
 #else
@@ -1507,8 +1612,10 @@ extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int ld
   if (!tma_ok) return gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, ep, st);
   // decode-sized M: swap-AB kernel (weights on the MMA M side)
   sw::init_mode();
-  if (sw::g_mode != 1 && epi->kind != SKB_EPI_LOGITS && (sw::g_mode == 2 || M <= 1024)) {
-    const int cs = sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K);
+  const bool logits_tma = epi->kind != SKB_EPI_LOGITS ||
+                          ((reinterpret_cast<uintptr_t>(epi->out) & 15) == 0 && epi->ldo % 4 == 0);
+  if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || M <= 1024)) {
+    const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);
     return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs);
   }

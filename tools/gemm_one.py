@@ -16,11 +16,23 @@ Nn, K = shapes[name]
 A = torch.randn(M, K, device="cuda").bfloat16()
 W = torch.randn(Nn, K, device="cuda").bfloat16()
 out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
-epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None, 0,
-                 None, 0, None, 0, 1, None, 0, None, 0)
+import os
+if os.environ.get("LOGITS"):
+    out = torch.zeros(M, Nn, device="cuda")
+    part = torch.zeros(M, 2 * ((Nn + 31) // 32), device="cuda")
+    epi = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None, 0,
+                     part.data_ptr(), part.shape[1] // 2, None, 0, 1, None, 0, None, 0)
+else:
+    epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None, 0,
+                     None, 0, None, 0, 1, None, 0, None, 0)
 N.call("skb_gemm_force_sw", 2 if na >= 0 else 1, max(na, 0), cs)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for i in range(3):
+    if i == 2:
+        torch.cuda.synchronize()
+        e0.record()
     N.call("skb_gemm", N.BF16, M, Nn, K, A.data_ptr(), K, W.data_ptr(), K, C.byref(epi),
            torch.cuda.current_stream().cuda_stream)
+e1.record()
 torch.cuda.synchronize()
-print("ok")
+print(f"{name} na={na} cs={cs} M={M} logits={bool(os.environ.get('LOGITS'))}: {e0.elapsed_time(e1) * 1e3:.1f} us")

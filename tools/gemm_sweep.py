@@ -16,7 +16,7 @@ sys.path.insert(0, ".")
 from paper_2207_05851_b200 import _native as N  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 640
-SHAPES = {"ssru": (2048, 1024), "qkv": (3072, 1024), "wo": (1024, 1024), "ffn1": (4096, 1024), "ffn2": (1024, 4096),
+SHAPES = {"qkv": (3072, 1024), "wo": (1024, 1024), "ffn1": (4096, 1024), "ffn2": (1024, 4096),
           "out_proj": (32000, 1024)}
 REPS = 24
 dev = "cuda"
@@ -69,11 +69,12 @@ for name, (Nn, K) in SHAPES.items():
         torch.matmul(A, Ws[r % ncopy].T, out=out)
 
     us = time_graph(cublas, REPS)
-    out_rows.append(dict(shape=name, cfg="cublas", us=round(us, 2), tflops=round(flops / us / 1e6, 1)))
+    out_rows.append(dict(shape=name, M=M, cfg="cublas", us=round(us, 2),
+                         tflops=round(flops / us / 1e6, 1)))
     print(json.dumps(out_rows[-1]), flush=True)
     cfgs = [("tc auto", 1, 0, 0), ("sw auto", 2, 0, 0)]
-    for na in (32, 48, 64, 80, 96, 112, 128, 160, 192, 256):
-        for cs in (1, 2, 4):
+    for na in (32, 48, 64, 80, 96, 128, 160, 256):
+        for cs in ((1, 4) if K >= 4096 else (1,)):
             if cs > 1 and na % (4 * cs):
                 continue
             cfgs.append((f"sw na{na} cs{cs}", 2, na, cs))
@@ -88,7 +89,7 @@ for name, (Nn, K) in SHAPES.items():
         except Exception as e:  # noqa: BLE001
             print(json.dumps(dict(shape=name, cfg=label, error=str(e)[:80])))
             break
-        out_rows.append(dict(shape=name, cfg=label, us=round(us, 2),
+        out_rows.append(dict(shape=name, M=M, cfg=label, us=round(us, 2),
                              tflops=round(flops / us / 1e6, 1), err=round(err, 4)))
         print(json.dumps(out_rows[-1]), flush=True)
     lib.skb_gemm_force_sw(0, 0, 0)

@@ -12,33 +12,42 @@ sys.path.insert(0, ".")
 from paper_2207_05851_b200 import _native as N  # noqa: E402
 
 M = 640
-shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024)}
+shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024),
+          "out_proj": (32000, 1024)}
 import os
 if os.environ.get("SHAPES"):
     shapes = {k: shapes[k] for k in os.environ["SHAPES"].split(",")}
 cfgs = [(int(a), int(b)) for a, b in (x.split(",") for x in sys.argv[1:])] or [(0, 0)]
 for name, (Nn, K) in shapes.items():
     A = torch.randn(M, K, device="cuda").bfloat16()
-    Ws = [torch.randn(Nn, K, device="cuda").bfloat16() for _ in range(8)]
-    out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
-    epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None, 0,
-                     None, 0, None, 0, 1, None, 0, None, 0)
+    Ws = [torch.randn(Nn, K, device="cuda").bfloat16() for _ in range(8 if Nn * K < 1e8 / 2 else 2)]
+    if os.environ.get("LOGITS"):
+        out = torch.zeros(M, Nn, device="cuda")
+        part = torch.zeros(M, 2 * ((Nn + 31) // 32), device="cuda")
+        epi = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None,
+                         0, part.data_ptr(), part.shape[1] // 2, None, 0, 1, None, 0, None, 0)
+    else:
+        out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+        epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None,
+                         0, None, 0, None, 0, 1, None, 0, None, 0)
     for na, cs in cfgs:
         N.call("skb_gemm_force_sw", 2, na, cs)
-        buf = (C.c_ulonglong * (1024 * 8))()
+        buf = (C.c_ulonglong * (1024 * 16))()
         for i in range(8):  # warm; the last launch is traced (its weights cold)
             if i == 7:
                 torch.cuda.synchronize()
                 N.call("skb_debug_gemm_trace", buf)  # clear
-            N.call("skb_gemm", N.BF16, M, Nn, K, A.data_ptr(), K, Ws[i].data_ptr(), K,
+            N.call("skb_gemm", N.BF16, M, Nn, K, A.data_ptr(), K, Ws[i % len(Ws)].data_ptr(), K,
                    C.byref(epi), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         N.call("skb_debug_gemm_trace", buf)
-        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8).astype(np.int64)
+        t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16).astype(np.int64)
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        rel = (t[:, :7] - t0) / 1e3
-        labels = ["entry", "epi1done", "postwait", "stage0", "lastmma/red", "accready", "exit"]
+        cols = [0, 2, 3, 5, 1, 8, 9, 10, 4, 11, 12, 6]
+        rel = (t[:, cols] - t0) / 1e3
+        labels = ["entry", "postwait", "stage0", "accready", "partial", "csync", "recv", "summed",
+                  "stored", "flushed", "stats", "exit"]
         print(f"{name} na={na} cs={cs} ctas={len(t)} sms={len(set(t[:, 7]))}")
         for j, lab in enumerate(labels):
             col = rel[:, j]
