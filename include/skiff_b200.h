@@ -280,6 +280,11 @@ int skb_debug_beam_prof(unsigned long long *host_buf_4096x10);
  * exit, smid, reduction phases) — builds with -DSKB_GEMM_TRACE only. */
 int skb_debug_gemm_trace(unsigned long long *host_buf_1024x16);
 
+/* Debug: per-CTA %globaltimer stamps of the last tensor-core self-attention
+ * launch (entry, after PDL wait, walk, entries, staged, attended) — builds
+ * with -DSKB_ATTN_TRACE only; read-and-clear. */
+int skb_debug_attn_trace(unsigned long long *host_buf_4096x8);
+
 /* out[r] = max over positions l < len[b] of enc[b, l, :] (model.py:496-500). */
 int skb_masked_maxpool(int B, int L, int d, const float *enc, const int *lengths, float *out,
                        void *stream);

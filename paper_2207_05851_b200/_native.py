@@ -73,6 +73,7 @@ SIGNATURES = {
     "skb_set_device": [i32],
     "skb_debug_beam_prof": [vp],
     "skb_debug_gemm_trace": [vp],
+    "skb_debug_attn_trace": [vp],
 }
 
 _lib = None

@@ -17,6 +17,8 @@
 #include "common.cuh"
 
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 namespace skb {
 
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(128) k_self_attention_step(
   const int t = *step;
   const size_t qrow = (size_t)r * ld_qkv;
   // store this step's k, v at slot (r, t)
-  const size_t cslot = (((size_t)r * H + h) * S_max + t) * dh;
+  const size_t cslot = (((size_t)r * S_max + t) * H + h) * dh;
   for (int c = lane; c < dh; c += 32) {
     qs[warp][c] = load_f(qkv, qkv_dtype, qrow + h * dh + c);
     store_f(kc, cache_dtype, cslot + c, load_f(qkv, qkv_dtype, qrow + D + h * dh + c));
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(128) k_self_attention_step(
     const void *vrow = nullptr;
     if (p <= t) {
       const int slot = p == t ? r : arow[p];
-      const size_t off = (((size_t)slot * H + h) * S_max + p) * dh;
+      const size_t off = (((size_t)slot * S_max + p) * H + h) * dh;
       s = dot_row(elem_ptr(kc, cache_dtype, off), cache_dtype, qs[warp], dh) * scale;
       vrow = elem_ptr(vc, cache_dtype, off);
     }
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(256, 3) k_self_attn_vec(
   float q8[8];
   {
     const size_t base = (size_t)r * ld_qkv + h * DH + sub * 8;
-    const size_t cslot = (((size_t)r * H + h) * S_max + t) * DH + sub * 8;
+    const size_t cslot = (((size_t)r * S_max + t) * H + h) * DH + sub * 8;
     if (qkv_dtype == SKB_BF16) {
       const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(qkv);
       const uint4 qv = *reinterpret_cast<const uint4 *>(src + base);
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(256, 3) k_self_attn_vec(
     for (int it = 0; it < ITER; ++it) {
       const int p = p0 + it * KPI + grp;
       if (sl[it] >= 0) {
-        const size_t off = (((size_t)sl[it] * H + h) * S_max + p) * DH + sub * 8;
+        const size_t off = (((size_t)sl[it] * S_max + p) * H + h) * DH + sub * 8;
         kk[it] = *reinterpret_cast<const uint4 *>(kc + off);
         vv[it] = *reinterpret_cast<const uint4 *>(vc + off);
       } else {
@@ -447,167 +449,6 @@ __global__ void __launch_bounds__(256, 3) k_self_attn_vec(
     for (int it = 0; it < ITER; ++it) sl[it] = sn[it];
   }
   // reduce the KPI key groups; lanes of group 0 own the output
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) o8[u] += __shfl_xor_sync(0xffffffffu, o8[u], o);
-  if (grp == 0) {
-    const float inv = 1.0f / l_run;
-    const size_t ob = (size_t)r * ldc + h * DH + sub * 8;
-    if (ctx_dtype == SKB_BF16) {
-      uint4 w;
-      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        __nv_bfloat162 pr = __floats2bfloat162_rn(o8[2 * u] * inv, o8[2 * u + 1] * inv);
-        wp[u] = *reinterpret_cast<uint32_t *>(&pr);
-      }
-      *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(ctx) + ob) = w;
-    } else {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) reinterpret_cast<float *>(ctx)[ob + u] = o8[u] * inv;
-    }
-  }
-}
-
-// Same mapping as k_self_attn_vec, software-pipelined: the ancestor slots
-// of 32 positions are held one per lane (loaded one 32-block ahead and
-// broadcast by shuffle), and the K/V of chunk c+1 are requested before chunk
-// c is reduced, so a warp keeps two chunks (2 x CH x 256 B) in flight and
-// pays one memory round trip per warp instead of one per chunk.
-template <int DH, int CH>
-__global__ void __launch_bounds__(256, 2) k_self_attn_pf(
-    int R, int H, const void *qkv, int ld_qkv, int qkv_dtype, __nv_bfloat16 *kc,
-    __nv_bfloat16 *vc, int S_max, const int *anc, const int *step, float scale, void *ctx, int ldc,
-    int ctx_dtype) {
-  PDL_ENTRY();
-  constexpr int LPK = DH / 8;      // lanes per key row (16 B each)
-  constexpr int KPI = 32 / LPK;    // keys per warp instruction
-  constexpr int ITER = CH / KPI;   // warp instructions per chunk (K and V each)
-  static_assert(CH <= 32 && 32 % CH == 0, "chunks must tile a 32-position block");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + warp, h = blockIdx.y;
-  if (r >= R) return;
-  const int D = H * DH;
-  const int t = *step;
-  const int sub = lane % LPK, grp = lane / LPK;
-  const int *arow = anc + ((size_t)(t & 1) * R + r) * S_max;
-  // ancestor slots, one position per lane: blocks 0 and 1 (positions < t)
-  int a_cur = lane < t ? __ldg(arow + lane) : r;
-  int a_nxt = 32 + lane < t ? __ldg(arow + 32 + lane) : r;
-  float q8[8];
-  {
-    const size_t base = (size_t)r * ld_qkv + h * DH + sub * 8;
-    const size_t cslot = (((size_t)r * H + h) * S_max + t) * DH + sub * 8;
-    if (qkv_dtype == SKB_BF16) {
-      const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(qkv);
-      const uint4 qv = *reinterpret_cast<const uint4 *>(src + base);
-      const __nv_bfloat162 *qp = reinterpret_cast<const __nv_bfloat162 *>(&qv);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 f = __bfloat1622float2(qp[u]);
-        q8[2 * u] = f.x;
-        q8[2 * u + 1] = f.y;
-      }
-      if (grp == 0) {
-        *reinterpret_cast<uint4 *>(kc + cslot) = *reinterpret_cast<const uint4 *>(src + base + D);
-        *reinterpret_cast<uint4 *>(vc + cslot) = *reinterpret_cast<const uint4 *>(src + base + 2 * D);
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) q8[u] = load_f(qkv, qkv_dtype, base + u);
-      if (grp == 0)
-        for (int u = 0; u < 8; ++u) {
-          kc[cslot + u] = __float2bfloat16_rn(load_f(qkv, qkv_dtype, base + D + u));
-          vc[cslot + u] = __float2bfloat16_rn(load_f(qkv, qkv_dtype, base + 2 * D + u));
-        }
-    }
-  }
-  __threadfence_block();
-  __syncwarp();
-  // slot of position p of this chunk (block register `ab` holds p & ~31)
-  auto load_chunk = [&](int p0, int ab, uint4 *kk, uint4 *vv) {
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int p = p0 + it * KPI + grp;
-      const int sl = __shfl_sync(0xffffffffu, ab, p & 31);
-      if (p <= t) {
-        const size_t off = (((size_t)sl * H + h) * S_max + p) * DH + sub * 8;
-        kk[it] = *reinterpret_cast<const uint4 *>(kc + off);
-        vv[it] = *reinterpret_cast<const uint4 *>(vc + off);
-      } else {
-        kk[it] = vv[it] = make_uint4(0, 0, 0, 0);
-      }
-    }
-  };
-  float m_run = -INFINITY, l_run = 0.f;
-  float o8[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) o8[u] = 0.f;
-  uint4 kk[ITER], vv[ITER];
-  load_chunk(0, a_cur, kk, vv);
-  for (int p0 = 0; p0 <= t; p0 += CH) {
-    const int pn = p0 + CH;
-    uint4 kn[ITER], vn[ITER];
-    const bool more = pn <= t;
-    const bool newblk = (pn & 31) == 0;
-    if (more) load_chunk(pn, newblk ? a_nxt : a_cur, kn, vn);
-    if (newblk) {  // rotate the ancestor block registers; fetch two blocks ahead
-      a_cur = a_nxt;
-      const int q = pn + 32 + lane;
-      a_nxt = q < t ? __ldg(arow + q) : r;
-    }
-    float sc[ITER];
-    float cmax = -INFINITY;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kk[it]);
-      float a = 0.f;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 f = __bfloat1622float2(kp[u]);
-        a = fmaf(q8[2 * u], f.x, a);
-        a = fmaf(q8[2 * u + 1], f.y, a);
-      }
-#pragma unroll
-      for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      sc[it] = (p0 + it * KPI + grp) <= t ? a * scale : -INFINITY;
-      cmax = fmaxf(cmax, sc[it]);
-    }
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    const float mnew = fmaxf(m_run, cmax);
-    const float corr = m_run == -INFINITY ? 0.f : expf(m_run - mnew);
-    float psum = 0.f;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      sc[it] = sc[it] == -INFINITY ? 0.f : expf(sc[it] - mnew);
-      psum += sc[it];
-    }
-#pragma unroll
-    for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
-    l_run = l_run * corr + psum;
-    m_run = mnew;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) o8[u] *= corr;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv[it]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 f = __bfloat1622float2(vp[u]);
-        o8[2 * u] = fmaf(sc[it], f.x, o8[2 * u]);
-        o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
-      }
-    }
-    if (more) {
-#pragma unroll
-      for (int it = 0; it < ITER; ++it) {
-        kk[it] = kn[it];
-        vv[it] = vn[it];
-      }
-    }
-  }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
@@ -1019,6 +860,340 @@ static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, 
 
 using namespace skb;
 
+// --------------- decoder self-attention on tensor cores, beam-shared
+// model.py:559-566 (kernels.py:510-547) for the G beam rows of a sentence.
+// The rows descend from one beam tree, so most (slot, position) cache
+// entries they reference are shared: at the benchmark only ~20% of the
+// per-row K/V reads are distinct.  A CTA owns (G rows, HG heads), one warp
+// per head:
+//   walk   warps scan 32-position blocks (one position per lane): ancestor
+//          slots of the G rows, distinct slots per position, block scans ->
+//          entry e = (slot, p) in position order, and a bitmask per row of
+//          the entries on its path;
+//   stage  the distinct entries' K and V rows for the CTA's HG heads are one
+//          contiguous 16*HG-element run each in the [slot][pos][head][dh]
+//          cache, moved by cp.async.bulk (TMA engine, mbarrier completion)
+//          into padded shared rows; position t comes from this step's qkv;
+//   attend per warp, a 16-row (G used) dense attention over the staged
+//          entries with mma.sync m16n8k16: S = Q K^T, the path mask, online
+//          softmax, O += P V (ldmatrix.trans).  More than CAP entries are
+//          processed in passes (online softmax carries across).
+#ifdef SKB_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[4096 * 8];
+#define AT_STAMP(slot)                                                                   \
+  do {                                                                                   \
+    if (threadIdx.x == 0) {                                                              \
+      unsigned long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                             \
+      const int _c = blockIdx.x + blockIdx.y * gridDim.x;                                \
+      if (_c < 4096) g_attn_trace[_c * 8 + (slot)] = _t;                                 \
+    }                                                                                    \
+  } while (0)
+#else
+#define AT_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+
+template <int DH, int HG, int GW>
+__global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
+    int R, int H, int G, const __nv_bfloat16 *__restrict__ qkv, int ld_qkv,
+    __nv_bfloat16 *kc, __nv_bfloat16 *vc, int S_max, const int *__restrict__ anc,
+    const int *__restrict__ step, float scale, __nv_bfloat16 *__restrict__ ctx, int ldc, int cap) {
+  constexpr int RUN = HG * DH * 2;       // bytes of one entry's K (or V) for the CTA's heads
+  constexpr int EP = RUN + 16;           // padded entry pitch in shared memory
+  extern __shared__ __align__(128) uint8_t sm_tc[];
+  uint8_t *Ks = sm_tc;                                    // [cap][EP]
+  uint8_t *Vs = Ks + (size_t)cap * EP;                    // [cap][EP]
+  const int EMAX = G * S_max;                             // entries upper bound
+  int *bstart = reinterpret_cast<int *>(Vs + (size_t)cap * EP);  // [nblk + 1]
+  short *esrc = reinterpret_cast<short *>(bstart + (S_max + 31) / 32 + 2);  // [EMAX] slot or -1-row
+  short *epos = esrc + EMAX;                              // [EMAX]
+  short *pent = epos + EMAX;                              // [S_max][GW] distinct slots per position
+  unsigned char *ek = reinterpret_cast<unsigned char *>(pent + (size_t)S_max * GW);  // [EMAX]
+  unsigned char *ploc = ek + EMAX;                        // [GW][S_max]
+  unsigned char *pcnt = ploc + (size_t)GW * S_max;        // [S_max]
+  short *pexcl = reinterpret_cast<short *>(
+      (reinterpret_cast<uintptr_t>(pcnt + S_max) + 1) & ~uintptr_t(1));  // [S_max]
+  AT_STAMP(0);
+  PDL_ENTRY();
+  AT_STAMP(1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * G, nr = min(G, R - r0);
+  const int h0 = blockIdx.y * HG;
+  const int t = *step, D = H * DH;
+  const int nblk = (t + 32) / 32;
+  const int *arow = anc + (size_t)(t & 1) * R * S_max;
+  const uint32_t ks_s = static_cast<uint32_t>(__cvta_generic_to_shared(Ks));
+  const uint32_t vs_s = static_cast<uint32_t>(__cvta_generic_to_shared(Vs));
+  // stage entry (slot or -1-row, position) into row ej of the current pass:
+  // the warp's lanes each copy 16-byte chunks of its K and V runs (cp.async)
+  auto stage = [&](int ej, int sl, int p) {
+    const __nv_bfloat16 *ksrc, *vsrc;
+    if (sl >= 0) {
+      const size_t off = (((size_t)sl * S_max + p) * H + h0) * DH;
+      ksrc = kc + off;
+      vsrc = vc + off;
+    } else {  // position t: this step's qkv row
+      ksrc = qkv + (size_t)(-1 - sl) * ld_qkv + D + h0 * DH;
+      vsrc = ksrc + D;
+    }
+#pragma unroll
+    for (int c = lane; c < RUN / 16; c += 32) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ks_s + (uint32_t)(ej * EP + c * 16)),
+                   "l"(ksrc + c * 8)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vs_s + (uint32_t)(ej * EP + c * 16)),
+                   "l"(vsrc + c * 8)
+                   : "memory");
+    }
+  };
+  // ---- walk, sweep 1: one 32-position block per warp (one position per
+  // lane): ancestor slots of the G rows, distinct slots per position (first
+  // row wins), block-local scan
+  for (int blk = warp; blk < nblk; blk += HG) {
+    const int p = blk * 32 + lane;
+    const bool valid = p <= t;
+    int sl[GW], loc[GW];
+#pragma unroll
+    for (int i = 0; i < GW; ++i) {
+      sl[i] = -2;
+      if (i < nr && valid) sl[i] = p == t ? -1 - (r0 + i) : __ldg(arow + (size_t)(r0 + i) * S_max + p);
+    }
+    int u = 0;
+#pragma unroll
+    for (int i = 0; i < GW; ++i) {
+      int w = -1;
+#pragma unroll
+      for (int j = 0; j < i; ++j)
+        if (w < 0 && sl[j] == sl[i]) w = loc[j];
+      if (w < 0 && i < nr) {
+        w = u++;
+        if (valid) pent[p * GW + w] = (short)sl[i];
+      }
+      loc[i] = w < 0 ? 0 : w;
+      if (i < nr && valid) ploc[i * S_max + p] = (unsigned char)loc[i];
+    }
+    if (!valid) u = 0;
+    int incl = u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int nn = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += nn;
+    }
+    if (valid) {
+      pcnt[p] = (unsigned char)u;
+      pexcl[p] = (short)(incl - u);
+    }
+    if (lane == 31) bstart[blk + 1] = incl;
+  }
+  AT_STAMP(7);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bstart[0] = 0;
+    for (int b = 1; b <= nblk; ++b) bstart[b] += bstart[b - 1];
+  }
+  __syncthreads();
+  // ---- sweep 2: the entry list in position order; ekey = (position, local
+  // index) decides on-path membership later: entry e is on row i's path iff
+  // ploc[i][p(e)] == k(e)
+  for (int p = threadIdx.x; p <= t; p += blockDim.x) {
+    const int e0 = bstart[p >> 5] + pexcl[p];
+    const int u = pcnt[p];
+    for (int k = 0; k < u; ++k) {
+      esrc[e0 + k] = pent[p * GW + k];
+      epos[e0 + k] = (short)p;
+      ek[e0 + k] = (unsigned char)k;
+    }
+  }
+  __syncthreads();
+  const int E = bstart[nblk];
+  // first pass: every warp copies every HG-th entry
+  for (int e = warp; e < min(E, cap); e += HG) stage(e, esrc[e], epos[e]);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  AT_STAMP(2);
+  // this step's k/v of my heads, for slot (row, t): loaded now (overlapping
+  // the staging copies), stored after the attention (only later steps read
+  // them; this step's copies source position t from qkv)
+  constexpr int KVC = (GW * RUN / 16 + 32 * HG - 1) / (32 * HG);  // chunks per thread, G <= GW
+  uint4 kvk[KVC], kvv[KVC];
+#pragma unroll
+  for (int q = 0; q < KVC; ++q) {
+    const int c = threadIdx.x + q * 32 * HG;
+    if (c < nr * (RUN / 16)) {
+      const int i = c / (RUN / 16), u = c % (RUN / 16);
+      const __nv_bfloat16 *src = qkv + (size_t)(r0 + i) * ld_qkv + h0 * DH + u * 8;
+      kvk[q] = *reinterpret_cast<const uint4 *>(src + D);
+      kvv[q] = *reinterpret_cast<const uint4 *>(src + 2 * D);
+    }
+  }
+  AT_STAMP(6);
+  // ---- Q fragments of my head (rows gq, gq+8 of the 16-row tile)
+  const int h = h0 + warp;
+  const int gq = lane >> 2, tq = lane & 3;
+  uint32_t qa[DH / 16][4];
+  {
+    const bool va = gq < nr, vb = gq + 8 < nr;
+    const __nv_bfloat16 *qa_p = qkv + (size_t)(r0 + (va ? gq : 0)) * ld_qkv + h * DH;
+    const __nv_bfloat16 *qb_p = qkv + (size_t)(r0 + (vb ? gq + 8 : 0)) * ld_qkv + h * DH;
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      const int c0 = ks * 16 + tq * 2;
+      qa[ks][0] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0) : 0u;
+      qa[ks][1] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0) : 0u;
+      qa[ks][2] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0 + 8) : 0u;
+      qa[ks][3] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0 + 8) : 0u;
+    }
+  }
+  const bool rva = gq < nr, rvb = gq + 8 < nr;
+  const unsigned char *pla = ploc + (size_t)(rva ? gq : 0) * S_max;
+  const unsigned char *plb = ploc + (size_t)(rvb ? gq + 8 : 0) * S_max;
+  float o[DH / 8][4];
+#pragma unroll
+  for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+  constexpr int NT = 8;  // n-tiles per pass (cap <= 64)
+  for (int eb = 0; eb < E; eb += cap) {
+    const int n = min(cap, E - eb);
+    const int npad = (n + 15) & ~15;
+    if (eb > 0) {  // later passes (the first was issued above)
+      for (int e = warp; e < n; e += HG) stage(e, esrc[eb + e], epos[eb + e]);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    // zero the padding entries (finite V for masked columns)
+    for (int c = threadIdx.x; c < (npad - n) * (RUN / 16); c += blockDim.x) {
+      const int e = n + c / (RUN / 16), u = c % (RUN / 16);
+      *reinterpret_cast<uint4 *>(Ks + (size_t)e * EP + u * 16) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4 *>(Vs + (size_t)e * EP + u * 16) = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (eb == 0) AT_STAMP(4);
+    // ---- S = Q K^T over the whole pass (independent n-tiles), path mask
+    float sc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+      if (nt * 8 < npad) {
+        const __nv_bfloat16 *krow =
+            reinterpret_cast<const __nv_bfloat16 *>(Ks + (size_t)(nt * 8 + gq) * EP) + warp * DH;
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t *>(krow + ks * 16 + tq * 2);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t *>(krow + ks * 16 + tq * 2 + 8);
+          mma_bf16_16816(sc[nt], qa[ks], b0, b1);
+        }
+      }
+    }
+    float cm_a = -INFINITY, cm_b = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ej = nt * 8 + tq * 2 + e;
+        bool oka = false, okb = false;
+        if (ej < n) {
+          const int pe = epos[eb + ej], ke = ek[eb + ej];
+          oka = rva && pla[pe] == ke;
+          okb = rvb && plb[pe] == ke;
+        }
+        sc[nt][e] = oka ? sc[nt][e] * scale : -INFINITY;
+        sc[nt][2 + e] = okb ? sc[nt][2 + e] * scale : -INFINITY;
+        cm_a = fmaxf(cm_a, sc[nt][e]);
+        cm_b = fmaxf(cm_b, sc[nt][2 + e]);
+      }
+#pragma unroll
+    for (int o2 = 1; o2 < 4; o2 <<= 1) {
+      cm_a = fmaxf(cm_a, __shfl_xor_sync(0xffffffffu, cm_a, o2));
+      cm_b = fmaxf(cm_b, __shfl_xor_sync(0xffffffffu, cm_b, o2));
+    }
+    const float mn_a = fmaxf(m_a, cm_a), mn_b = fmaxf(m_b, cm_b);
+    const float cr_a = mn_a == -INFINITY ? 1.f : (m_a == -INFINITY ? 0.f : __expf(m_a - mn_a));
+    const float cr_b = mn_b == -INFINITY ? 1.f : (m_b == -INFINITY ? 0.f : __expf(m_b - mn_b));
+    float ps_a = 0.f, ps_b = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sc[nt][e] = sc[nt][e] == -INFINITY ? 0.f : __expf(sc[nt][e] - mn_a);
+        sc[nt][2 + e] = sc[nt][2 + e] == -INFINITY ? 0.f : __expf(sc[nt][2 + e] - mn_b);
+        ps_a += sc[nt][e];
+        ps_b += sc[nt][2 + e];
+      }
+#pragma unroll
+    for (int o2 = 1; o2 < 4; o2 <<= 1) {
+      ps_a += __shfl_xor_sync(0xffffffffu, ps_a, o2);
+      ps_b += __shfl_xor_sync(0xffffffffu, ps_b, o2);
+    }
+    l_a = l_a * cr_a + ps_a;
+    l_b = l_b * cr_b + ps_b;
+    m_a = mn_a;
+    m_b = mn_b;
+#pragma unroll
+    for (int nn = 0; nn < DH / 8; ++nn) {
+      o[nn][0] *= cr_a; o[nn][1] *= cr_a;
+      o[nn][2] *= cr_b; o[nn][3] *= cr_b;
+    }
+    // ---- O += P V, 16 entries per k-step
+#pragma unroll
+    for (int kk = 0; kk < NT / 2; ++kk) {
+      if (kk * 16 < npad) {
+        uint32_t pa[4];
+        pa[0] = pack_bf16(sc[2 * kk][0], sc[2 * kk][1]);
+        pa[1] = pack_bf16(sc[2 * kk][2], sc[2 * kk][3]);
+        pa[2] = pack_bf16(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+        pa[3] = pack_bf16(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+        const uint32_t vrow = vs_s + (uint32_t)((kk * 16 + (lane & 15)) * EP + warp * DH * 2);
+#pragma unroll
+        for (int nn = 0; nn < DH / 8; ++nn) {
+          uint32_t b0, b1;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                       : "=r"(b0), "=r"(b1)
+                       : "r"(vrow + nn * 16));
+          mma_bf16_16816(o[nn], pa, b0, b1);
+        }
+      }
+    }
+    __syncthreads();  // the staging area is reused by the next pass
+  }
+  AT_STAMP(5);
+#pragma unroll
+  for (int q = 0; q < KVC; ++q) {
+    const int c = threadIdx.x + q * 32 * HG;
+    if (c < nr * (RUN / 16)) {
+      const int i = c / (RUN / 16), u = c % (RUN / 16);
+      const size_t cs = (((size_t)(r0 + i) * S_max + t) * H + h0) * DH + u * 8;
+      *reinterpret_cast<uint4 *>(kc + cs) = kvk[q];
+      *reinterpret_cast<uint4 *>(vc + cs) = kvv[q];
+    }
+  }
+  // ---- normalise and store rows gq, gq+8
+  const float ia = 1.0f / l_a, ib = 1.0f / l_b;
+#pragma unroll
+  for (int nn = 0; nn < DH / 8; ++nn) {
+    const int c = h * DH + nn * 8 + tq * 2;
+    if (gq < nr)
+      *reinterpret_cast<uint32_t *>(ctx + (size_t)(r0 + gq) * ldc + c) = pack_bf16(o[nn][0] * ia, o[nn][1] * ia);
+    if (gq + 8 < nr)
+      *reinterpret_cast<uint32_t *>(ctx + (size_t)(r0 + gq + 8) * ldc + c) =
+          pack_bf16(o[nn][2] * ib, o[nn][3] * ib);
+  }
+}
+
+static size_t self_tc_smem(int dh, int hg, int gw, int G, int S_max, int cap) {
+  const size_t ep = (size_t)hg * dh * 2 + 16;
+  const int emax = G * S_max;
+  size_t b = 2 * (size_t)((cap + 15) / 16 * 16) * ep;  // K, V staging
+  b += (size_t)((S_max + 31) / 32 + 2) * 4;     // bstart
+  b += 2 * (size_t)emax * 2;                    // esrc, epos
+  b += (size_t)S_max * gw * 2;                  // pent
+  b += (size_t)emax;                            // ek
+  b += (size_t)gw * S_max;                      // ploc
+  b += (size_t)((S_max + 1) & ~1);              // pcnt
+  b += (size_t)S_max * 2 + 16;                  // pexcl
+  return (b + 127) & ~(size_t)127;
+}
+
 extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qkv, int ld_qkv,
                                      int qkv_dtype, const int *lengths, void *ctx, int ldc,
                                      int ctx_dtype, void *stream) {
@@ -1070,16 +1245,56 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
     auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
     auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
     const float sc = attn_scale(dh);
-    static int pf = -1;
-    if (pf < 0) {
-      const char *e = getenv("SKB_ATTN_PF");
-      pf = e ? atoi(e) : 0;  // measured slower in the decode graph (fewer resident warps)
+    static int tc_mode = -1, tc_cap = 0, tc_hg = 0;
+    if (tc_mode < 0) {
+      const char *e = getenv("SKB_ATTN_TC");
+      tc_mode = e ? atoi(e) : 1;
+      e = getenv("SKB_ATTN_CAP");
+      tc_cap = e ? atoi(e) : 48;
+      if (tc_cap > 64) tc_cap = 64;  // one pass = at most 8 mma n-tiles
+      if (tc_cap < 16) tc_cap = 16;
+      e = getenv("SKB_ATTN_HG");
+      tc_hg = e ? atoi(e) : 4;
     }
-    if (dh == 64 && pf)
-      launch_k(k_self_attn_pf<64, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
-               qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
-    else if (dh == 64)
-      launch_k(k_self_attn_vec<64, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
+    const int G2 = rows_per_group;
+    int hg = tc_hg;
+    while (hg > 1 && H % hg) hg >>= 1;
+    if (tc_mode && G2 >= 1 && G2 <= 16 && qkv_dtype == SKB_BF16 && ctx_dtype == SKB_BF16 &&
+        dh == 64 && ldc % 2 == 0 && ld_qkv % 8 == 0 && (hg == 2 || hg == 4 || hg == 8)) {
+      const int gw = G2 <= 8 ? 8 : 16;
+      const size_t smem = self_tc_smem(64, hg, gw, G2, S_max, tc_cap);
+      dim3 g((R + G2 - 1) / G2, H / hg);
+      auto go = [&](auto kern_fn) {
+        // per-kernel opt-in shared memory size (all instantiations share the
+        // function-pointer type, so key by address)
+        static std::mutex mu;
+        static std::unordered_map<const void *, size_t> set;
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          size_t &cur = set[reinterpret_cast<const void *>(kern_fn)];
+          if (smem > cur) {
+            cudaFuncSetAttribute(kern_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cur = smem;
+          }
+        }
+        launch_k(kern_fn, g, 32 * hg, smem, as_stream(stream), R, H, G2,
+                 reinterpret_cast<const __nv_bfloat16 *>(qkv), ld_qkv, k, v, S_max, anc, step, sc,
+                 reinterpret_cast<__nv_bfloat16 *>(ctx), ldc, tc_cap);
+      };
+      if (gw == 16) {
+        if (hg == 8) go(k_self_attn_tc<64, 8, 16>);
+        else if (hg == 2) go(k_self_attn_tc<64, 2, 16>);
+        else go(k_self_attn_tc<64, 4, 16>);
+      } else {
+        if (hg == 8) go(k_self_attn_tc<64, 8, 8>);
+        else if (hg == 2) go(k_self_attn_tc<64, 2, 8>);
+        else go(k_self_attn_tc<64, 4, 8>);
+      }
+      SKB_CHECK_LAUNCH("k_self_attn_tc");
+      return SKB_OK;
+    }
+    if (dh == 64)
+      launch_k(k_self_attn_vec<64, 8>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
                qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);
     else if (dh == 32)
       launch_k(k_self_attn_vec<32, 16>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
@@ -1096,6 +1311,18 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
       ldc, ctx_dtype);
   SKB_CHECK_LAUNCH("k_self_attention_step");
   return SKB_OK;
+}
+
+extern "C" int skb_debug_attn_trace(unsigned long long *host) {
+#ifdef SKB_ATTN_TRACE
+  cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(g_attn_trace));
+  static unsigned long long zeros[4096 * 8];
+  cudaMemcpyToSymbol(g_attn_trace, zeros, sizeof(zeros));
+  return SKB_OK;
+#else
+  (void)host;
+  return SKB_ERR_UNSUPPORTED;
+#endif
 }
 
 extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int ldq, int q_dtype,

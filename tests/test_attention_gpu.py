@@ -24,8 +24,8 @@ def _ref_self(qkv, kc, vc, anc_cur, t, H, dh):
         ks, vs = [], []
         for p in range(t):
             s = int(anc_cur[r, p])
-            ks.append(kc[s, :, p].float())
-            vs.append(vc[s, :, p].float())
+            ks.append(kc[s, p].float())
+            vs.append(vc[s, p].float())
         ks.append(knew[r])
         vs.append(vnew[r])
         K = torch.stack(ks, 1)  # H, t+1, dh
@@ -35,18 +35,31 @@ def _ref_self(qkv, kc, vc, anc_cur, t, H, dh):
     return out.view(R, D)
 
 
-@pytest.mark.parametrize("G,t,dh", [(5, 0, 64), (5, 7, 64), (5, 45, 64), (4, 70, 32), (3, 33, 128),
-                                    (1, 40, 64)])
-def test_self_attention_grouped_matches_reference(G, t, dh):
-    g = torch.Generator(device="cuda").manual_seed(t * 10 + G)
-    B, H, S = 6, 4, 80
+@pytest.mark.parametrize("G,t,dh,H", [(5, 0, 64, 4), (5, 7, 64, 4), (5, 45, 64, 4), (4, 70, 32, 4),
+                                      (3, 33, 128, 4), (1, 40, 64, 4), (8, 79, 64, 8),
+                                      (16, 63, 64, 4), (5, 60, 64, 16), (2, 79, 64, 6)])
+@pytest.mark.parametrize("tree", [False, True])
+def test_self_attention_grouped_matches_reference(G, t, dh, H, tree):
+    """Cache layout [slot][pos][head][dh]; the beam rows of a group reference
+    ancestor slots of their own group.  `tree` draws them from a beam tree
+    (mostly shared history, the tensor-core kernel's common case); otherwise
+    uniformly (mostly distinct entries: several staging passes)."""
+    g = torch.Generator(device="cuda").manual_seed(t * 10 + G + H)
+    B, S = 6, 80
     R, D = B * G, H * dh
     qkv = torch.randn(R, 3 * D, device="cuda", generator=g).bfloat16()
-    kc = torch.randn(R, H, S, dh, device="cuda", generator=g).bfloat16()
-    vc = torch.randn(R, H, S, dh, device="cuda", generator=g).bfloat16()
+    kc = torch.randn(R, S, H, dh, device="cuda", generator=g).bfloat16()
+    vc = torch.randn(R, S, H, dh, device="cuda", generator=g).bfloat16()
     anc = torch.zeros(2, R, S, dtype=torch.int32, device="cuda")
     grp = torch.arange(R, device="cuda") // G
-    anc[t & 1] = (grp[:, None] * G + torch.randint(0, G, (R, S), device="cuda", generator=g)).int()
+    if tree:
+        hist = torch.arange(R, device="cuda")[:, None].repeat(1, S)
+        for p in range(1, S):
+            par = grp * G + torch.randint(0, max(1, G // 2), (R,), device="cuda", generator=g)
+            hist[:, :p] = hist[par, :p]
+        anc[t & 1] = hist.int()
+    else:
+        anc[t & 1] = (grp[:, None] * G + torch.randint(0, G, (R, S), device="cuda", generator=g)).int()
     step = torch.tensor([t], dtype=torch.int32, device="cuda")
     ref = _ref_self(qkv, kc, vc, anc[t & 1], t, H, dh)
     ctx = torch.zeros(R, D, device="cuda", dtype=torch.bfloat16)
@@ -54,8 +67,8 @@ def test_self_attention_grouped_matches_reference(G, t, dh):
     torch.cuda.synchronize()
     assert (ctx.float() - ref).abs().max().item() < 2e-2
     # the fresh k/v landed in slot (r, t)
-    assert torch.equal(kc[:, :, t].reshape(R, D), qkv[:, D:2 * D])
-    assert torch.equal(vc[:, :, t].reshape(R, D), qkv[:, 2 * D:])
+    assert torch.equal(kc[:, t].reshape(R, D), qkv[:, D:2 * D])
+    assert torch.equal(vc[:, t].reshape(R, D), qkv[:, 2 * D:])
 
 
 @pytest.mark.parametrize("G,L", [(5, 30), (1, 17), (4, 90)])
