@@ -128,11 +128,11 @@ def build_model(precision="bf16"):
     return model, vocabs
 
 
-def make_batch(model, vocabs, sentences, beam, alpha):
+def make_batch(model, vocabs, sentences, beam, alpha, slot=0):
     from paper_2207_05851_b200.engine import BeamBatch
     from paper_2207_05851_b200.search import SentenceInput, _chunk_job
     jobs = [_chunk_job(model, SentenceInput(tokens=s), vocabs, None)[0] for s in sentences]
-    return BeamBatch(model, jobs, beam, alpha)
+    return BeamBatch(model, jobs, beam, alpha, slot=slot)
 
 
 def gemm_roofline(model, R, L, peak):
@@ -273,13 +273,14 @@ def run_ours(args):
             dist.gather(toks, out, dst=0)
 
     # ---- warm-up (also compiles TMA descriptors, captures graphs)
-    for w in range(args.warmup):
-        bb = make_batch(model, vocabs, sents(1000 + w), K, args.alpha)
+    for w in range(max(args.warmup, 2)):  # both workspace slots get their graphs
+        bb = make_batch(model, vocabs, sents(1000 + w), K, args.alpha, slot=w & 1)
         bb.run()
         gather(bb)
     torch.cuda.synchronize()
     # ---- value: inputs staged in HBM before the timed region
-    batches = [make_batch(model, vocabs, sents(s), K, args.alpha) for s in range(args.steps)]
+    batches = [make_batch(model, vocabs, sents(s), K, args.alpha, slot=s & 1)
+               for s in range(args.steps)]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -288,9 +289,15 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     results = []
+    prev = None  # batch i+1 is launched before batch i is read back (two workspaces)
     for bb in batches:
-        results.append(bb.run())
-        gather(bb)
+        bb.start()
+        if prev is not None:
+            results.append(prev.finish())
+            gather(prev)
+        prev = bb
+    results.append(prev.finish())
+    gather(prev)
     e1.record()
     torch.cuda.synchronize()
     if world > 1:

@@ -784,6 +784,159 @@ __global__ void __launch_bounds__(128) k_attn_mma(
 }
 
 // Dispatch helper for the grouped attention (cross and encoder).
+// ---------------------- cross-attention on tensor cores, head-grouped
+// model.py:568-573: the G beam rows of a sentence attend over its encoder
+// memory.  A CTA owns (sentence, HG heads), one warp per head: the K and V
+// rows of the HG heads are one contiguous run per source position in the
+// all-layers cross K/V matrix, staged once with cp.async into padded shared
+// rows; each warp then runs a 16-row (G used) mma.sync attention over
+// 32-key chunks with the source-length mask and online softmax.
+template <int DH, int HG>
+__global__ void __launch_bounds__(32 * HG) k_cross_tc(
+    int R, int G, int H, const __nv_bfloat16 *__restrict__ q, int ldq,
+    const __nv_bfloat16 *__restrict__ kv, int ld_kv, int koff, int voff, int L,
+    const int *__restrict__ row_sent, const int *__restrict__ lengths, float scale,
+    __nv_bfloat16 *__restrict__ ctx, int ldc) {
+  constexpr int RUN = HG * DH * 2;  // bytes per source position and head group
+  constexpr int EP = RUN + 16;      // padded shared row pitch
+  constexpr int CH = RUN / 16;      // 16-byte chunks per row
+  extern __shared__ __align__(128) uint8_t sm_x[];
+  PDL_ENTRY();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * G, nr = min(G, R - r0);
+  const int h0 = blockIdx.y * HG;
+  const int b = row_sent ? row_sent[r0] : blockIdx.x;
+  const int len = lengths[b];
+  const int Lp = (L + 31) & ~31;
+  uint8_t *Ks = sm_x;
+  uint8_t *Vs = sm_x + (size_t)Lp * EP;
+  const uint32_t ks_s = static_cast<uint32_t>(__cvta_generic_to_shared(Ks));
+  const uint32_t vs_s = static_cast<uint32_t>(__cvta_generic_to_shared(Vs));
+  for (int idx = threadIdx.x; idx < Lp * CH; idx += blockDim.x) {
+    const int j = idx / CH, c = idx - j * CH;
+    if (j < len) {
+      const __nv_bfloat16 *src = kv + (size_t)(b * L + j) * ld_kv + h0 * DH + c * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ks_s + (uint32_t)(j * EP + c * 16)),
+                   "l"(src + koff)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(vs_s + (uint32_t)(j * EP + c * 16)),
+                   "l"(src + voff)
+                   : "memory");
+    } else {  // zero keys (masked below; V must be finite)
+      *reinterpret_cast<uint4 *>(Ks + (size_t)j * EP + c * 16) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4 *>(Vs + (size_t)j * EP + c * 16) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  // Q fragments of my head while the copies fly
+  const int h = h0 + warp;
+  const int gq = lane >> 2, tq = lane & 3;
+  const bool va = gq < nr, vb = gq + 8 < nr;
+  uint32_t qa[DH / 16][4];
+  {
+    const __nv_bfloat16 *qa_p = q + (size_t)(r0 + (va ? gq : 0)) * ldq + h * DH;
+    const __nv_bfloat16 *qb_p = q + (size_t)(r0 + (vb ? gq + 8 : 0)) * ldq + h * DH;
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      const int c0 = ks * 16 + tq * 2;
+      qa[ks][0] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0) : 0u;
+      qa[ks][1] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0) : 0u;
+      qa[ks][2] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0 + 8) : 0u;
+      qa[ks][3] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0 + 8) : 0u;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  float o[DH / 8][4];
+#pragma unroll
+  for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+  for (int j0 = 0; j0 < len; j0 += 32) {
+    float sc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+      const __nv_bfloat16 *krow =
+          reinterpret_cast<const __nv_bfloat16 *>(Ks + (size_t)(j0 + nt * 8 + gq) * EP) + warp * DH;
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t *>(krow + ks * 16 + tq * 2);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t *>(krow + ks * 16 + tq * 2 + 8);
+        mma_bf16_16816(sc[nt], qa[ks], b0, b1);
+      }
+    }
+    float cm_a = -INFINITY, cm_b = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool ok = j0 + nt * 8 + tq * 2 + e < len;
+        sc[nt][e] = ok ? sc[nt][e] * scale : -INFINITY;
+        sc[nt][2 + e] = ok ? sc[nt][2 + e] * scale : -INFINITY;
+        cm_a = fmaxf(cm_a, sc[nt][e]);
+        cm_b = fmaxf(cm_b, sc[nt][2 + e]);
+      }
+#pragma unroll
+    for (int o2 = 1; o2 < 4; o2 <<= 1) {
+      cm_a = fmaxf(cm_a, __shfl_xor_sync(0xffffffffu, cm_a, o2));
+      cm_b = fmaxf(cm_b, __shfl_xor_sync(0xffffffffu, cm_b, o2));
+    }
+    const float mn_a = fmaxf(m_a, cm_a), mn_b = fmaxf(m_b, cm_b);
+    const float cr_a = m_a == -INFINITY ? 0.f : __expf(m_a - mn_a);
+    const float cr_b = m_b == -INFINITY ? 0.f : __expf(m_b - mn_b);
+    float ps_a = 0.f, ps_b = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sc[nt][e] = sc[nt][e] == -INFINITY ? 0.f : __expf(sc[nt][e] - mn_a);
+        sc[nt][2 + e] = sc[nt][2 + e] == -INFINITY ? 0.f : __expf(sc[nt][2 + e] - mn_b);
+        ps_a += sc[nt][e];
+        ps_b += sc[nt][2 + e];
+      }
+#pragma unroll
+    for (int o2 = 1; o2 < 4; o2 <<= 1) {
+      ps_a += __shfl_xor_sync(0xffffffffu, ps_a, o2);
+      ps_b += __shfl_xor_sync(0xffffffffu, ps_b, o2);
+    }
+    l_a = l_a * cr_a + ps_a;
+    l_b = l_b * cr_b + ps_b;
+    m_a = mn_a;
+    m_b = mn_b;
+#pragma unroll
+    for (int nn = 0; nn < DH / 8; ++nn) {
+      o[nn][0] *= cr_a; o[nn][1] *= cr_a;
+      o[nn][2] *= cr_b; o[nn][3] *= cr_b;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t pa[4];
+      pa[0] = pack_bf16(sc[2 * kk][0], sc[2 * kk][1]);
+      pa[1] = pack_bf16(sc[2 * kk][2], sc[2 * kk][3]);
+      pa[2] = pack_bf16(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+      pa[3] = pack_bf16(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+      const uint32_t vrow = vs_s + (uint32_t)((j0 + kk * 16 + (lane & 15)) * EP + warp * DH * 2);
+#pragma unroll
+      for (int nn = 0; nn < DH / 8; ++nn) {
+        uint32_t b0, b1;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                     : "=r"(b0), "=r"(b1)
+                     : "r"(vrow + nn * 16));
+        mma_bf16_16816(o[nn], pa, b0, b1);
+      }
+    }
+  }
+  const float ia = 1.0f / l_a, ib = 1.0f / l_b;
+#pragma unroll
+  for (int nn = 0; nn < DH / 8; ++nn) {
+    const int c = h * DH + nn * 8 + tq * 2;
+    if (va) *reinterpret_cast<uint32_t *>(ctx + (size_t)(r0 + gq) * ldc + c) = pack_bf16(o[nn][0] * ia, o[nn][1] * ia);
+    if (vb)
+      *reinterpret_cast<uint32_t *>(ctx + (size_t)(r0 + gq + 8) * ldc + c) =
+          pack_bf16(o[nn][2] * ib, o[nn][3] * ib);
+  }
+}
+
 static bool attn_vec_ok(int dh, int q_dtype, int kv_dtype, const void *q, int ldq, const void *kv,
                         int ld_kv, int koff, int voff, int qoff) {
   return (dh == 32 || dh == 64 || dh == 128) && q_dtype == SKB_BF16 && kv_dtype == SKB_BF16 &&
@@ -1334,6 +1487,31 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
   if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "cross_attention_step: head dim %d", dh);
   if (R == 0) return SKB_OK;
   const int G = rows_per_group > 0 ? rows_per_group : 1;
+  static int xtc = -1;
+  if (xtc < 0) {
+    const char *e = getenv("SKB_CROSS_TC");
+    xtc = e ? atoi(e) : 1;
+  }
+  if (xtc && dh == 64 && G <= 16 && H % 4 == 0 && q_dtype == SKB_BF16 && kv_dtype == SKB_BF16 &&
+      ctx_dtype == SKB_BF16 && ldq % 8 == 0 && ld_kv % 8 == 0 && koff % 8 == 0 && voff % 8 == 0 &&
+      ldc % 2 == 0 && (reinterpret_cast<uintptr_t>(kv) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(q) & 3) == 0) {
+    const size_t smem = (size_t)2 * ((L + 31) & ~31) * (4 * 64 * 2 + 16);
+    if (smem <= 200 * 1024) {
+      static size_t set = 0;
+      if (smem > set) {
+        cudaFuncSetAttribute(k_cross_tc<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        set = smem;
+      }
+      dim3 g((R + G - 1) / G, H / 4);
+      launch_k(k_cross_tc<64, 4>, g, 128, smem, as_stream(stream), R, G, H,
+               reinterpret_cast<const __nv_bfloat16 *>(q), ldq,
+               reinterpret_cast<const __nv_bfloat16 *>(kv), ld_kv, koff, voff, L, row_sent, lengths,
+               attn_scale(dh), reinterpret_cast<__nv_bfloat16 *>(ctx), ldc);
+      SKB_CHECK_LAUNCH("k_cross_tc");
+      return SKB_OK;
+    }
+  }
   if (attn_vec_ok(dh, q_dtype, kv_dtype, q, ldq, kv, ld_kv, koff, voff, 0) &&
       launch_attn_vec(R, G, H, dh, q, ldq, 0, kv, ld_kv, koff, voff, L, row_sent, lengths,
                       attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream)) == 0) {

@@ -259,6 +259,8 @@ class DecodeWorkspace:
         self.factors_out = z(B * nf1 * S_max).view(B, nf1, S_max)
         self.out_host = torch.zeros(B * S_max + B * nf1 * S_max + 2 * B, dtype=I32,
                                     pin_memory=True)
+        self.lp_host = torch.zeros(B, dtype=torch.float64, pin_memory=True)
+        self.out_ready = None
         self.eos_col = None
         self.state = None
         self.graph_enc = self.graph_1 = self.graph_n = None
@@ -361,8 +363,11 @@ class DecodeWorkspace:
                 ev.record()
         return steps
 
-    def collect(self) -> tuple:
-        """Backtrack the best hypotheses; one D2H copy of everything."""
+    def enqueue_collect(self) -> None:
+        """Backtrack the best hypotheses and start one asynchronous D2H copy
+        of everything into pinned memory (stream-ordered right after this
+        batch's decode, so a following batch can be launched before the
+        results are read)."""
         B, S, nf1 = self.B, self.S_max, max(self.nf, 1)
         kern.beam_finalize(self.state, self.tokens_out, self.factors_out)
         h = self.out_host
@@ -371,7 +376,19 @@ class DecodeWorkspace:
         h[B * S + B * nf1 * S:B * S + B * nf1 * S + B].copy_(self.st["best_steps"],
                                                               non_blocking=True)
         h[B * S + B * nf1 * S + B:].copy_(self.st["best_forced"], non_blocking=True)
-        lp = self.st["best_logprob"].to("cpu", non_blocking=False)
+        self.lp_host.copy_(self.st["best_logprob"], non_blocking=True)
+        self.out_ready = torch.cuda.Event()
+        self.out_ready.record()
+
+    def collect(self) -> tuple:
+        """Wait for the D2H copy of enqueue_collect() and unpack it."""
+        if getattr(self, "out_ready", None) is None:
+            self.enqueue_collect()
+        self.out_ready.synchronize()
+        self.out_ready = None
+        B, S, nf1 = self.B, self.S_max, max(self.nf, 1)
+        h = self.out_host
+        lp = self.lp_host.clone()
         arr = h.numpy()
         toks = arr[:B * S].reshape(B, S)
         facs = arr[B * S:B * S + B * nf1 * S].reshape(B, nf1, S)
@@ -381,7 +398,7 @@ class DecodeWorkspace:
 
 
 _WS_CACHE: dict = {}
-_WS_MAX = 4
+_WS_MAX = 6
 
 
 def _workspace(model, key, *args):
@@ -402,7 +419,7 @@ class BeamBatch:
     finalize, one D2H copy of the results."""
 
     def __init__(self, model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
-                 nvs_threshold: float | None = None, use_graph: bool = True):
+                 nvs_threshold: float | None = None, use_graph: bool = True, slot: int = 0):
         if beam < 1:
             raise ConfigError(f"beam size must be at least 1, got {beam}")
         if beam > 32:
@@ -410,6 +427,7 @@ class BeamBatch:
         self.model, self.jobs, self.K, self.alpha = model, jobs, beam, alpha
         self.use_graph = use_graph
         self.nvs_threshold = nvs_threshold
+        self.slot = slot  # workspace slot: consecutive batches alternate (pipelining)
         c = model.config
         nf, nsf = len(c.target_factor_specs), len(c.source_factor_specs)
         self.nf = nf
@@ -438,7 +456,7 @@ class BeamBatch:
             U = int(U_ids.size)
         else:
             U = V
-        key = (B, L, self.S_max, K, P, U, self.alpha, restricted)
+        key = (B, L, self.S_max, K, P, U, self.alpha, restricted, self.slot)
         ws = _workspace(model, key, B, L, self.S_max, K, P, U, self.alpha, restricted)
         self.ws = ws
         # this batch's inputs: own pinned staging + own device copy (several
@@ -517,7 +535,9 @@ class BeamBatch:
     def tokens_out(self):
         return self.ws.tokens_out
 
-    def run(self) -> list[ChunkResult]:
+    def start(self) -> None:
+        """Launch encoder + decode + finalize + the D2H copy; returns without
+        waiting (the host can prepare and launch the next batch)."""
         if self.ws is None:  # NVS: the active sets come from the encoder output
             m, c = self.model, self.model.config
             nsf = len(c.source_factor_specs)
@@ -543,7 +563,15 @@ class BeamBatch:
         ws.in_dev.copy_(self.in_dev, non_blocking=True)   # device-resident inputs
         ws.reset()
         self.steps_run = ws.run(self.use_graph)
+        ws.enqueue_collect()
+
+    def finish(self) -> list[ChunkResult]:
+        """Wait for this batch's results (launched by start())."""
         return self.collect()
+
+    def run(self) -> list[ChunkResult]:
+        self.start()
+        return self.finish()
 
     def collect(self) -> list[ChunkResult]:
         toks, facs, steps, forced, lp = self.ws.collect()
@@ -570,11 +598,20 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
     order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i].src_ids))
     per_batch = max(1, max_rows // beam)
     results: list[ChunkResult | None] = [None] * len(jobs)
-    for s in range(0, len(order), per_batch):
+    # two batches in flight: batch n+1 is prepared and launched before the
+    # results of batch n are read back (alternating workspaces)
+    pending = None
+    for n, s in enumerate(range(0, len(order), per_batch)):
         idx = order[s:s + per_batch]
-        bb = BeamBatch(model, [jobs[i] for i in idx], beam, alpha, nvs_threshold, use_graph)
-        for i, r in zip(idx, bb.run()):
-            results[i] = r
+        bb = BeamBatch(model, [jobs[i] for i in idx], beam, alpha, nvs_threshold, use_graph,
+                       slot=n & 1)
+        bb.start()
+        if pending is not None:
+            for i, r in zip(pending[0], pending[1].finish()):
+                results[i] = r
+        pending = (idx, bb)
+    for i, r in zip(pending[0], pending[1].finish()):
+        results[i] = r
     return results
 
 
