@@ -81,6 +81,18 @@ typedef struct skb_epilogue {
   long long splitk_ws_elems;
   unsigned *splitk_counters;
   int splitk_counters_n;
+  /* SKB_EPI_RESID only, optional fused LayerNorm of the updated rows        */
+  /* (kernels.py:298-324; replaces the skb_layernorm launch that follows a   */
+  /* residual GEMM, model.py:562-575): ln_out[m] = LN(x[m]) * gain + bias,   */
+  /* bf16 [M, ln_ldo].  ln_counter: caller-owned, zero-initialised uint32    */
+  /* [>= ceil(M / 16)] per call site, never reset (arrival tickets of the    */
+  /* CTAs that finish an activation-row tile).  NULL ln_out disables it.     */
+  const float *ln_gain;
+  const float *ln_bias;
+  float ln_eps;
+  void *ln_out;
+  int ln_ldo;
+  unsigned *ln_counter;
 } skb_epilogue;
 
 /* Library identity / diagnostics */

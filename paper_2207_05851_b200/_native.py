@@ -28,7 +28,8 @@ class Epilogue(C.Structure):
                 ("step", vp), ("state_stride", C.c_longlong), ("lse_part", vp),
                 ("lse_ld", i32), ("mask", vp), ("mask_words", i32), ("rows_per_group", i32),
                 ("splitk_ws", vp), ("splitk_ws_elems", C.c_longlong), ("splitk_counters", vp),
-                ("splitk_counters_n", i32)]
+                ("splitk_counters_n", i32), ("ln_gain", vp), ("ln_bias", vp),
+                ("ln_eps", C.c_float), ("ln_out", vp), ("ln_ldo", i32), ("ln_counter", vp)]
 
 
 class BeamState(C.Structure):

@@ -42,6 +42,13 @@ struct EpiArgs {
   int splits;
   float *ws;
   unsigned *counters;
+  // fused LayerNorm of the residual rows (RESID, swap-AB kernel)
+  const float *ln_gain;
+  const float *ln_bias;
+  float ln_eps;
+  __nv_bfloat16 *ln_out;
+  int ln_ldo;
+  unsigned *ln_counter;
 };
 
 // Partial log-softmax statistics of `cnt` consecutive logits of row m
@@ -893,7 +900,7 @@ __device__ __forceinline__ void stage16(uint32_t base, bool bf16, int mloc, int 
 // in shared memory and before the store is issued.
 template <int KIND, typename F>
 __device__ __forceinline__ void flush_tile(const CUtensorMap *tmO, uint32_t base, int c0, int c1,
-                                           bool leader, F before_store) {
+                                           bool leader, F before_store, bool full_wait = false) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("bar.sync 1, 128;" ::: "memory");
   before_store();
@@ -910,8 +917,52 @@ __device__ __forceinline__ void flush_tile(const CUtensorMap *tmO, uint32_t base
                    "r"(c0), "r"(c1), "r"(base)
                    : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (full_wait)  // the writes themselves are complete (another CTA reads them)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    else
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
+}
+
+// One LayerNorm row (kernels.py:298-324), warp per row: the same arithmetic
+// and order as k_layernorm_reg<NV> (elementwise.cu), NV = d / 128 <= 8.
+// x is read from L2 (written by other CTAs' bulk reduce of this kernel).
+__device__ __forceinline__ void ln_row(const EpiArgs &e, int m, int d, int lane) {
+  const int nv = d >> 7;
+  const float4 *xr = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(e.out) +
+                                                      (size_t)m * e.ldo);
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = i < nv ? __ldcg(xr + lane + 32 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float mu = warp_sum(s) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) {
+      const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, f = v[i].w - mu;
+      q += (a * a + b * b) + (c * c + f * f);
+    }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / (float)d + e.ln_eps);
+  const float4 *g4 = reinterpret_cast<const float4 *>(e.ln_gain);
+  const float4 *b4 = reinterpret_cast<const float4 *>(e.ln_bias);
+  uint2 *o = reinterpret_cast<uint2 *>(e.ln_out + (size_t)m * e.ln_ldo);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) {
+      const int c4 = lane + 32 * i;
+      const float4 g = __ldg(g4 + c4), bb = __ldg(b4 + c4);
+      const float o0 = ((v[i].x - mu) * inv) * g.x + bb.x, o1 = ((v[i].y - mu) * inv) * g.y + bb.y;
+      const float o2 = ((v[i].z - mu) * inv) * g.z + bb.z, o3 = ((v[i].w - mu) * inv) * g.w + bb.w;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t *>(&p0);
+      w.y = *reinterpret_cast<uint32_t *>(&p1);
+      o[c4] = w;
+    }
 }
 
 // LOGITS epilogue (model.py:577-581, kernels.py:287-295): partial
@@ -1145,7 +1196,7 @@ __global__ void __launch_bounds__(192, 1)
           if (KIND == SKB_EPI_LOGITS && dbg != 3)
             logits_stats(ep, stg, M, N, m0, n0, Na, warp - 2, lane);
           if (warp == 3 && lane == 0) SW_STAMP(12);
-        });
+        }, KIND == SKB_EPI_RESID && ep.ln_out != nullptr);
       }
     } else {
       // park the fp32 partial in my shared memory: part[m][128] (row-major
@@ -1223,10 +1274,40 @@ __global__ void __launch_bounds__(192, 1)
       }
       if (warp == 2 && lane == 0) SW_STAMP(10);
       if (KIND != SKB_EPI_SSRU && tma_out)
-        flush_tile<KIND>(&tmO, stg, n0, m0 + c0, warp == 2 && lane == 0, [] {});
+        flush_tile<KIND>(&tmO, stg, n0, m0 + c0, warp == 2 && lane == 0, [] {},
+                         KIND == SKB_EPI_RESID && ep.ln_out != nullptr);
     }
     if (warp == 2 && lane == 0) SW_STAMP(4);
     cluster_sync_all();  // peers are done reading my shared memory
+  }
+  // ---- fused LayerNorm of this activation-row tile (RESID): the CTAs that
+  // write the tile's columns (n_wt x CS of them, all resident: the next
+  // kernel is launched only after every CTA of this grid has started) take
+  // an arrival ticket; once the whole tile is written each of their epilogue
+  // warps normalises a share of its rows.  Same arithmetic as the LN kernel.
+  if (KIND == SKB_EPI_RESID && ep.ln_out != nullptr && warp >= 2) {
+    __shared__ int ln_go;
+    if (warp == 2 && lane == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      const unsigned G = (unsigned)(((N + 127) / 128) * CS);
+      unsigned *ctr = ep.ln_counter + at;
+      const unsigned tk = atomicAdd(ctr, 1u);
+      const unsigned target = tk - tk % G + G;
+      unsigned cur;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+        if ((int)(cur - target) >= 0) break;
+        __nanosleep(40);
+      }
+      __threadfence();
+      ln_go = 1;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    (void)ln_go;
+    const int G4 = ((N + 127) / 128) * CS * 4;
+    for (int rl = (wt * CS + rank) * 4 + (warp - 2); rl < Na && m0 + rl < M; rl += G4)
+      ln_row(ep, m0 + rl, N, lane);
   }
   __syncthreads();
 #ifdef SKB_GEMM_TRACE
@@ -1521,6 +1602,13 @@ static EpiArgs to_args(const skb_epilogue *e) {
   a.splits = 1;
   a.ws = e->splitk_ws;
   a.counters = e->splitk_counters;
+  a.ln_gain = e->ln_gain;
+  a.ln_bias = e->ln_bias;
+  a.ln_eps = e->ln_eps;
+  a.ln_out = reinterpret_cast<__nv_bfloat16 *>(e->ln_out);
+  a.ln_ldo = e->ln_ldo;
+  a.ln_counter = e->ln_counter;
+  if (e->kind != SKB_EPI_RESID) a.ln_out = nullptr;
   return a;
 }
 
@@ -1554,6 +1642,13 @@ static int gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, 
 }  // namespace skb
 
 using namespace skb;
+
+// A residual GEMM with a requested LayerNorm that did not run on the
+// swap-AB kernel (which fuses it) is followed by the LN kernel.
+static int ln_after(int M, int N, const skb_epilogue *epi, void *stream) {
+  return skb_layernorm(M, N, reinterpret_cast<const float *>(epi->out), epi->ldo, epi->ln_gain,
+                       epi->ln_bias, epi->ln_eps, epi->ln_out, epi->ln_ldo, SKB_BF16, stream);
+}
 
 extern "C" int skb_tc_available(void) {
   int dev = 0, major = 0, minor = 0;
@@ -1596,11 +1691,26 @@ extern "C" int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, i
   int rc = check_args(in_dtype, M, N, K, A, W, epi);
   if (rc) return rc;
   if (M == 0) return SKB_OK;
-  return gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, to_args(epi), as_stream(stream));
+  rc = gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, to_args(epi), as_stream(stream));
+  if (rc) return rc;
+  if (epi->kind == SKB_EPI_RESID && epi->ln_out) return ln_after(M, N, epi, stream);
+  return SKB_OK;
 }
+
+static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
+                     int ldw, const skb_epilogue *epi, void *stream, bool &fused_ln);
 
 extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
                         int ldw, const skb_epilogue *epi, void *stream) {
+  bool fused = false;
+  const int rc = gemm_impl(in_dtype, M, N, K, A, lda, W, ldw, epi, stream, fused);
+  if (rc || M == 0) return rc;
+  if (epi->kind == SKB_EPI_RESID && epi->ln_out && !fused) return ln_after(M, N, epi, stream);
+  return SKB_OK;
+}
+
+static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
+                     int ldw, const skb_epilogue *epi, void *stream, bool &fused_ln) {
   int rc = check_args(in_dtype, M, N, K, A, W, epi);
   if (rc) return rc;
   if (M == 0) return SKB_OK;
@@ -1614,9 +1724,14 @@ extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int ld
   sw::init_mode();
   const bool logits_tma = epi->kind != SKB_EPI_LOGITS ||
                           ((reinterpret_cast<uintptr_t>(epi->out) & 15) == 0 && epi->ldo % 4 == 0);
+  const bool ln_fused = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr;
+  if (ln_fused && (!epi->ln_gain || !epi->ln_bias || !epi->ln_counter || N % 128 || N > 1024 ||
+                   epi->ln_ldo % 4))
+    return fail(SKB_ERR_CONFIG, "gemm: fused LayerNorm needs gain/bias/counter, N %% 128 == 0 <= 1024");
   if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || M <= 1024)) {
     const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);
+    fused_ln = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr;
     return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs);
   }
   // Tile width BN and split-K factor S from a bytes-per-SM cost model: every

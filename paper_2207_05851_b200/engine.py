@@ -74,6 +74,10 @@ class StepBuffers:
             self.kc = torch.zeros(D, cap, S_max, d, device=dev, dtype=cdt)
             self.vc = torch.zeros(D, cap, S_max, d, device=dev, dtype=cdt)
         self.anc = torch.zeros(2, R, S_max, dtype=I32, device=dev)
+        # LayerNorm fused into the residual GEMMs (bf16 path): arrival tickets
+        # per (call site, 16-row tile); monotonic, never reset
+        self.fuse_ln = cdt == torch.bfloat16 and d % 128 == 0 and d <= 1024 and D > 0
+        self.ln_ctr = torch.zeros(3 * max(D, 1), (R + 15) // 16 + 1, dtype=I32, device=dev)
 
 
 def step_forward(model: Model, sb: StepBuffers) -> None:
@@ -84,25 +88,38 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
     nf = len(c.target_factor_specs)
     kern.embed_target(sb.tok, model.E_trg, model.pe_trg, sb.step, sb.ftok if nf else None,
                       model.trg_ftab_ptrs if nf else None, sb.x)
+    fuse = sb.fuse_ln
+    D = len(model.dec)
+
+    def resid(A, W, bias, site, ln):
+        """x += A.W^T (+bias); then h = LN(x) (fused into the GEMM when possible)."""
+        if fuse:
+            kern.gemm(A, W, sb.x, N.EPI_RESID, bias, ln=ln, ln_out=sb.h, ln_counter=sb.ln_ctr[site])
+        else:
+            kern.gemm(A, W, sb.x, N.EPI_RESID, bias)
+            kern.layernorm(sb.x, *ln, sb.h)
+
     for li, Ly in enumerate(model.dec):
-        kern.layernorm(sb.x, *Ly.ln_self, sb.h)
+        nxt = model.dec[li + 1].ln_self if li + 1 < D else model.ln_final
+        if li == 0:
+            kern.layernorm(sb.x, *Ly.ln_self, sb.h)
         if c.decoder_kind == SSRU:
             kern.gemm(sb.h, Ly.w_ssru, sb.x, N.EPI_SSRU, Ly.b_ssru, c_state=sb.cell[li],
                       src_row=sb.parent, step=sb.step, state_stride=R * d)
+            kern.layernorm(sb.x, *Ly.ln_cross, sb.h)
         else:
             kern.gemm(sb.h, Ly.wqkv, sb.qkv)
             kern.self_attention_step(sb.qkv, sb.kc[li], sb.vc[li], sb.anc, sb.step, sb.ctx,
                                      R, H, dh, sb.S_max, sb.group)
-            kern.gemm(sb.ctx, Ly.wo, sb.x, N.EPI_RESID)
-        kern.layernorm(sb.x, *Ly.ln_cross, sb.h)
+            resid(sb.ctx, Ly.wo, None, 3 * li, Ly.ln_cross)
         kern.gemm(sb.h, Ly.wq_c, sb.q)
         kern.cross_attention_step(sb.q, sb.ckv, li * 2 * d, li * 2 * d + d, sb.L, sb.row_sent,
                                   sb.lengths, sb.ctx, R, H, dh, sb.group)
-        kern.gemm(sb.ctx, Ly.wo_c, sb.x, N.EPI_RESID)
-        kern.layernorm(sb.x, *Ly.ln_ffn, sb.h)
+        resid(sb.ctx, Ly.wo_c, None, 3 * li + 1, Ly.ln_ffn)
         kern.gemm(sb.h, Ly.w1, sb.f, N.EPI_RELU, Ly.b1)
-        kern.gemm(sb.f, Ly.w2, sb.x, N.EPI_RESID, Ly.b2)
-    kern.layernorm(sb.x, *model.ln_final, sb.h)
+        resid(sb.f, Ly.w2, Ly.b2, 3 * li + 2, nxt)
+    if D == 0:
+        kern.layernorm(sb.x, *model.ln_final, sb.h)
     kern.gemm(sb.h, sb.E_out, sb.logits, N.EPI_LOGITS, lse_part=sb.lse_part, mask=sb.mask,
               rows_per_group=sb.group)
     if nf:

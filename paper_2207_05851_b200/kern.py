@@ -41,8 +41,12 @@ def dcode(t: torch.Tensor) -> int:
 
 
 def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_row=None,
-         step=None, state_stride=0, lse_part=None, mask=None, rows_per_group=1, simt=False):
-    """out (or residual x) <- epilogue(A[M,K] . W[N,K]^T)."""
+         step=None, state_stride=0, lse_part=None, mask=None, rows_per_group=1, simt=False,
+         ln=None, ln_out=None, ln_counter=None, eps=1e-5):
+    """out (or residual x) <- epilogue(A[M,K] . W[N,K]^T).  For RESID, ln =
+    (gain, bias) with ln_out (bf16) and ln_counter also writes
+    ln_out = LayerNorm(x) of the updated rows (fused on the swap-AB kernel,
+    else a LayerNorm launch follows)."""
     M = A.shape[0] if M is None else M
     Nn, K = W.shape
     epi = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), out.stride(0), dcode(out), None,
@@ -50,6 +54,11 @@ def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_ro
                      N.ptr(step), state_stride, N.ptr(lse_part),
                      lse_part.shape[1] // 2 if lse_part is not None else 0, N.ptr(mask),
                      mask.shape[1] if mask is not None else 0, rows_per_group)
+    if ln is not None:
+        epi.ln_gain, epi.ln_bias = ln[0].data_ptr(), ln[1].data_ptr()
+        epi.ln_eps = eps
+        epi.ln_out, epi.ln_ldo = ln_out.data_ptr(), ln_out.stride(0)
+        epi.ln_counter = ln_counter.data_ptr()
     N.call("skb_gemm_simt" if simt else "skb_gemm", dcode(A), M, Nn, K, A.data_ptr(),
            A.stride(0), W.data_ptr(), W.stride(0), C.byref(epi), stream())
     _count()

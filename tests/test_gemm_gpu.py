@@ -286,3 +286,35 @@ def test_swap_ab_ssru_cluster(gemm_path, na, cs):
     torch.cuda.synchronize()
     assert (c_next.double() - c).abs().max().item() < 1e-3
     assert (x.double() - (x0.double() + torch.relu(c))).abs().max().item() < 1e-3
+
+
+@pytest.mark.parametrize("M,Nn,K,cs", [(640, 1024, 1024, 0), (640, 1024, 4096, 0), (77, 512, 1024, 0),
+                                       (300, 1024, 4096, 4), (5, 256, 1024, 0), (640, 1024, 1024, 1)])
+def test_resid_fused_layernorm(gemm_path, M, Nn, K, cs):
+    """RESID with a fused LayerNorm (model.py:562-575): x += A.W^T + b, then
+    h = LN(x) bf16 — bitwise equal to the standalone LayerNorm kernel on the
+    updated x, on both the fused (swap-AB) and the fallback (LN launch) path;
+    the arrival tickets make repeated launches on one counter row valid."""
+    from paper_2207_05851_b200 import kern
+    if cs:
+        N.call("skb_gemm_force_sw", 2 if gemm_path == "sw" else 1, 0, cs)
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(Nn, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    gain = torch.rand(Nn, device="cuda", generator=g) + 0.5
+    lb = torch.randn(Nn, device="cuda", generator=g)
+    ctr = torch.zeros(64, dtype=torch.int32, device="cuda")
+    x0 = torch.randn(M, Nn, device="cuda", generator=g) * 3 + 1
+    for rep in range(3):
+        x = x0.clone()
+        h = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+        kern.gemm(A, W, x, N.EPI_RESID, bias, ln=(gain, lb), ln_out=h, ln_counter=ctr)
+        h_ref = torch.zeros_like(h)
+        kern.layernorm(x, gain, lb, h_ref)
+        torch.cuda.synchronize()
+        ref = x0.double() + A.double() @ W.double().T + bias.double()
+        assert (x.double() - ref).abs().max().item() <= 2e-3 * K ** 0.5
+        assert torch.equal(h, h_ref), (h.float() - h_ref.float()).abs().max().item()
+        want = torch.nn.functional.layer_norm(x, (Nn,), gain, lb, eps=1e-5)
+        assert (h.float() - want).abs().max().item() < 3e-2
