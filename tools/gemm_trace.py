@@ -21,7 +21,17 @@ cfgs = [(int(a), int(b)) for a, b in (x.split(",") for x in sys.argv[1:])] or [(
 for name, (Nn, K) in shapes.items():
     A = torch.randn(M, K, device="cuda").bfloat16()
     Ws = [torch.randn(Nn, K, device="cuda").bfloat16() for _ in range(8 if Nn * K < 1e8 / 2 else 2)]
-    if os.environ.get("LOGITS"):
+    if os.environ.get("RESIDLN"):
+        out = torch.zeros(M, Nn, device="cuda")
+        hln = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+        gain = torch.ones(Nn, device="cuda")
+        lb = torch.zeros(Nn, device="cuda")
+        ctr = torch.zeros(64, dtype=torch.int32, device="cuda")
+        lnp = torch.zeros(M, 16, device="cuda")
+        epi = N.Epilogue(N.EPI_RESID, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None,
+                         0, None, 0, None, 0, 1, None, 0, None, 0, gain.data_ptr(), lb.data_ptr(),
+                         1e-5, hln.data_ptr(), Nn, ctr.data_ptr())
+    elif os.environ.get("LOGITS"):
         out = torch.zeros(M, Nn, device="cuda")
         part = torch.zeros(M, 2 * ((Nn + 31) // 32), device="cuda")
         epi = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None,
@@ -44,10 +54,10 @@ for name, (Nn, K) in shapes.items():
         t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16).astype(np.int64)
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        cols = [0, 2, 3, 5, 1, 8, 9, 10, 4, 11, 12, 6]
+        cols = [0, 2, 3, 5, 1, 8, 9, 10, 4, 11, 12, 13, 14, 6]
         rel = (t[:, cols] - t0) / 1e3
-        labels = ["entry", "postwait", "stage0", "accready", "partial", "csync", "recv", "summed",
-                  "stored", "flushed", "stats", "exit"]
+        labels = ["entry", "postwait", "stage0", "accready", "epi/partial", "csync", "recv",
+                  "summed", "stored", "flushed", "stats", "ln_ticket", "ln_rows", "exit"]
         print(f"{name} na={na} cs={cs} ctas={len(t)} sms={len(set(t[:, 7]))}")
         for j, lab in enumerate(labels):
             col = rel[:, j]
