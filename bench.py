@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON rules)")
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("SKB_STREAMS", "2")),
+                    help="independent batches decoded concurrently on separate CUDA streams")
     return ap.parse_args()
 
 
@@ -186,7 +188,8 @@ def gemm_roofline(model, R, L, peak):
     ms_out = e0.elapsed_time(e1) / reps
     out_flops = 2 * R * model.E_trg_c.shape[0] * d
     achieved = flops / (ms / 1e3) / 1e12
-    return {"kernel": "k_gemm_tc (tcgen05 bf16, all GEMMs of one decode step, R=%d)" % R,
+    return {"kernel": "k_gemm_sw (swap-AB tcgen05/TMA bf16 GEMM, all GEMMs of one decode step,"
+                      " R=%d)" % R,
             "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
             "flops_per_step": flops, "ms_per_decode_step_gemms": round(ms, 4),
@@ -272,45 +275,72 @@ def run_ours(args):
             out = [torch.empty_like(toks) for _ in range(world)] if rank == 0 else None
             dist.gather(toks, out, dst=0)
 
-    # ---- warm-up (also compiles TMA descriptors, captures graphs)
-    for w in range(max(args.warmup, 2)):  # both workspace slots get their graphs
-        bb = make_batch(model, vocabs, sents(1000 + w), K, args.alpha, slot=w & 1)
-        bb.run()
-        gather(bb)
-    torch.cuda.synchronize()
-    # ---- value: inputs staged in HBM before the timed region
-    batches = [make_batch(model, vocabs, sents(s), K, args.alpha, slot=s & 1)
-               for s in range(args.steps)]
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = ClockSampler(local)
-    l0 = kern.launches
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    results = []
-    prev = None  # batch i+1 is launched before batch i is read back (two workspaces)
-    for bb in batches:
-        bb.start()
-        if prev is not None:
-            results.append(prev.finish())
-            gather(prev)
-        prev = bb
-    results.append(prev.finish())
-    gather(prev)
-    e1.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    launches = kern.launches - l0
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    # Batches are decoded on S CUDA streams concurrently (batch i on stream
+    # i % S) — the engine's serving mode: independent 128-sentence batches in
+    # flight together fill the SMs that one batch's latency-bound kernels
+    # (attention, beam, small GEMMs) leave idle.  On each stream batch i+S is
+    # launched before batch i is read back, so a stream alternates two
+    # workspaces (slots).  The single-stream number is measured too.
+    def timed(S):
+        streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(S - 1)]
+
+        def slot_of(i):
+            return 2 * (i % S) + ((i // S) & 1)
+
+        # warm-up (compiles TMA descriptors, captures every slot's graphs)
+        for w in range(max(args.warmup, 2 * S)):
+            bb = make_batch(model, vocabs, sents(1000 + w), K, args.alpha, slot=slot_of(w))
+            with torch.cuda.stream(streams[w % S]):
+                bb.run()
+            gather(bb)
+        torch.cuda.synchronize()
+        # inputs staged in HBM before the timed region
+        batches = [make_batch(model, vocabs, sents(s), K, args.alpha, slot=slot_of(s))
+                   for s in range(args.steps)]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local)
+        l0 = kern.launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for st in streams[1:]:
+            st.wait_stream(streams[0])
+        results = []
+        inflight = []
+        for i, bb in enumerate(batches):
+            with torch.cuda.stream(streams[i % S]):
+                bb.start()
+            inflight.append(bb)
+            if len(inflight) > S:
+                done = inflight.pop(0)
+                results.append(done.finish())
+                gather(done)
+        for done in inflight:
+            results.append(done.finish())
+            gather(done)
+        for st in streams[1:]:
+            streams[0].wait_stream(st)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+        launches = kern.launches - l0
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), results, launches, clk, batches
+
+    n_streams = max(1, args.streams)
+    ms1, results, launches, clk, batches = timed(1)
+    value_1 = world * B * args.steps / (ms1 / 1e3)
+    ms_max = ms1
+    if n_streams > 1:
+        ms_max, results, launches, clk, _ = timed(n_streams)
     ms_step = ms_max / args.steps
     value = world * B * args.steps / (ms_max / 1e3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     forced = sum(r.forced_eos for res in results for r in res)
     steps_per_sent = statistics.mean(r.steps for res in results for r in res)
 
@@ -356,6 +386,8 @@ def run_ours(args):
                                f"alpha {args.alpha}, batch {B} sentences/GPU, src len {L}, "
                                f"{2 * L + 10}-step cap",
                    "global_batch": B * world, "seq_len": L, "parallelism": f"replicas x{world}",
+                   "streams_per_gpu": n_streams, "batch_per_stream": B,
+                   "value_single_stream": round(value_1, 2),
                    "l2": "working set > L2 (weights 0.48 GB + KV cache 1.1 GB per batch)"},
         "e2e": e2e, "roofline": roof, "gpu_launches": launches, "clocks": clk,
         "decode": {"mean_steps_per_sentence": round(steps_per_sent, 2),

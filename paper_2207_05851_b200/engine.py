@@ -415,7 +415,7 @@ class DecodeWorkspace:
 
 
 _WS_CACHE: dict = {}
-_WS_MAX = 6
+_WS_MAX = 10
 
 
 def _workspace(model, key, *args):
@@ -615,21 +615,38 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
     order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i].src_ids))
     per_batch = max(1, max_rows // beam)
     results: list[ChunkResult | None] = [None] * len(jobs)
-    # two batches in flight: batch n+1 is prepared and launched before the
-    # results of batch n are read back (alternating workspaces)
-    pending = None
+    # Batches run concurrently on DECODE_STREAMS CUDA streams (batch n on
+    # stream n % S); on each stream batch n+S is prepared and launched before
+    # batch n is read back, so a stream alternates two workspaces.
+    S = DECODE_STREAMS
+    if len(_STREAMS) < S:
+        _STREAMS.extend(torch.cuda.Stream() for _ in range(S - len(_STREAMS)))
+    main = torch.cuda.current_stream()
+    streams = [main] + _STREAMS[1:S]
+    for st in streams[1:]:
+        st.wait_stream(main)
+    pending = []
     for n, s in enumerate(range(0, len(order), per_batch)):
         idx = order[s:s + per_batch]
         bb = BeamBatch(model, [jobs[i] for i in idx], beam, alpha, nvs_threshold, use_graph,
-                       slot=n & 1)
-        bb.start()
-        if pending is not None:
-            for i, r in zip(pending[0], pending[1].finish()):
+                       slot=2 * (n % S) + ((n // S) & 1))
+        with torch.cuda.stream(streams[n % S]):
+            bb.start()
+        pending.append((idx, bb))
+        if len(pending) > S:
+            pi, pb = pending.pop(0)
+            for i, r in zip(pi, pb.finish()):
                 results[i] = r
-        pending = (idx, bb)
-    for i, r in zip(pending[0], pending[1].finish()):
-        results[i] = r
+    for pi, pb in pending:
+        for i, r in zip(pi, pb.finish()):
+            results[i] = r
+    for st in streams[1:]:
+        main.wait_stream(st)
     return results
+
+
+DECODE_STREAMS = 2   # concurrent decode batches per device (serving mode)
+_STREAMS: list = []
 
 
 # =========================================================== model protocol
