@@ -123,6 +123,12 @@ int skb_gemm_force(int bn, int cs, int splits);
  * K-split; 0 = choose automatically. */
 int skb_gemm_force_sw(int mode, int na, int cs);
 
+/* Number of independent decode streams the caller runs concurrently on this
+ * device (default 1).  The swap-AB GEMM sizes its tiles for its share of the
+ * SMs (fewer, larger tiles ingest fewer bytes in total).  Affects launches
+ * made (or graphs captured) after the call; numerics are unchanged. */
+int skb_set_concurrency(int streams);
+
 /* Same, forcing the SIMT path (for parity tests of the tcgen05 path). */
 int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
                   int ldw, const skb_epilogue *epi, void *stream);

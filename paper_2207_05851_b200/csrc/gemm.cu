@@ -1489,13 +1489,23 @@ static int pick_cs(int N, int K) {
 // CTAs co-reside per SM (113 KB ring), each streams (128 + Na) rows of K,
 // plus a fixed per-CTA cost worth ~160 rows; CTA slots beyond one wave
 // cost proportionally.
+int g_concurrency = 1;  // independent decode streams sharing the GPU (skb_set_concurrency)
+
 static int pick_na(int M, int N, int CS) {
-  const int slots = 2 * tc::num_sms();
+  // with several decode streams in flight each GEMM gets a share of the SMs:
+  // fewer, larger tiles ingest fewer bytes in total
+  const int slots = 2 * tc::num_sms() / (g_concurrency > 0 ? g_concurrency : 1);
   const int n_wt = (N + 127) / 128;
   const int na_max = CS > 1 ? 80 : 160;  // split-K partial + receive slots fit the ring
+  static int na_floor = -1;
+  if (na_floor < 0) {
+    const char *e = getenv("SKB_SW_NA_MIN");
+    na_floor = e ? atoi(e) : 16;
+  }
   int best = 16;
   double best_c = 1e30;
   for (int na = 16; na <= na_max; na += 16) {
+    if (na < na_floor && na + 16 <= na_max && (long)n_wt * ((M + na - 1) / na) > 1) continue;
     if (CS > 1 && na % (4 * CS)) continue;
     const double ctas = (double)n_wt * ((M + na - 1) / na) * CS;
     const double waves = ctas <= slots ? 1.0 : ctas / slots;
@@ -1663,6 +1673,12 @@ extern "C" int skb_gemm_force(int bn, int cs, int splits) {
   tc::g_force_bn = bn;
   tc::g_force_cs = cs;
   tc::g_force_s = splits;
+  return SKB_OK;
+}
+
+extern "C" int skb_set_concurrency(int streams) {
+  if (streams < 1 || streams > 16) return fail(SKB_ERR_CONFIG, "concurrency %d out of [1, 16]", streams);
+  sw::g_concurrency = streams;
   return SKB_OK;
 }
 

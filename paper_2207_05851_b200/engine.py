@@ -415,7 +415,7 @@ class DecodeWorkspace:
 
 
 _WS_CACHE: dict = {}
-_WS_MAX = 10
+_WS_MAX = 16
 
 
 def _workspace(model, key, *args):
@@ -473,7 +473,7 @@ class BeamBatch:
             U = int(U_ids.size)
         else:
             U = V
-        key = (B, L, self.S_max, K, P, U, self.alpha, restricted, self.slot)
+        key = (B, L, self.S_max, K, P, U, self.alpha, restricted, self.slot, kern.concurrency)
         ws = _workspace(model, key, B, L, self.S_max, K, P, U, self.alpha, restricted)
         self.ws = ws
         # this batch's inputs: own pinned staging + own device copy (several
@@ -526,6 +526,9 @@ class BeamBatch:
         self.eos_col = eos_col
         self.h2d_bytes = self.in_host.numel() * 4
         self.in_dev = self.in_host.to(model.device, non_blocking=True)
+        # start() may run on another stream: it waits for this copy
+        self.in_ready = torch.cuda.Event()
+        self.in_ready.record()
 
     # the attributes bench.py / tests read
     @property
@@ -577,6 +580,7 @@ class BeamBatch:
         if ws.state is None or ws.eos_col != self.eos_col:
             ws.bind_state(self.eos_col)
             ws.graph_1 = ws.graph_n = None  # the step graph bakes eos_col in
+        torch.cuda.current_stream().wait_event(self.in_ready)
         ws.in_dev.copy_(self.in_dev, non_blocking=True)   # device-resident inputs
         ws.reset()
         self.steps_run = ws.run(self.use_graph)
@@ -618,7 +622,9 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
     # Batches run concurrently on DECODE_STREAMS CUDA streams (batch n on
     # stream n % S); on each stream batch n+S is prepared and launched before
     # batch n is read back, so a stream alternates two workspaces.
-    S = DECODE_STREAMS
+    n_batches = (len(order) + per_batch - 1) // per_batch
+    S = max(1, min(DECODE_STREAMS, n_batches))
+    kern.set_concurrency(S)
     if len(_STREAMS) < S:
         _STREAMS.extend(torch.cuda.Stream() for _ in range(S - len(_STREAMS)))
     main = torch.cuda.current_stream()

@@ -13,7 +13,18 @@ import torch
 from . import _native as N
 
 launches = 0
+concurrency = 1  # decode streams sharing the device (GEMM tile sizing; see set_concurrency)
 _splitk = None  # (workspace fp32, counters int32) shared by all GEMMs of a device
+
+
+def set_concurrency(n: int) -> None:
+    """Tell the GEMMs how many independent decode streams share the device
+    (tiles are sized for a 1/n share of the SMs).  Workspaces captured under
+    another setting are not reused (the setting is part of their key)."""
+    global concurrency
+    if n != concurrency:
+        N.call("skb_set_concurrency", int(n))
+        concurrency = int(n)
 
 
 def set_splitk_workspace(ws, counters) -> None:
