@@ -113,3 +113,27 @@ def test_tiny_bf16_agreement_report():
     print(f"bf16 tiny greedy: {same}/{len(gold)} identical, token agreement {tok_agree:.3f}")
     assert all(r.forced_eos == g["forced_eos"] for r, g in zip(recs, gold))
     assert tok_agree > 0.5
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_concurrent_stream_batches_identical(precision):
+    """decode_jobs runs its batches concurrently on several CUDA streams, with
+    GEMM tiles sized for the shared device (skb_set_concurrency).  Tile sizes
+    never change numerics, so the records are identical to one stream."""
+    from paper_2207_05851_b200 import engine
+    from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
+    m = product_model("toy", precision)
+    vocabs = product_vocabs("toy")
+    rng = np.random.default_rng(5)
+    words = [vocabs.src_vocab.to_token(i) for i in range(4, len(vocabs.src_vocab))]
+    inputs = [SentenceInput(tokens=[words[i] for i in rng.integers(0, len(words), rng.integers(3, 20))])
+              for _ in range(40)]
+    old = engine.DECODE_STREAMS
+    try:
+        out = {}
+        for streams in (1, 3):
+            engine.DECODE_STREAMS = streams
+            out[streams] = translate(m, vocabs, inputs, SearchSettings(beam=3), max_rows=24)
+    finally:
+        engine.DECODE_STREAMS = old
+    assert [(r.text, r.score) for r in out[1]] == [(r.text, r.score) for r in out[3]]
