@@ -12,7 +12,11 @@ from pathlib import Path
 
 from .errors import ConfigError, NumericError, ShapeError
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libskiff_b200.so"
+import os
+
+# SKB_LIB: alternative build of the same library (A/B experiments)
+LIB_PATH = Path(os.environ.get("SKB_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libskiff_b200.so")
 
 SKB_OK, SKB_ERR_SHAPE, SKB_ERR_CONFIG, SKB_ERR_LAUNCH, SKB_ERR_NUMERIC, SKB_ERR_UNSUPPORTED = range(6)
 F32, BF16 = 0, 1
