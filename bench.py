@@ -137,6 +137,17 @@ def make_batch(model, vocabs, sentences, beam, alpha, slot=0):
     return BeamBatch(model, jobs, beam, alpha, slot=slot)
 
 
+def _gemm_traffic():
+    """DRAM bytes (read + write) of one decode step's GEMM launches from the
+    committed ncu --set full capture (profiles/r1_gemm_step_traffic.json,
+    made by tools/ncu_step.sh; cold-L2 serialised replay), or None."""
+    p = ROOT / "profiles" / "r1_gemm_step_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return {"bytes_per_step": d["dram_bytes_per_step"], "source": d["source"]}
+
+
 def gemm_roofline(model, R, L, peak):
     """Time every GEMM of one decode step (all 6 layers + output projection)
     with CUDA events on the launching stream; achieved = algorithmic FLOPs
@@ -191,7 +202,7 @@ def gemm_roofline(model, R, L, peak):
     return {"kernel": "k_gemm_sw (swap-AB tcgen05/TMA bf16 GEMM, all GEMMs of one decode step,"
                       " R=%d)" % R,
             "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
-            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": _gemm_traffic(),
             "flops_per_step": flops, "ms_per_decode_step_gemms": round(ms, 4),
             "out_proj": {"ms": round(ms_out, 4),
                          "tflops": round(out_flops / (ms_out / 1e3) / 1e12, 1)}}
