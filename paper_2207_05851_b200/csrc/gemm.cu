@@ -1280,34 +1280,25 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 2 && lane == 0) SW_STAMP(4);
     cluster_sync_all();  // peers are done reading my shared memory
   }
-  // ---- fused LayerNorm of this activation-row tile (RESID): the CTAs that
-  // write the tile's columns (n_wt x CS of them, all resident: the next
-  // kernel is launched only after every CTA of this grid has started) take
-  // an arrival ticket; once the whole tile is written each of their epilogue
-  // warps normalises a share of its rows.  Same arithmetic as the LN kernel.
+  // ---- fused LayerNorm of this activation-row tile (RESID): every CTA that
+  // writes columns of the tile (n_wt x CS of them) takes an arrival ticket
+  // once its writes are complete; the CTA drawing the tile's last ticket
+  // normalises all of the tile's rows (no CTA ever waits for another, so
+  // the kernel cannot deadlock however few of its CTAs are resident).
+  // Same arithmetic as the LN kernel.
   if (KIND == SKB_EPI_RESID && ep.ln_out != nullptr && warp >= 2) {
-    __shared__ int ln_go;
+    volatile uint32_t &ln_last = tmem_slot[1];  // flag beside the TMEM address (dynamic smem)
     if (warp == 2 && lane == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence();
       const unsigned G = (unsigned)(((N + 127) / 128) * CS);
-      unsigned *ctr = ep.ln_counter + at;
-      const unsigned tk = atomicAdd(ctr, 1u);
-      const unsigned target = tk - tk % G + G;
-      unsigned cur;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
-        if ((int)(cur - target) >= 0) break;
-        __nanosleep(40);
-      }
-      __threadfence();
-      ln_go = 1;
+      const unsigned tk = atomicAdd(ep.ln_counter + at, 1u);
+      ln_last = (tk % G) == G - 1;
+      if (ln_last) __threadfence();
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    (void)ln_go;
-    const int G4 = ((N + 127) / 128) * CS * 4;
-    for (int rl = (wt * CS + rank) * 4 + (warp - 2); rl < Na && m0 + rl < M; rl += G4)
-      ln_row(ep, m0 + rl, N, lane);
+    if (ln_last)
+      for (int rl = warp - 2; rl < Na && m0 + rl < M; rl += 4) ln_row(ep, m0 + rl, N, lane);
   }
   __syncthreads();
 #ifdef SKB_GEMM_TRACE
