@@ -137,6 +137,35 @@ def make_batch(model, vocabs, sentences, beam, alpha, slot=0):
     return BeamBatch(model, jobs, beam, alpha, slot=slot)
 
 
+def batch1_latency(model, vocabs, L, V, n=21):
+    """The metric's second part: batch-1 latency through translate() (host
+    strings in, records out, one sentence per call), greedy and beam 5, p50
+    over n sentences of length L (wall clock around the public call, which
+    synchronises on its result)."""
+    import torch
+    from paper_2207_05851_b200 import kern
+    from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
+    kern.set_concurrency(1)
+    out = {}
+    for name, beam in (("greedy", 1), ("beam5", 5)):
+        sents = synth_sentences(n + 2, L, V, seed=4242)
+        st = SearchSettings(beam=beam)
+        for s in sents[:2]:  # warm-up: workspace + captured graphs for this shape
+            translate(model, vocabs, [SentenceInput(tokens=s)], st)
+        torch.cuda.synchronize()
+        ts = []
+        for s in sents[2:]:
+            t0 = time.perf_counter()
+            recs = translate(model, vocabs, [SentenceInput(tokens=s)], st)
+            ts.append((time.perf_counter() - t0) * 1e3)
+            assert recs[0].error is None
+        ts.sort()
+        out[name] = {"p50_ms": round(statistics.median(ts), 3), "p90_ms": round(ts[int(0.9 * (n - 1))], 3),
+                     "steps": 2 * L + 10}
+    out["api"] = "paper_2207_05851_b200.search.translate, 1 sentence per call, L=%d" % L
+    return out
+
+
 def _gemm_traffic():
     """DRAM bytes (read + write) of one decode step's GEMM launches from the
     committed ncu --set full capture (profiles/r1_gemm_step_traffic.json,
@@ -391,6 +420,7 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    lat = None if args.no_e2e else batch1_latency(model, vocabs, L, V)
     roof = gemm_roofline(model, B * K, L, peak_tf)
     roof["peak_source"] = peak_src
     breakdown = step_breakdown(batches[-1])
@@ -406,7 +436,8 @@ def run_ours(args):
                    "streams_per_gpu": n_streams, "batch_per_stream": B,
                    "value_single_stream": round(value_1, 2),
                    "l2": "working set > L2 (weights 0.48 GB + KV cache 1.1 GB per batch)"},
-        "e2e": e2e, "roofline": roof, "gpu_launches": launches, "clocks": clk,
+        "e2e": e2e, "batch1_latency": lat, "roofline": roof, "gpu_launches": launches,
+        "clocks": clk,
         "decode": {"mean_steps_per_sentence": round(steps_per_sent, 2),
                    "forced_eos_sentences": forced, "step_breakdown_ms": breakdown},
     }
