@@ -1100,26 +1100,33 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       // weights first: independent of the previous kernel (PDL prologue)
       const int pre = nkc < stages ? nkc : stages;
+#ifdef SKB_GEMM_TRACE
+      // timing experiments: 4 = skip the activation loads, 5 = skip weights
+      const int ldbg = g_dbg;
+#else
+      constexpr int ldbg = 0;
+#endif
+      const int sbx = ldbg == 4 ? W_BYTES : (ldbg == 5 ? SB - W_BYTES : SB);
 #pragma unroll 1
       for (int q = 0; q < pre; ++q) {
-        mbar_expect_tx(&full[q], SB);
-        tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * BK, n0, &full[q]);
+        mbar_expect_tx(&full[q], sbx);
+        if (ldbg != 5) tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * BK, n0, &full[q]);
       }
       pdl_wait();
       pdl_trigger();
       SW_STAMP(2);
 #pragma unroll 1
       for (int q = 0; q < pre; ++q)
-        tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * BK, m0, &full[q]);
+        if (ldbg != 4) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * BK, m0, &full[q]);
 #pragma unroll 1
       for (int it = pre; it < nkc; ++it) {
         const int s = it % stages;
         const uint32_t ph = (it / stages) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t *st = smem + s * SB;
-        mbar_expect_tx(&full[s], SB);
-        tma_load_2d(st, &tmW, (kb0 + it) * BK, n0, &full[s]);
-        tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * BK, m0, &full[s]);
+        mbar_expect_tx(&full[s], sbx);
+        if (ldbg != 5) tma_load_2d(st, &tmW, (kb0 + it) * BK, n0, &full[s]);
+        if (ldbg != 4) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * BK, m0, &full[s]);
       }
     } else {
       pdl_wait();

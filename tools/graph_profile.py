@@ -15,9 +15,12 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 import bench  # noqa: E402
 
+import os
+B = int(os.environ.get("BATCH", "128"))
+K = int(os.environ.get("BEAM", "5"))
 model, vocabs = bench.build_model("bf16")
-sents = bench.synth_sentences(128, 30, 32000, seed=13)
-bb = bench.make_batch(model, vocabs, sents, 5, 1.0)
+sents = bench.synth_sentences(B, 30, 32000, seed=13)
+bb = bench.make_batch(model, vocabs, sents, K, 1.0)
 for _ in range(2):
     bb.run()
 torch.cuda.synchronize()
