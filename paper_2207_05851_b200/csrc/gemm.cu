@@ -1761,7 +1761,12 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   const bool can_split = epi->splitk_ws != nullptr && epi->splitk_counters != nullptr;
   tc::init_forces();
   const int force_bn = tc::g_force_bn, force_s = tc::g_force_s;
-  const int bns[3] = {256, 128, 64};
+  // BN <= 128: two accumulators of BN columns keep every CTA at <= 256 TMEM
+  // columns, so the (at most two) TMEM-using CTAs an SM holds never block in
+  // tcgen05.alloc — with several decode streams sharing the device a CTA
+  // blocked there (holding shared memory) could otherwise stall the others.
+  // BN = 256 stays available through skb_gemm_force.
+  const int bns[3] = {force_bn == 256 ? 256 : 128, 128, 64};
   auto cost = [&](long m, int bn, int sp) {
     const long tiles = ((m + tc::BM - 1) / tc::BM) * ((N + bn - 1) / bn) * sp;
     const long rounds = (tiles + nsm - 1) / nsm;
