@@ -222,9 +222,9 @@ class Model:
         kern.gemm(a, self.w_ckv, out)
         return out
 
-    def nvs_mask_device(self, enc, lengths, B, L, threshold) -> torch.Tensor:
-        """NVS head (model.py:496-517): masked max-pool, linear, sigmoid >
-        threshold, as a [B, ceil(V/32)] bitmask on the device."""
+    def nvs_logits_device(self, enc, lengths, B, L) -> torch.Tensor:
+        """nvs_logits (model.py:496-501): masked max-pool over the unpadded
+        encoder positions, then one linear layer; fp32 [B, V]."""
         d, V = self.config.d_model, self.config.trg_vocab_size
         pooled = torch.empty(B, d, device=self.device)
         kern.masked_maxpool(enc, lengths, pooled, B, L, d)
@@ -235,6 +235,13 @@ class Model:
             pc = pooled
         logits = torch.empty(B, V, device=self.device)
         kern.gemm(pc, self.w_nvs, logits, N.EPI_STORE, self.b_nvs)
+        return logits
+
+    def nvs_mask_device(self, enc, lengths, B, L, threshold) -> torch.Tensor:
+        """NVS head (model.py:496-517): masked max-pool, linear, sigmoid >
+        threshold, as a [B, ceil(V/32)] bitmask on the device."""
+        V = self.config.trg_vocab_size
+        logits = self.nvs_logits_device(enc, lengths, B, L)
         mask = torch.empty(B, (V + 31) // 32, device=self.device, dtype=torch.int32)
         kern.nvs_mask(logits, float(np.float32(threshold)), mask)
         return mask
@@ -263,10 +270,49 @@ class Model:
         GPU buffer)."""
         return state.step_forward(prev_ids, prev_factor_ids)
 
+    def forward_sequence(self, src_ids, src_factor_ids, src_lengths, trg_in_ids,
+                         trg_in_factor_ids) -> "SequenceOutput":
+        """model.py:444-492, teacher forced: target inputs carry BOS at
+        position 0 (and the shift marker in factor streams).  The decoder
+        runs position by position on the device step kernels — the causal
+        self-attention of the full pass is the incremental attention over the
+        cached K/V (the reference's own invariant, test_model.py:270-282) —
+        and the SSRU recurrence is its scan.  surface: raw logits [B, T, V]."""
+        from .engine import _HostView
+        trg = np.asarray(trg_in_ids)
+        if trg.ndim != 2:
+            raise ShapeError(f"trg_in_ids must be [B, T], got shape {trg.shape}")
+        B, T = trg.shape
+        c = self.config
+        fac_in = [np.asarray(f) for f in trg_in_factor_ids]
+        if len(fac_in) != len(c.target_factor_specs):
+            raise ShapeError(f"model wants {len(c.target_factor_specs)} target factor streams, "
+                             f"got {len(fac_in)}")
+        st = self.decode_init(src_ids, src_factor_ids, src_lengths)
+        surf, facs = [], [[] for _ in fac_in]
+        for t in range(T):
+            o = self.decode_step(st, trg[:, t], [f[:, t] for f in fac_in])
+            surf.append(o.surface.device_tensor)
+            for k, f in enumerate(o.factors):
+                facs[k].append(f.device_tensor)
+        nvs = None
+        if c.nvs_enabled:
+            nvs = _HostView(self.nvs_logits_device(st.enc.x, st.enc.lengths, st.enc.B, st.enc.L))
+        return SequenceOutput(_HostView(torch.stack(surf, 1)),
+                              [_HostView(torch.stack(f, 1)) for f in facs], nvs)
+
 
 def mask_to_ids(mask_row: np.ndarray, V: int) -> np.ndarray:
     bits = np.unpackbits(mask_row.astype("<u4").view(np.uint8), bitorder="little")
     return np.flatnonzero(bits[:V]).astype(np.int64)
+
+
+@dataclass
+class SequenceOutput:
+    """model.py:283-288: teacher-forced outputs (host-readable wrappers)."""
+    surface: object
+    factors: list
+    nvs: object | None
 
 
 @dataclass

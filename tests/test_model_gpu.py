@@ -74,3 +74,23 @@ def test_nvs_select_matches_reference():
     st = m.decode_init(g["src"], [], g["lens"])
     ids = m.nvs_select(st.enc, g["lens"], 0.5, [0, 1, 3])
     np.testing.assert_array_equal(np.concatenate(ids), g["nvs_ids"])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("name", [n for n, s in CONFIGS.items()
+                                  if s.get("steps") and s["steps"].get("teacher")])
+def test_forward_sequence_matches_reference(name, precision):
+    """model.py:444-492 (teacher forced) on the device vs the REFERENCE's own
+    forward_sequence logits (tests/golden/steps_*.npz 'teacher_logits')."""
+    g = np.load(GOLDEN / f"steps_{name}.npz")
+    m = product_model(name, precision)
+    nsf, ntf = len(m.config.source_factor_specs), len(m.config.target_factor_specs)
+    out = m.forward_sequence(g["src"][:1], [g[f"src_factor{i}"][:1] for i in range(nsf)],
+                             g["lens"][:1], g["fed"].T[:1],
+                             [g[f"fed_factor{k}"].T[:1] for k in range(ntf)])
+    got = out.surface.data
+    ref = g["teacher_logits"]
+    assert got.shape == ref.shape
+    worst = float(np.abs(O.log_softmax(got) - O.log_softmax(ref)).max())
+    assert worst <= TOL[precision], worst
+    assert len(out.factors) == ntf
