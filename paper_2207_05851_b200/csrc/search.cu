@@ -53,32 +53,64 @@ __device__ __forceinline__ void list_insert(double (&k)[MAXK], float (&l)[MAXK],
 }
 
 
-// K-th largest of the values held by a CTA (each thread passes its values
-// through `feed`); K <= MAXK.  Exact; used to bound the beam threshold from
-// the per-32-column group maxima the output GEMM wrote.
+// Order-preserving integer images of fp32 / fp64 keys (no NaNs occur;
+// -0 is folded into +0 so that equal keys map to equal images), so warp
+// selections run on redux.sync instead of five-level shuffle trees.
+__device__ __forceinline__ unsigned ord32(float v) {
+  const unsigned u = __float_as_uint(v + 0.0f);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord32(unsigned o) {
+  return __uint_as_float((o >> 31) ? (o & 0x7fffffffu) : ~o);
+}
+__device__ __forceinline__ unsigned long long ord64(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v + 0.0);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Lane holding the best entry of the warp in the order (key desc, col asc,
+// lane asc) among lanes with `has`; -1 if none.
+__device__ __forceinline__ int warp_best(double key, int col, bool has) {
+  const unsigned long long o = ord64(key);
+  const unsigned hi = has ? (unsigned)(o >> 32) : 0u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const bool h1 = has && hi == mh;
+  const unsigned ml = __reduce_max_sync(0xffffffffu, h1 ? (unsigned)o : 0u);
+  const bool h2 = h1 && (unsigned)o == ml;
+  const unsigned mc = __reduce_min_sync(0xffffffffu, h2 ? (unsigned)col : 0xffffffffu);
+  const unsigned who = __ballot_sync(0xffffffffu, h2 && (unsigned)col == mc);
+  return who ? __ffs(who) - 1 : -1;
+}
+
+// First maximum (value desc, column asc) across the warp.
+__device__ __forceinline__ void warp_argmax(float &v, int &col) {
+  const unsigned m = __reduce_max_sync(0xffffffffu, ord32(v));
+  const unsigned c = __reduce_min_sync(0xffffffffu, ord32(v) == m ? (unsigned)col : 0xffffffffu);
+  v = unord32(m);
+  col = (int)c;
+}
+
+// K rounds of "take the warp maximum of the lanes' sorted lists' heads";
+// writes the K values (descending) through lane 0 when out != nullptr and
+// returns the K-th largest.  Exact; used to bound the beam threshold from the
+// per-32-column group maxima the output GEMM wrote.
 template <int MAXK>
-__device__ __forceinline__ void warp_topk_vals(float (&v)[MAXK], int K, float *out_warp) {
-  // v sorted descending per lane; K rounds of warp max with pop-one
+__device__ __forceinline__ float warp_kth(float (&v)[MAXK], int K, float *out = nullptr) {
   const int lane = threadIdx.x & 31;
+  float last = -INFINITY;
   for (int j = 0; j < K; ++j) {
-    float b = v[0];
-    int bl = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ob = __shfl_xor_sync(0xffffffffu, b, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ob > b || (ob == b && ol < bl)) {
-        b = ob;
-        bl = ol;
-      }
-    }
-    if (lane == 0) out_warp[j] = b;
+    const unsigned o = ord32(v[0]);
+    const unsigned m = __reduce_max_sync(0xffffffffu, o);
+    const int bl = __ffs(__ballot_sync(0xffffffffu, o == m)) - 1;
+    last = unord32(m);
+    if (out && lane == 0) out[j] = last;
     if (lane == bl) {
 #pragma unroll
       for (int q = 0; q + 1 < MAXK; ++q) v[q] = v[q + 1];
       v[MAXK - 1] = -INFINITY;
     }
   }
+  return last;
 }
 
 template <int MAXK>
@@ -93,80 +125,84 @@ __device__ __forceinline__ void vals_insert(float (&v)[MAXK], float x) {
     }
 }
 
-// K-th largest value across the warp's per-lane sorted lists (K <= MAXK).
-template <int MAXK>
-__device__ __forceinline__ float warp_kth(float (&v)[MAXK], int K) {
-  const int lane = threadIdx.x & 31;
-  float last = -INFINITY;
-  for (int j = 0; j < K; ++j) {
-    float b = v[0];
-    int bl = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ob = __shfl_xor_sync(0xffffffffu, b, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ob > b || (ob == b && ol < bl)) {
-        b = ob;
-        bl = ol;
-      }
-    }
-    last = b;
-    if (lane == bl) {
-#pragma unroll
-      for (int q = 0; q + 1 < MAXK; ++q) v[q] = v[q + 1];
-      v[MAXK - 1] = -INFINITY;
-    }
-  }
-  return last;
-}
-
 // Optional phase timestamps (build with SKB_NVCC_EXTRA=-DSKB_PROFILE_PHASES)
 #ifdef SKB_PROFILE_PHASES
 __device__ unsigned long long g_tprof[4096 * 10];
 #define TP(k)                                                                         \
   do {                                                                                \
     unsigned long long _t;                                                            \
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t));                             \
-    if (lane == 0 && r < 4096) g_tprof[r * 10 + (k)] = _t;                            \
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t)::"memory");                   \
+    if (lane == 0 && r < 1024 && s < 4) g_tprof[((s << 10) + r) * 10 + (k)] = _t;     \
   } while (0)
 #else
-#define TP(k) \
-  do {        \
-  } while (0)
+// phase boundaries stay compiler scheduling fences: without them ptxas
+// interleaves the phases of k_beam_step and the kernel runs ~1.7x slower
+#define TP(k) asm volatile("" ::: "memory")
 #endif
 
-// Shared-memory layout of one sentence CTA (K warps).
-template <int MAXK>
+// Shared-memory layout of one sentence CTA (K rows x SUB warps).
+template <int MAXK, int SUB>
 struct BeamSmem {
   double key[MAXK][MAXK];   // row lists (row, rank)
   float lp[MAXK][MAXK];
   int col[MAXK][MAXK];
   int cnt[MAXK];
   int arg[MAXK];
-  int cg[MAXK][64];         // per-warp candidate group list
+  int cg[MAXK][SUB][64];    // per-warp candidate group list
+  // per-warp partial results of a row, combined by the row's first warp
+  double skey[MAXK][SUB][MAXK];
+  float slp[MAXK][SUB][MAXK];
+  int scol[MAXK][SUB][MAXK];
+  int scnt[MAXK][SUB];
+  float sav[MAXK][SUB];     // first-max argmax (value, column)
+  int sac[MAXK][SUB];
+  float rm[MAXK][SUB];      // row max / sum of exp partials
+  float rs[MAXK][SUB];
+  float rgv[MAXK][SUB * MAXK];  // top group maxima
 };
 
-// One CTA per sentence, one warp per beam row (slot r = b*K + i); the rows
+#ifndef SKB_BEAM_SUB5
+#define SKB_BEAM_SUB5 4  // warps per beam row at K = 5
+#endif
+
+// Barrier over the SUB warps of one beam row (named barrier 1 + row).
+template <int SUB>
+__device__ __forceinline__ void row_sync(int row) {
+  __syncwarp();
+#ifdef SKB_ROWSYNC_ALL
+  __syncthreads();
+#else
+  if constexpr (SUB > 1) asm volatile("barrier.sync %0, %1;" ::"r"(1 + row), "r"(SUB * 32) : "memory");
+#endif
+}
+
+// One CTA per sentence, SUB warps per beam row (slot r = b*K + i); the rows
 // exchange their candidate lists through shared memory (one barrier), so
-// there are no global atomics or fences.  Per row:
+// there are no global atomics or fences.  Per row, each warp takes every
+// SUB-th block of 32 columns (groups):
 //   1. log-softmax statistics: combine the output GEMM's per-32-column
 //      (max, sum exp) partials (staged in shared memory), or reduce the row;
+//      the warps' max / sum partials are combined in warp order;
 //   2. candidate columns: with partials, only 32-column groups whose max can
 //      reach the top K (exact pruning: the margin covers the fp32 rounding
 //      of (x - max) - lse and the fp64 rounding of s_r + lp, so ties are
 //      never lost); otherwise every active column;
 //   3. per-lane top-K of float64 keys s_r + lp (first-max argmax of lp at the
-//      final step), merged across the warp with shuffles;
+//      final step), merged across the warp with shuffles, then across the
+//      row's warps (columns are disjoint, so the order stays exact);
 // then warp 0 merges the <= K row lists in lexsort order (score desc, token
 // asc, parent asc) and routes EOS / survivors (search.py:363-393).
-template <int MAXK>
-__global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict__ logits, int ld,
-                                                          int lp_in, skb_beam_state st) {
+template <int MAXK, int SUB>
+__global__ void __launch_bounds__(MAXK * 32 * SUB)
+    k_beam_step(const float *__restrict__ logits, int ld, int lp_in, skb_beam_state st) {
   PDL_ENTRY();
   extern __shared__ __align__(16) uint8_t beam_smem[];
-  BeamSmem<MAXK> &sm = *reinterpret_cast<BeamSmem<MAXK> *>(beam_smem);
-  float2 *part_s = reinterpret_cast<float2 *>(beam_smem + ((sizeof(BeamSmem<MAXK>) + 15) & ~size_t(15)));
-  const int lane = threadIdx.x & 31, i = threadIdx.x >> 5;
+  using Smem = BeamSmem<MAXK, SUB>;
+  Smem &sm = *reinterpret_cast<Smem *>(beam_smem);
+  float2 *part_s = reinterpret_cast<float2 *>(beam_smem + ((sizeof(Smem) + 15) & ~size_t(15)));
+  constexpr int SW = 32 * SUB;  // threads per row
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = w / SUB, s = w % SUB;
   const int K = st.K, U = st.U;
   const int R = st.B * K;
   const int b = blockIdx.x;
@@ -175,10 +211,13 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
   const int nf = st.n_factors;
   const int G = (U + 31) >> 5;
   TP(0);
-  if (st.done[b]) return;
+  // independent state loads issued together (one round trip)
+  const int done = st.done[b];
   const int nalive = st.n_alive[b];
   const int plen = st.prefix_len[b];
-  const bool final_force = (t == st.max_len[b] - 1) && (t >= plen);
+  const int mlen = st.max_len[b];
+  if (done) return;
+  const bool final_force = (t == mlen - 1) && (t >= plen);
   const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
 
   if (i < nalive) {
@@ -204,46 +243,73 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
         const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
         const int n4 = al ? (G >> 1) : 0;
         if (!al)
-          for (int g = lane; g < G; g += 32) part_s[(size_t)i * G + g] = gpart[g];
-        for (int q0 = lane; q0 < n4; q0 += 32 * 8) {
+          for (int g = s * 32 + lane; g < G; g += SW) part_s[(size_t)i * G + g] = gpart[g];
+        for (int q0 = s * 32 + lane; q0 < n4; q0 += SW * 8) {
           float4 v[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (q0 + 32 * u < n4) v[u] = __ldcs(src + q0 + 32 * u);
+            if (q0 + SW * u < n4) v[u] = __ldcs(src + q0 + SW * u);
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            if (q0 + 32 * u < n4) dst[q0 + 32 * u] = v[u];
+            if (q0 + SW * u < n4) dst[q0 + SW * u] = v[u];
         }
-        if (al && (G & 1) && lane == 0) part_s[(size_t)i * G + G - 1] = gpart[G - 1];
-        __syncwarp();
+        if (al && (G & 1) && s == 0 && lane == 0) part_s[(size_t)i * G + G - 1] = gpart[G - 1];
+        row_sync<SUB>(i);
       }
       TP(2);
       float gv[MAXK];
 #pragma unroll
       for (int j = 0; j < MAXK; ++j) gv[j] = -INFINITY;
       float m = -INFINITY;
-      for (int g = lane; g < G; g += 32) {
+      for (int g = s * 32 + lane; g < G; g += SW) {
         const float v = part[g].x;
         m = fmaxf(m, v);
         if (v > gv[MAXK - 1]) vals_insert<MAXK>(gv, v);
       }
-      mx = warp_max(m);
+      m = unord32(__reduce_max_sync(0xffffffffu, ord32(m)));
+      if (do_topk) warp_kth<MAXK>(gv, kk, &sm.rgv[i][s * MAXK]);
+      if (lane == 0) sm.rm[i][s] = m;
+      row_sync<SUB>(i);
+      mx = sm.rm[i][0];
+#pragma unroll
+      for (int q = 1; q < SUB; ++q) mx = fmaxf(mx, sm.rm[i][q]);
       float sum = 0.f;
-      for (int g = lane; g < G; g += 32) {
+      for (int g = s * 32 + lane; g < G; g += SW) {
         const float2 p = part[g];
         if (p.x != -INFINITY) sum += p.y * expf(p.x - mx);
       }
-      lse = logf(warp_sum(sum));
-      if (do_topk) T = warp_kth<MAXK>(gv, kk);
+      sum = warp_sum(sum);
+      if (lane == 0) sm.rs[i][s] = sum;
+      if (do_topk) {  // K-th largest of the warps' top group maxima
+        float v1[1];
+        v1[0] = lane < SUB * kk ? sm.rgv[i][(lane / kk) * MAXK + lane % kk] : -INFINITY;
+        T = warp_kth<1>(v1, kk);
+      }
+      row_sync<SUB>(i);
+      float tot = sm.rs[i][0];
+#pragma unroll
+      for (int q = 1; q < SUB; ++q) tot += sm.rs[i][q];
+      lse = logf(tot);
     } else if (!lp_in) {
       float m = -INFINITY;
-      for (int c = lane; c < U; c += 32)
+      for (int c = s * 32 + lane; c < U; c += SW)
         if (col_active(mask, c)) m = fmaxf(m, row[c]);
-      mx = warp_max(m);
+      m = unord32(__reduce_max_sync(0xffffffffu, ord32(m)));
+      if (lane == 0) sm.rm[i][s] = m;
+      row_sync<SUB>(i);
+      mx = sm.rm[i][0];
+#pragma unroll
+      for (int q = 1; q < SUB; ++q) mx = fmaxf(mx, sm.rm[i][q]);
       float sum = 0.f;
-      for (int c = lane; c < U; c += 32)
+      for (int c = s * 32 + lane; c < U; c += SW)
         if (col_active(mask, c)) sum += expf(row[c] - mx);
-      lse = logf(warp_sum(sum));
+      sum = warp_sum(sum);
+      if (lane == 0) sm.rs[i][s] = sum;
+      row_sync<SUB>(i);
+      float tot = sm.rs[i][0];
+#pragma unroll
+      for (int q = 1; q < SUB; ++q) tot += sm.rs[i][q];
+      lse = logf(tot);
     }
 
     TP(3);
@@ -279,10 +345,12 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
       const float thr_arg =
           need_argmax ? mx - 4e-6f * (2.0f * fabsf(mx) + fabsf(lse) + 1.0f) : INFINITY;
       const float thr = fminf(thr_top, thr_arg);
-      // collect candidate groups in increasing order (ballot per 32 groups)
+      // collect this warp's candidate groups in increasing order (ballot per
+      // 32 groups)
+      int *cg = sm.cg[i][s];
       int ncg = 0;
       bool overflow = false;
-      for (int g0 = 0; g0 < G; g0 += 32) {
+      for (int g0 = s * 32; g0 < G; g0 += SW) {
         const int g = g0 + lane;
         unsigned cand = __ballot_sync(0xffffffffu, g < G && part[g].x >= thr);
         const int n = __popc(cand);
@@ -290,7 +358,7 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
           overflow = true;
           break;
         }
-        if ((cand >> lane) & 1u) sm.cg[i][ncg + __popc(cand & ((1u << lane) - 1u))] = g;
+        if ((cand >> lane) & 1u) cg[ncg + __popc(cand & ((1u << lane) - 1u))] = g;
         ncg += n;
       }
       __syncwarp();
@@ -301,17 +369,17 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
           float xv[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const int c = q0 + u < ncg ? (sm.cg[i][q0 + u] << 5) + lane : U;
+            const int c = q0 + u < ncg ? (cg[q0 + u] << 5) + lane : U;
             xv[u] = c < U ? __ldcs(row + c) : 0.f;
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const int c = q0 + u < ncg ? (sm.cg[i][q0 + u] << 5) + lane : U;
+            const int c = q0 + u < ncg ? (cg[q0 + u] << 5) + lane : U;
             if (c < U) visit(c, xv[u]);
           }
         }
       } else {
-        for (int g0 = 0; g0 < G; g0 += 32) {
+        for (int g0 = s * 32; g0 < G; g0 += SW) {
           const int g = g0 + lane;
           unsigned cand = __ballot_sync(0xffffffffu, g < G && part[g].x >= thr);
           while (cand) {
@@ -325,63 +393,32 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
       const bool vec = (U & 3) == 0 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0;
       if (vec) {
         const float4 *row4 = reinterpret_cast<const float4 *>(row);
-        for (int c4 = lane; c4 < (U >> 2); c4 += 32) {
+        for (int c4 = s * 32 + lane; c4 < (U >> 2); c4 += SW) {
           const float4 v = __ldcs(row4 + c4);
           const int c = 4 * c4;
           visit(c, v.x); visit(c + 1, v.y); visit(c + 2, v.z); visit(c + 3, v.w);
         }
       } else {
-        for (int c = lane; c < U; c += 32) visit(c, row[c]);
+        for (int c = s * 32 + lane; c < U; c += SW) visit(c, row[c]);
       }
     }
     TP(4);
     // first max of lp across the warp (ties -> lowest column)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float oa = __shfl_xor_sync(0xffffffffu, amax, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, acol, o);
-      if (oa > amax || (oa == amax && oc < acol)) {
-        amax = oa;
-        acol = oc;
-      }
+    warp_argmax(amax, acol);
+    if (lane == 0) {
+      sm.sav[i][s] = amax;
+      sm.sac[i][s] = acol;
     }
-    if (lane == 0) sm.arg[i] = acol;
-    if (!do_topk) {
-      if (lane == 0) {
-        const float x = row[fcol];
-        const float lp = lp_in ? x : (x - mx) - lse;
-        // forced steps: float32 key fl32(fl32(s) + lp) (NEP 50 promotion)
-        const float key32 = (float)s_r + lp;
-        sm.key[i][0] = (double)key32;
-        sm.lp[i][0] = lp;
-        sm.col[i][0] = fcol;
-        sm.cnt[i] = 1;
-      }
-    } else {
+    __syncwarp();
+    if (do_topk) {  // this warp's top kk, best first
       int cnt = 0;
       for (int j = 0; j < kk; ++j) {
-        double bk = tk[0];
-        int bc = tc[0], bl = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-          const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-          if (better(ok, oc, bk, bc) || (ok == bk && oc == bc && ol < bl)) {
-            bk = ok;
-            bc = oc;
-            bl = ol;
-          }
-        }
-        const float blp = __shfl_sync(0xffffffffu, tl[0], bl);
-        if (bc == INT_MAX) break;
-        if (lane == 0) {
-          sm.key[i][j] = bk;
-          sm.lp[i][j] = blp;
-          sm.col[i][j] = bc;
-        }
-        ++cnt;
+        const int bl = warp_best(tk[0], tc[0], tc[0] != INT_MAX);
+        if (bl < 0) break;
         if (lane == bl) {
+          sm.skey[i][s][j] = tk[0];
+          sm.slp[i][s][j] = tl[0];
+          sm.scol[i][s][j] = tc[0];
 #pragma unroll
           for (int q = 0; q + 1 < MAXK; ++q) {
             tk[q] = tk[q + 1];
@@ -392,43 +429,94 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
           tl[MAXK - 1] = -INFINITY;
           tc[MAXK - 1] = INT_MAX;
         }
+        ++cnt;
       }
-      if (lane == 0) sm.cnt[i] = cnt;
+      if (lane == 0) sm.scnt[i][s] = cnt;
     }
-    // factor choices of this row (search.py:261-272): prefix override at
-    // t - 1, else first-max of the factor logits
-    for (int k = 0; k < nf; ++k) {
-      int choice = -1;
-      if (t >= 1 && st.prefix_fac && t - 1 < st.P)
-        choice = st.prefix_fac[((size_t)b * nf + k) * st.P + t - 1];
-      if (choice < 0) {
-        const float *fr = st.fac_logits + (size_t)r * st.fac_ld;
-        const int lo = st.fac_off[k], hi = st.fac_off[k + 1];
-        float bm = -INFINITY;
-        int bcol = INT_MAX;
-        for (int c = lo + lane; c < hi; c += 32)
-          if (fr[c] > bm) {
-            bm = fr[c];
-            bcol = c - lo;
-          }
+    row_sync<SUB>(i);
+    if (s == 0) {
+      if (lane == 0) {  // first max over the warps, in column order
+        float ba = sm.sav[i][0];
+        int bcol = sm.sac[i][0];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float om = __shfl_xor_sync(0xffffffffu, bm, o);
-          const int oc = __shfl_xor_sync(0xffffffffu, bcol, o);
-          if (om > bm || (om == bm && oc < bcol)) {
-            bm = om;
-            bcol = oc;
+        for (int q = 1; q < SUB; ++q) {
+          const float a = sm.sav[i][q];
+          const int c = sm.sac[i][q];
+          if (a > ba || (a == ba && c < bcol)) {
+            ba = a;
+            bcol = c;
           }
         }
-        choice = bcol == INT_MAX ? 0 : bcol;
+        sm.arg[i] = bcol;
       }
-      if (lane == 0) st.fac_choice[(size_t)r * nf + k] = choice;
+      TP(8);
+      if (!do_topk) {
+        if (lane == 0) {
+          const float x = row[fcol];
+          const float lp = lp_in ? x : (x - mx) - lse;
+          // forced steps: float32 key fl32(fl32(s) + lp) (NEP 50 promotion)
+          const float key32 = (float)s_r + lp;
+          sm.key[i][0] = (double)key32;
+          sm.lp[i][0] = lp;
+          sm.col[i][0] = fcol;
+          sm.cnt[i] = 1;
+        }
+      } else {
+        // merge the SUB sorted warp lists (disjoint columns): kk rounds of a
+        // warp argmax over the list heads held by lanes 0..SUB-1
+        __syncwarp();  // reconverge after the lane-0 section (shuffles below)
+        const int my_cnt = lane < SUB ? sm.scnt[i][lane] : 0;
+        int head = 0, cnt = 0;
+        for (int j = 0; j < kk; ++j) {
+          const bool has = head < my_cnt;
+          const int bq = warp_best(has ? sm.skey[i][lane][head] : 0.0, has ? sm.scol[i][lane][head] : 0, has);
+          if (bq < 0) break;
+          if (lane == bq) {
+            sm.key[i][j] = sm.skey[i][lane][head];
+            sm.lp[i][j] = sm.slp[i][lane][head];
+            sm.col[i][j] = sm.scol[i][lane][head];
+            ++head;
+          }
+          ++cnt;
+        }
+        if (lane == 0) sm.cnt[i] = cnt;
+      }
+      TP(9);
+      // factor choices of this row (search.py:261-272): prefix override at
+      // t - 1, else first-max of the factor logits
+      for (int k = 0; k < nf; ++k) {
+        int choice = -1;
+        if (t >= 1 && st.prefix_fac && t - 1 < st.P)
+          choice = st.prefix_fac[((size_t)b * nf + k) * st.P + t - 1];
+        if (choice < 0) {
+          const float *fr = st.fac_logits + (size_t)r * st.fac_ld;
+          const int lo = st.fac_off[k], hi = st.fac_off[k + 1];
+          float bm = -INFINITY;
+          int bcol = INT_MAX;
+          for (int c = lo + lane; c < hi; c += 32)
+            if (fr[c] > bm) {
+              bm = fr[c];
+              bcol = c - lo;
+            }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, bm, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, bcol, o);
+            if (om > bm || (om == bm && oc < bcol)) {
+              bm = om;
+              bcol = oc;
+            }
+          }
+          choice = bcol == INT_MAX ? 0 : bcol;
+        }
+        if (lane == 0) st.fac_choice[(size_t)r * nf + k] = choice;
+      }
     }
   }
   TP(5);
   __syncthreads();
   TP(6);
-  if (i != 0) return;
+  if (w != 0) return;
 
   // ---- warp 0: merge the row lists.  K rounds of a warp argmax over the
   // row-list heads in the exact order (score desc, token asc, parent asc);
@@ -443,25 +531,9 @@ __global__ void __launch_bounds__(MAXK * 32) k_beam_step(const float *__restrict
   float pick_lp = 0.f;
   for (int sel = 0; sel < K; ++sel) {
     const bool has = lane < nalive && head < my_cnt;
-    double bk = has ? sm.key[lane][head] : 0.0;
-    int bc = has ? sm.col[lane][head] : 0;
-    int bq = lane;
-    bool bh = has;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-      const bool oh = __shfl_xor_sync(0xffffffffu, (int)bh, o) != 0;
-      const bool take = oh && (!bh || ok > bk || (ok == bk && (oc < bc || (oc == bc && oq < bq))));
-      if (take) {
-        bk = ok;
-        bc = oc;
-        bq = oq;
-        bh = true;
-      }
-    }
-    if (!bh) break;
+    const int bq = warp_best(has ? sm.key[lane][head] : 0.0, has ? sm.col[lane][head] : 0, has);
+    if (bq < 0) break;
+    const int bc = __shfl_sync(0xffffffffu, has ? sm.col[lane][head] : 0, bq);
     const float plp = __shfl_sync(0xffffffffu, has ? sm.lp[lane][head] : 0.f, bq);
     if (lane == sel) {
       pick_q = bq;
@@ -594,21 +666,22 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
       cudaFuncSetAttribute(kern_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(kern_ptr, sv.B, threads, smem, s, logits, ld_logits, lp_in, sv);
   };
-  const int th = sv.K * 32;
+  // SUB warps per beam row (<= 1024 threads, register budget of the
+  // per-lane MAXK lists)
   if (sv.K <= 1)
-    go(k_beam_step<1>, sizeof(BeamSmem<1>), th);
+    go(k_beam_step<1, 8>, sizeof(BeamSmem<1, 8>), sv.K * 32 * 8);
   else if (sv.K <= 2)
-    go(k_beam_step<2>, sizeof(BeamSmem<2>), th);
+    go(k_beam_step<2, 8>, sizeof(BeamSmem<2, 8>), sv.K * 32 * 8);
   else if (sv.K <= 4)
-    go(k_beam_step<4>, sizeof(BeamSmem<4>), th);
+    go(k_beam_step<4, 4>, sizeof(BeamSmem<4, 4>), sv.K * 32 * 4);
   else if (sv.K <= 5)
-    go(k_beam_step<5>, sizeof(BeamSmem<5>), th);
+    go(k_beam_step<5, SKB_BEAM_SUB5>, sizeof(BeamSmem<5, SKB_BEAM_SUB5>), sv.K * 32 * SKB_BEAM_SUB5);
   else if (sv.K <= 8)
-    go(k_beam_step<8>, sizeof(BeamSmem<8>), th);
+    go(k_beam_step<8, 2>, sizeof(BeamSmem<8, 2>), sv.K * 32 * 2);
   else if (sv.K <= 16)
-    go(k_beam_step<16>, sizeof(BeamSmem<16>), th);
+    go(k_beam_step<16, 1>, sizeof(BeamSmem<16, 1>), sv.K * 32);
   else
-    go(k_beam_step<32>, sizeof(BeamSmem<32>), th);
+    go(k_beam_step<32, 1>, sizeof(BeamSmem<32, 1>), sv.K * 32);
   SKB_CHECK_LAUNCH("k_beam_step");
   return SKB_OK;
 }

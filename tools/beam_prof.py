@@ -28,10 +28,15 @@ for rep in range(3):
     torch.cuda.synchronize()
 buf = (C.c_ulonglong * (4096 * 10))()
 print("rc", N.lib().skb_debug_beam_prof(buf))
-a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 10)[:640].astype(np.int64)
-t0 = a[:, 0].min()
-rel = (a - t0) / 1000.0
-for k in range(8):
-    col = rel[:, k][a[:, k] > 0]
-    if len(col):
-        print(f"phase {k}: n={len(col):4d} min={col.min():8.2f} med={np.median(col):8.2f} max={col.max():8.2f} us")
+A = np.frombuffer(buf, dtype=np.uint64).reshape(4, 1024, 10)[:, :640].astype(np.int64)
+t0 = A[0, :, 0].min()
+for sw in range(4):  # warp s of each row (SUB warps per row)
+    a = A[sw]
+    if not (a > 0).any():
+        continue
+    print(f"-- warp {sw} of each row")
+    rel = (a - t0) / 1000.0
+    for k in range(10):
+        col = rel[:, k][a[:, k] > 0]
+        if len(col):
+            print(f"phase {k}: n={len(col):4d} min={col.min():8.2f} med={np.median(col):8.2f} max={col.max():8.2f} us")
