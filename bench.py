@@ -237,6 +237,66 @@ def gemm_roofline(model, R, L, peak):
                          "tflops": round(out_flops / (ms_out / 1e3) / 1e12, 1)}}
 
 
+def topk_roofline(bb, hbm_peak, reps=20):
+    """k_beam_step (top-k + log-softmax finish + beam bookkeeping) at step 35
+    of the benchmark batch, launched back to back on its stream; achieved =
+    the algorithmic bytes R*A*4 (the fp32 logits it ranks) per
+    launch / average launch time.  The kernel itself reads only the output
+    GEMM's per-32-column (max, sum exp) partials and the candidate groups,
+    so its DRAM traffic is far below the algorithmic figure."""
+    import torch
+    from paper_2207_05851_b200 import kern
+    sb = bb.sb
+    sb.step.fill_(35)
+    R, U = bb.B * bb.K, sb.logits.shape[1]
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e9
+    for _ in range(3):
+        bb.done.zero_()
+        bb.n_alive.fill_(bb.K)
+        e0.record(st)
+        for _ in range(reps):
+            kern.beam_step(sb.logits, bb.state)
+        e1.record(st)
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / reps)
+    nbytes = R * U * 4
+    achieved = nbytes / (best / 1e3) / 1e9
+    return {"kernel": "k_beam_step (K=%d, R=%d, A=%d)" % (bb.K, R, U), "bound": "hbm",
+            "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "us_per_launch": round(best * 1e3, 2),
+            "algorithmic_bytes_per_launch": nbytes, "traffic": _beam_traffic()}
+
+
+def _beam_traffic():
+    """DRAM bytes per k_beam_step launch from the committed ncu capture
+    (profiles/r1_beam_step_traffic.json), or None."""
+    p = ROOT / "profiles" / "r1_beam_step_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"]}
+
+
+def ideal_floor(model, B, K, L, S, peak_tf_sustained, hbm):
+    """SURVEY.md 8d per-GPU floor: every GEMM FLOP at the sustained bf16 peak
+    plus the HBM terms (top-k logits, self-attention KV, cross K/V) at the
+    measured copy bandwidth, for one batch of B sentences over S steps."""
+    from paper_2207_05851_b200.config import decoder_step_cost, encoder_cost
+    c = model.config
+    d, D = c.d_model, c.decoder_layers
+    macs = encoder_cost(c, L) + D * 2 * L * d * d + sum(
+        (1 if t == 0 else K) * decoder_step_cost(c, t, L) for t in range(S))
+    flops = 2.0 * macs * B
+    R = B * K
+    hbm_bytes = sum(R * c.trg_vocab_size * 4 + D * 2 * R * (t + 1) * d * 2 + D * 2 * B * L * d * 2
+                    for t in range(S))
+    ms = flops / (peak_tf_sustained * 1e12) * 1e3 + hbm_bytes / (hbm * 1e9) * 1e3
+    return {"ms_per_batch": round(ms, 3), "sentences_per_s": round(B / (ms / 1e3), 1),
+            "gflop_per_sentence": round(flops / B / 1e9, 2), "hbm_gb_per_batch": round(hbm_bytes / 1e9, 2)}
+
+
 def step_breakdown(bb):
     """Eager replay of one mid-sequence decode step with CUDA events between
     kernel groups (attention, GEMMs, LN, beam) — explains `value`."""
@@ -424,6 +484,11 @@ def run_ours(args):
     roof = gemm_roofline(model, B * K, L, peak_tf)
     roof["peak_source"] = peak_src
     breakdown = step_breakdown(batches[-1])
+    hbm = peaks.get("hbm_gbs", 6466.1)
+    topk = topk_roofline(batches[-1], hbm)
+    topk["peak_source"] = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback"
+    floor = ideal_floor(model, B, K, L, 2 * L + 10, peaks.get("bf16_tflops_sustained", 1422.5), hbm)
+    floor["frac"] = round(value / world / floor["sentences_per_s"], 4)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
@@ -436,7 +501,8 @@ def run_ours(args):
                    "streams_per_gpu": n_streams, "batch_per_stream": B,
                    "value_single_stream": round(value_1, 2),
                    "l2": "working set > L2 (weights 0.48 GB + KV cache 1.1 GB per batch)"},
-        "e2e": e2e, "batch1_latency": lat, "roofline": roof, "gpu_launches": launches,
+        "e2e": e2e, "batch1_latency": lat, "roofline": roof, "roofline_topk": topk,
+        "floor": floor, "gpu_launches": launches,
         "clocks": clk,
         "decode": {"mean_steps_per_sentence": round(steps_per_sent, 2),
                    "forced_eos_sentences": forced, "step_breakdown_ms": breakdown},
