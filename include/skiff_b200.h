@@ -93,10 +93,25 @@ typedef struct skb_epilogue {
   void *ln_out;
   int ln_ldo;
   unsigned *ln_counter;
+  /* Optional LayerNorm of the GEMM input (kernels.py:298-324 feeding       */
+  /* kernels.py:479-484; model.py:562-581): when ln_in != NULL the GEMM      */
+  /* computes A[m] = LN(ln_in[m]) * ln_in_gain + ln_in_bias (eps ln_in_eps,  */
+  /* fp32 [M, ln_in_ld] -> bf16 A) first.  Small M: inside the GEMM (every   */
+  /* CTA normalises its activation rows into shared memory, A is not        */
+  /* written); otherwise a LayerNorm launch writes A, then the GEMM runs.   */
+  /* Bit-identical either way.  Not for RESID/SSRU (they update ln_in).     */
+  const float *ln_in;
+  int ln_in_ld;
+  const float *ln_in_gain;
+  const float *ln_in_bias;
+  float ln_in_eps;
 } skb_epilogue;
 
 /* Library identity / diagnostics */
 const char *skb_version(void);
+/* Kernels enqueued by the last skb_gemm / skb_gemm_simt call on this host  */
+/* thread (1, or 2 when a LayerNorm launch accompanied the GEMM).           */
+int skb_last_launches(void);
 const char *skb_last_error(void);
 /* 1 if the tcgen05 GEMM path is usable on the current device (sm_100). */
 int skb_tc_available(void);

@@ -33,7 +33,9 @@ class Epilogue(C.Structure):
                 ("lse_ld", i32), ("mask", vp), ("mask_words", i32), ("rows_per_group", i32),
                 ("splitk_ws", vp), ("splitk_ws_elems", C.c_longlong), ("splitk_counters", vp),
                 ("splitk_counters_n", i32), ("ln_gain", vp), ("ln_bias", vp),
-                ("ln_eps", C.c_float), ("ln_out", vp), ("ln_ldo", i32), ("ln_counter", vp)]
+                ("ln_eps", C.c_float), ("ln_out", vp), ("ln_ldo", i32), ("ln_counter", vp),
+                ("ln_in", vp), ("ln_in_ld", i32), ("ln_in_gain", vp), ("ln_in_bias", vp),
+                ("ln_in_eps", C.c_float)]
 
 
 class BeamState(C.Structure):
@@ -56,6 +58,7 @@ SIGNATURES = {
     "skb_version": [],
     "skb_last_error": [],
     "skb_tc_available": [],
+    "skb_last_launches": [],
     "skb_gemm": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
     "skb_gemm_simt": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
     "skb_gemm_force": [i32, i32, i32],

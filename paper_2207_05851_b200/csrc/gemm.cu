@@ -49,6 +49,12 @@ struct EpiArgs {
   __nv_bfloat16 *ln_out;
   int ln_ldo;
   unsigned *ln_counter;
+  // LayerNorm of the input rows computed in the swap-AB kernel's prologue
+  const float *lnx;
+  int lnx_ld;
+  const float *lnx_g;
+  const float *lnx_b;
+  float lnx_eps;
 };
 
 // Partial log-softmax statistics of `cnt` consecutive logits of row m
@@ -965,6 +971,47 @@ __device__ __forceinline__ void ln_row(const EpiArgs &e, int m, int d, int lane)
     }
 }
 
+// Prologue LayerNorm (kernels.py:298-324) of input row m into row rl of the
+// kernel's resident activation panel: K-major bf16, one [Na][64] SW128 tile
+// per 64-column k-block, i.e. exactly the bytes a TMA load of LN(x) would
+// have placed there.  Same arithmetic as ln_row / k_layernorm_reg (bitwise).
+__device__ __forceinline__ void ln_row_panel(const EpiArgs &e, int m, int rl, int d, int Na,
+                                             uint8_t *panel, int lane, const float4 (&g)[8],
+                                             const float4 (&bb)[8]) {
+  const int nv = d >> 7;
+  const float4 *xr = reinterpret_cast<const float4 *>(e.lnx + (size_t)m * e.lnx_ld);
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = i < nv ? __ldcg(xr + lane + 32 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float mu = warp_sum(s) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) {
+      const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, f = v[i].w - mu;
+      q += (a * a + b * b) + (c * c + f * f);
+    }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / (float)d + e.lnx_eps);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < nv) {
+      const int c4 = lane + 32 * i;
+      const float o0 = ((v[i].x - mu) * inv) * g[i].x + bb[i].x, o1 = ((v[i].y - mu) * inv) * g[i].y + bb[i].y;
+      const float o2 = ((v[i].z - mu) * inv) * g[i].z + bb[i].z, o3 = ((v[i].w - mu) * inv) * g[i].w + bb[i].w;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t *>(&p0);
+      w.y = *reinterpret_cast<uint32_t *>(&p1);
+      const int c = 4 * c4, cc = c & 63;
+      *reinterpret_cast<uint2 *>(panel + (size_t)(c >> 6) * Na * 128 + rl * 128 +
+                                 ((((cc >> 3) ^ (rl & 7))) << 4) + (cc & 7) * 2) = w;
+    }
+}
+
 // LOGITS epilogue (model.py:577-581, kernels.py:287-295): partial
 // log-softmax statistics (max, sum exp(x - max)) of every 32-column group of
 // the staged fp32 logit tile, over the row's active columns.  Eight lanes
@@ -1043,7 +1090,7 @@ __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int
 //   warps 2..5 : epilogue, TMEM lane quarter = warp % 4
 // grid (weight tiles x activation tiles, CS), cluster (1, CS): the CS CTAs
 // of a cluster share the output tile and split K.
-template <int KIND, int CS>
+template <int KIND, int CS, bool LNX = false>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_sw(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmO, int M, int N, int K, int Na, int stages,
@@ -1052,12 +1099,21 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  const int SB = W_BYTES + Na * 128;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + stages * SB);
+  // prologue-LayerNorm mode: the ring holds weight tiles only and the
+  // normalised activation rows sit in a resident panel [nk][Na][64] (SW128)
+  // (a separate instantiation: its registers would lower co-residency of
+  // the plain kernel)
+  constexpr bool lnx = LNX && CS == 1 && KIND != SKB_EPI_RESID && KIND != SKB_EPI_SSRU;
+  constexpr bool lnout = LNX && KIND == SKB_EPI_RESID;  // fused LayerNorm of the updated rows
+  const int SB = lnx ? W_BYTES : W_BYTES + Na * 128;
+  uint8_t *panel = smem + stages * SB;
+  const int panel_bytes = lnx ? ((K + BK - 1) / BK) * Na * 128 : 0;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + stages * SB + panel_bytes);
   uint64_t *empty = full + stages;
   uint64_t *tfull = empty + stages;
   uint64_t *rbar = tfull + 1;  // split-K: peers' partial slices landed
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + 1);
+  uint64_t *xready = rbar + 1;  // prologue LayerNorm: panel written
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CS > 1 ? (int)blockIdx.y : 0;
@@ -1079,6 +1135,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(rbar, 1);
+    mbar_init(xready, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
@@ -1106,7 +1163,7 @@ __global__ void __launch_bounds__(192, 1)
 #else
       constexpr int ldbg = 0;
 #endif
-      const int sbx = ldbg == 4 ? W_BYTES : (ldbg == 5 ? SB - W_BYTES : SB);
+      const int sbx = lnx ? W_BYTES : (ldbg == 4 ? W_BYTES : (ldbg == 5 ? SB - W_BYTES : SB));
 #pragma unroll 1
       for (int q = 0; q < pre; ++q) {
         mbar_expect_tx(&full[q], sbx);
@@ -1117,7 +1174,7 @@ __global__ void __launch_bounds__(192, 1)
       SW_STAMP(2);
 #pragma unroll 1
       for (int q = 0; q < pre; ++q)
-        if (ldbg != 4) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * BK, m0, &full[q]);
+        if (ldbg != 4 && !lnx) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * BK, m0, &full[q]);
 #pragma unroll 1
       for (int it = pre; it < nkc; ++it) {
         const int s = it % stages;
@@ -1126,7 +1183,7 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t *st = smem + s * SB;
         mbar_expect_tx(&full[s], sbx);
         if (ldbg != 5) tma_load_2d(st, &tmW, (kb0 + it) * BK, n0, &full[s]);
-        if (ldbg != 4) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * BK, m0, &full[s]);
+        if (ldbg != 4 && !lnx) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * BK, m0, &full[s]);
       }
     } else {
       pdl_wait();
@@ -1135,6 +1192,10 @@ __global__ void __launch_bounds__(192, 1)
     pdl_wait();
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(128, Na);
+      if (lnx) {
+        mbar_wait(xready, 0);
+        SW_STAMP(14);
+      }
 #pragma unroll 1
       for (int it = 0; it < nkc; ++it) {
         const int s = it % stages;
@@ -1143,7 +1204,7 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t *st = smem + s * SB;
         const uint64_t da = umma_desc_sw128(st);
-        const uint64_t db = umma_desc_sw128(st + W_BYTES);
+        const uint64_t db = umma_desc_sw128(lnx ? panel + (size_t)(kb0 + it) * Na * 128 : st + W_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (it > 0 || k > 0) ? 1u : 0u);
@@ -1159,7 +1220,34 @@ __global__ void __launch_bounds__(192, 1)
   const float *cprev = nullptr;
   float *cnext = nullptr;
   if (warp >= 2) {
-    pdl_wait();
+    if constexpr (lnx) {
+      // before the grid dependency: gain / bias (parameters) into registers,
+      // zero rows past M (they feed only output columns never stored)
+      float4 lg[8], lb[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < (K >> 7)) {
+          lg[i] = __ldg(reinterpret_cast<const float4 *>(ep.lnx_g) + lane + 32 * i);
+          lb[i] = __ldg(reinterpret_cast<const float4 *>(ep.lnx_b) + lane + 32 * i);
+        }
+#pragma unroll 1
+      for (int rl = warp - 2; rl < Na; rl += 4)
+        if (m0 + rl >= M)
+#pragma unroll 1
+          for (int c = lane; c < K / 8; c += 32)
+            *reinterpret_cast<uint4 *>(panel + (size_t)(c >> 3) * Na * 128 + rl * 128 + (c & 7) * 16) =
+                make_uint4(0u, 0u, 0u, 0u);
+      pdl_wait();
+      // normalise this tile's activation rows into the panel
+#pragma unroll 1
+      for (int rl = warp - 2; rl < Na && m0 + rl < M; rl += 4)
+        ln_row_panel(ep, m0 + rl, rl, K, Na, panel, lane, lg, lb);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(xready);
+      if (warp == 2 && lane == 0) SW_STAMP(13);
+    } else {
+      pdl_wait();
+    }
     if (KIND == SKB_EPI_SSRU) {
       cprev = ep.c_prev;
       cnext = ep.c_next;
@@ -1203,7 +1291,7 @@ __global__ void __launch_bounds__(192, 1)
           if (KIND == SKB_EPI_LOGITS && dbg != 3)
             logits_stats(ep, stg, M, N, m0, n0, Na, warp - 2, lane);
           if (warp == 3 && lane == 0) SW_STAMP(12);
-        }, KIND == SKB_EPI_RESID && ep.ln_out != nullptr);
+        }, lnout);
       }
     } else {
       // park the fp32 partial in my shared memory: part[m][128] (row-major
@@ -1282,7 +1370,7 @@ __global__ void __launch_bounds__(192, 1)
       if (warp == 2 && lane == 0) SW_STAMP(10);
       if (KIND != SKB_EPI_SSRU && tma_out)
         flush_tile<KIND>(&tmO, stg, n0, m0 + c0, warp == 2 && lane == 0, [] {},
-                         KIND == SKB_EPI_RESID && ep.ln_out != nullptr);
+                         lnout);
     }
     if (warp == 2 && lane == 0) SW_STAMP(4);
     cluster_sync_all();  // peers are done reading my shared memory
@@ -1293,7 +1381,7 @@ __global__ void __launch_bounds__(192, 1)
   // normalises all of the tile's rows (no CTA ever waits for another, so
   // the kernel cannot deadlock however few of its CTAs are resident).
   // Same arithmetic as the LN kernel.
-  if (KIND == SKB_EPI_RESID && ep.ln_out != nullptr && warp >= 2) {
+  if (lnout && warp >= 2) {
     volatile uint32_t &ln_last = tmem_slot[1];  // flag beside the TMEM address (dynamic smem)
     if (warp == 2 && lane == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1355,13 +1443,13 @@ static int make_map_out(CUtensorMap *out, const void *ptr, int rows, int cols, i
   return SKB_OK;
 }
 
-template <int KIND, int CS>
+template <int KIND, int CS, bool LNX = false>
 static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
                     const CUtensorMap &mo, int Na, int stages, int stg_off, int tma_out,
                     size_t smem, EpiArgs ep, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_sw<KIND, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaFuncSetAttribute(k_gemm_sw<KIND, CS, LNX>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     attr_set = true;
   }
   const int n_wt = (N + 127) / 128, n_at = (M + Na - 1) / Na;
@@ -1386,8 +1474,8 @@ static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMa
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS>, mw, mx, mo, M, N, K, Na, stages, stg_off, tma_out,
-                     ep);
+  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS, LNX>, mw, mx, mo, M, N, K, Na, stages, stg_off,
+                     tma_out, ep);
   SKB_CHECK_LAUNCH("k_gemm_sw");
   return SKB_OK;
 }
@@ -1396,6 +1484,16 @@ template <int KIND>
 static int launch_k2(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
                      const CUtensorMap &mo, int Na, int CS, int stages, int stg_off, int tma_out,
                      size_t smem, EpiArgs ep, cudaStream_t st) {
+  if constexpr (KIND == SKB_EPI_STORE || KIND == SKB_EPI_RELU)
+    if (ep.lnx) return launch_t<KIND, 1, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+  if constexpr (KIND == SKB_EPI_RESID)
+    if (ep.ln_out) {
+      if (CS == 4)
+        return launch_t<KIND, 4, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+      if (CS == 2)
+        return launch_t<KIND, 2, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+      return launch_t<KIND, 1, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+    }
   if (CS == 4)
     return launch_t<KIND, 4>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
   if (CS == 2)
@@ -1421,9 +1519,13 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   if (rc) return rc;
   rc = tc::make_map(&mx, X, M, K, ldx, Na);
   if (rc) return rc;
-  const int SB = W_BYTES + Na * 128;
+  const bool lnx = ep.lnx != nullptr;
+  if (lnx && (CS != 1 || K % 128 || K > 1024 || ep.kind == SKB_EPI_RESID || ep.kind == SKB_EPI_SSRU))
+    return fail(SKB_ERR_CONFIG, "gemm_sw: prologue LayerNorm needs CS=1, K %% 128 == 0 <= 1024");
+  const int SB = lnx ? W_BYTES : W_BYTES + Na * 128;
   const int nk = (K + tc::BK - 1) / tc::BK;
   const int nkc = (nk + CS - 1) / CS;
+  const int panel_bytes = lnx ? nk * Na * 128 : 0;
   // TMA-store epilogue: the output tile is staged in the (drained) ring
   const bool f32o = ep.kind == SKB_EPI_RESID || ep.out_dtype == SKB_F32;
   const int es = f32o ? 4 : 2;
@@ -1443,13 +1545,13 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
     budget = e ? atoi(e) : 113 * 1024;
     if (budget > SMEM_MAX) budget = SMEM_MAX;
   }
-  int stages = (budget - 1024 - 512) / SB;
+  int stages = (budget - 1024 - 512 - panel_bytes) / SB;
   if (stages < 2) stages = 2;
   if (stages > nkc) stages = nkc;
   if (stages * SB < need) stages = (need + SB - 1) / SB;
-  if (stages < 1 || stages * SB + 1024 + 512 > SMEM_MAX)
+  if (stages < 1 || stages * SB + panel_bytes + 1024 + 512 > SMEM_MAX)
     return fail(SKB_ERR_UNSUPPORTED, "gemm_sw: Na=%d CS=%d does not fit", Na, CS);
-  const size_t smem = (size_t)stages * SB + 1024 + 512;
+  const size_t smem = (size_t)stages * SB + panel_bytes + 1024 + 512;
   CUtensorMap mo;
   if (tma_out) {
     rc = make_map_out(&mo, ep.out, M, N, ep.ldo, f32o, rows_box);
@@ -1466,6 +1568,9 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
       return launch_k2<SKB_EPI_SSRU>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
     case SKB_EPI_LOGITS:
       if (CS != 1 || !tma_out) return fail(SKB_ERR_CONFIG, "gemm_sw: LOGITS needs CS=1 and TMA output");
+      if (ep.lnx)
+        return launch_t<SKB_EPI_LOGITS, 1, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep,
+                                                 st);
       return launch_t<SKB_EPI_LOGITS, 1>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
     default:
       return launch_k2<SKB_EPI_STORE>(M, N, K, mw, mx, mo, Na, CS, stages, stg_off, tma_out, smem, ep, st);
@@ -1514,6 +1619,18 @@ static int pick_na(int M, int N, int CS) {
     }
   }
   return best;
+}
+
+// Largest M whose input LayerNorm runs in the GEMM prologue (every CTA
+// normalises its own activation rows; beyond this the redundant row reads
+// cost more than the LayerNorm launch they save).  SKB_LN_PROLOGUE_MAX.
+static int lnx_max_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SKB_LN_PROLOGUE_MAX");
+    v = e ? atoi(e) : 32;
+  }
+  return v;
 }
 
 int g_mode = -1, g_na = 0, g_cs = 0;  // mode: 0 auto, 1 never, 2 always
@@ -1617,6 +1734,11 @@ static EpiArgs to_args(const skb_epilogue *e) {
   a.ln_ldo = e->ln_ldo;
   a.ln_counter = e->ln_counter;
   if (e->kind != SKB_EPI_RESID) a.ln_out = nullptr;
+  a.lnx = nullptr;  // set by gemm_impl when the prologue LayerNorm is used
+  a.lnx_ld = e->ln_in_ld;
+  a.lnx_g = e->ln_in_gain;
+  a.lnx_b = e->ln_in_bias;
+  a.lnx_eps = e->ln_in_eps;
   return a;
 }
 
@@ -1653,7 +1775,20 @@ using namespace skb;
 
 // A residual GEMM with a requested LayerNorm that did not run on the
 // swap-AB kernel (which fuses it) is followed by the LN kernel.
+static thread_local int g_last_launches = 0;
+
+// A = LN(ln_in) as its own launch (large M, SIMT and tc paths)
+static int ln_before(int in_dtype, int M, int K, const void *A, int lda, const skb_epilogue *epi,
+                     void *stream) {
+  ++g_last_launches;
+  return skb_layernorm(M, K, epi->ln_in, epi->ln_in_ld, epi->ln_in_gain, epi->ln_in_bias,
+                       epi->ln_in_eps, const_cast<void *>(A), lda, in_dtype, stream);
+}
+
+extern "C" int skb_last_launches(void) { return g_last_launches; }
+
 static int ln_after(int M, int N, const skb_epilogue *epi, void *stream) {
+  ++g_last_launches;
   return skb_layernorm(M, N, reinterpret_cast<const float *>(epi->out), epi->ldo, epi->ln_gain,
                        epi->ln_bias, epi->ln_eps, epi->ln_out, epi->ln_ldo, SKB_BF16, stream);
 }
@@ -1705,6 +1840,11 @@ extern "C" int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, i
   int rc = check_args(in_dtype, M, N, K, A, W, epi);
   if (rc) return rc;
   if (M == 0) return SKB_OK;
+  g_last_launches = 1;
+  if (epi->ln_in) {
+    rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
+    if (rc) return rc;
+  }
   rc = gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, to_args(epi), as_stream(stream));
   if (rc) return rc;
   if (epi->kind == SKB_EPI_RESID && epi->ln_out) return ln_after(M, N, epi, stream);
@@ -1717,6 +1857,7 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
 extern "C" int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
                         int ldw, const skb_epilogue *epi, void *stream) {
   bool fused = false;
+  g_last_launches = 1;
   const int rc = gemm_impl(in_dtype, M, N, K, A, lda, W, ldw, epi, stream, fused);
   if (rc || M == 0) return rc;
   if (epi->kind == SKB_EPI_RESID && epi->ln_out && !fused) return ln_after(M, N, epi, stream);
@@ -1733,7 +1874,13 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   const bool tma_ok = in_dtype == SKB_BF16 && K % 8 == 0 && lda % 8 == 0 && ldw % 8 == 0 &&
                       (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
                       (reinterpret_cast<uintptr_t>(W) & 15) == 0;
-  if (!tma_ok) return gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, ep, st);
+  if (!tma_ok) {
+    if (epi->ln_in) {
+      rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
+      if (rc) return rc;
+    }
+    return gemm_simt(in_dtype, M, N, K, A, lda, W, ldw, ep, st);
+  }
   // decode-sized M: swap-AB kernel (weights on the MMA M side)
   sw::init_mode();
   const bool logits_tma = epi->kind != SKB_EPI_LOGITS ||
@@ -1746,7 +1893,23 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
     const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);
     fused_ln = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr;
+    if (epi->ln_in) {
+      // input LayerNorm in the prologue while each CTA's share is small;
+      // else one LayerNorm launch writes A first (identical bits)
+      if (cs == 1 && M <= sw::lnx_max_rows() && K % 128 == 0 && K <= 1024 && epi->kind != SKB_EPI_RESID &&
+          epi->kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(epi->ln_in) & 15) == 0 &&
+          epi->ln_in_ld % 4 == 0) {
+        ep.lnx = epi->ln_in;
+      } else {
+        rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
+        if (rc) return rc;
+      }
+    }
     return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs);
+  }
+  if (epi->ln_in) {
+    rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
+    if (rc) return rc;
   }
   // Tile width BN and split-K factor S from a bytes-per-SM cost model: every
   // work unit streams (BM + BN) x K/S bf16 operands (plus an fp32 partial

@@ -97,38 +97,42 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
     D = len(model.dec)
 
     def resid(A, W, bias, site, ln):
-        """x += A.W^T (+bias); then h = LN(x) (fused into the GEMM when possible)."""
+        """x += A.W^T (+bias); with SKB_FUSE_LN the epilogue also writes h = LN(x)."""
         if fuse:
             kern.gemm(A, W, sb.x, N.EPI_RESID, bias, ln=ln, ln_out=sb.h, ln_counter=sb.ln_ctr[site])
         else:
             kern.gemm(A, W, sb.x, N.EPI_RESID, bias)
-            kern.layernorm(sb.x, *ln, sb.h)
+
+    def on_h(W, out, kind, bias, ln, h_ready, **kw):
+        """GEMM over h = LN(x) (model.py:562-581).  Unless the fused residual
+        epilogue already wrote h, the LayerNorm runs in the GEMM's prologue
+        (small batches) or as a launch right before it (identical bits)."""
+        kern.gemm(sb.h, W, out, kind, bias, ln_in=None if h_ready else (sb.x, *ln), **kw)
 
     for li, Ly in enumerate(model.dec):
         nxt = model.dec[li + 1].ln_self if li + 1 < D else model.ln_final
-        if li == 0:
-            kern.layernorm(sb.x, *Ly.ln_self, sb.h)
         if c.decoder_kind == SSRU:
+            if li == 0 or not fuse:  # the SSRU epilogue updates x: LN first
+                kern.layernorm(sb.x, *Ly.ln_self, sb.h)
             kern.gemm(sb.h, Ly.w_ssru, sb.x, N.EPI_SSRU, Ly.b_ssru, c_state=sb.cell[li],
                       src_row=sb.parent, step=sb.step, state_stride=R * d)
-            kern.layernorm(sb.x, *Ly.ln_cross, sb.h)
+            on_h(Ly.wq_c, sb.q, N.EPI_STORE, None, Ly.ln_cross, False)
         else:
-            kern.gemm(sb.h, Ly.wqkv, sb.qkv)
+            on_h(Ly.wqkv, sb.qkv, N.EPI_STORE, None, Ly.ln_self, fuse and li > 0)
             kern.self_attention_step(sb.qkv, sb.kc[li], sb.vc[li], sb.anc, sb.step, sb.ctx,
                                      R, H, dh, sb.S_max, sb.group)
             resid(sb.ctx, Ly.wo, None, 3 * li, Ly.ln_cross)
-        kern.gemm(sb.h, Ly.wq_c, sb.q)
+            on_h(Ly.wq_c, sb.q, N.EPI_STORE, None, Ly.ln_cross, fuse)
         kern.cross_attention_step(sb.q, sb.ckv, li * 2 * d, li * 2 * d + d, sb.L, sb.row_sent,
                                   sb.lengths, sb.ctx, R, H, dh, sb.group)
         resid(sb.ctx, Ly.wo_c, None, 3 * li + 1, Ly.ln_ffn)
-        kern.gemm(sb.h, Ly.w1, sb.f, N.EPI_RELU, Ly.b1)
+        on_h(Ly.w1, sb.f, N.EPI_RELU, Ly.b1, Ly.ln_ffn, fuse)
         resid(sb.f, Ly.w2, Ly.b2, 3 * li + 2, nxt)
-    if D == 0:
-        kern.layernorm(sb.x, *model.ln_final, sb.h)
-    kern.gemm(sb.h, sb.E_out, sb.logits, N.EPI_LOGITS, lse_part=sb.lse_part, mask=sb.mask,
-              rows_per_group=sb.group)
+    h_ready = fuse and D > 0
+    on_h(sb.E_out, sb.logits, N.EPI_LOGITS, None, model.ln_final, h_ready, lse_part=sb.lse_part,
+         mask=sb.mask, rows_per_group=sb.group)
     if nf:
-        kern.gemm(sb.h, model.w_fac, sb.fac, N.EPI_STORE, model.b_fac)
+        on_h(model.w_fac, sb.fac, N.EPI_STORE, model.b_fac, model.ln_final, h_ready)
 
 
 # ====================================================================== jobs

@@ -53,11 +53,13 @@ def dcode(t: torch.Tensor) -> int:
 
 def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_row=None,
          step=None, state_stride=0, lse_part=None, mask=None, rows_per_group=1, simt=False,
-         ln=None, ln_out=None, ln_counter=None, eps=1e-5):
+         ln=None, ln_out=None, ln_counter=None, eps=1e-5, ln_in=None):
     """out (or residual x) <- epilogue(A[M,K] . W[N,K]^T).  For RESID, ln =
     (gain, bias) with ln_out (bf16) and ln_counter also writes
     ln_out = LayerNorm(x) of the updated rows (fused on the swap-AB kernel,
-    else a LayerNorm launch follows)."""
+    else a LayerNorm launch follows).  ln_in = (x, gain, bias): the GEMM input
+    is A = LayerNorm(x) (kernels.py:298-324), computed in the GEMM's prologue
+    at small M (A is then not written) or by a LayerNorm launch into A."""
     M = A.shape[0] if M is None else M
     Nn, K = W.shape
     epi = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), out.stride(0), dcode(out), None,
@@ -70,9 +72,13 @@ def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_ro
         epi.ln_eps = eps
         epi.ln_out, epi.ln_ldo = ln_out.data_ptr(), ln_out.stride(0)
         epi.ln_counter = ln_counter.data_ptr()
+    if ln_in is not None:
+        x, g, b = ln_in
+        epi.ln_in, epi.ln_in_ld = x.data_ptr(), x.stride(0)
+        epi.ln_in_gain, epi.ln_in_bias, epi.ln_in_eps = g.data_ptr(), b.data_ptr(), eps
     N.call("skb_gemm_simt" if simt else "skb_gemm", dcode(A), M, Nn, K, A.data_ptr(),
            A.stride(0), W.data_ptr(), W.stride(0), C.byref(epi), stream())
-    _count()
+    _count(N.lib().skb_last_launches())
 
 
 def layernorm(x, gain, bias, out, rows=None, eps=1e-5):

@@ -318,3 +318,40 @@ def test_resid_fused_layernorm(gemm_path, M, Nn, K, cs):
         assert torch.equal(h, h_ref), (h.float() - h_ref.float()).abs().max().item()
         want = torch.nn.functional.layer_norm(x, (Nn,), gain, lb, eps=1e-5)
         assert (h.float() - want).abs().max().item() < 3e-2
+
+
+@pytest.mark.parametrize("M", [1, 5, 16, 17, 32, 33, 80])
+@pytest.mark.parametrize("kind,Nn,K", [(N.EPI_STORE, 3072, 1024), (N.EPI_RELU, 4096, 1024),
+                                       (N.EPI_LOGITS, 8000, 1024), (N.EPI_STORE, 512, 256)])
+def test_gemm_input_layernorm(gemm_path, M, kind, Nn, K):
+    """GEMM over A = LN(x) (ln_in, model.py:562-581): the LayerNorm inside the
+    swap-AB kernel's prologue (small M) or as a launch before the GEMM is
+    bitwise equal to the LayerNorm kernel followed by the plain GEMM."""
+    from paper_2207_05851_b200 import kern
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn)
+    x = torch.randn(M, K, device="cuda", generator=g) * 2 + 0.5
+    gain = torch.rand(K, device="cuda", generator=g) + 0.5
+    lb = torch.randn(K, device="cuda", generator=g)
+    W = (torch.randn(Nn, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g) if kind == N.EPI_RELU else None
+    f32 = kind == N.EPI_LOGITS
+    G = (Nn + 31) // 32
+    outs = []
+    for fused in (True, False):
+        h = torch.zeros(M, K, device="cuda", dtype=torch.bfloat16)
+        out = torch.zeros(M, Nn, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+        part = torch.zeros(M, 2 * G, device="cuda") if f32 else None
+        if fused:
+            kern.gemm(h, W, out, kind, bias, lse_part=part, ln_in=(x, gain, lb))
+        else:
+            kern.layernorm(x, gain, lb, h)
+            kern.gemm(h, W, out, kind, bias, lse_part=part)
+        torch.cuda.synchronize()
+        outs.append((out, part))
+    assert torch.equal(outs[0][0], outs[1][0]), (outs[0][0].float() - outs[1][0].float()).abs().max()
+    if f32:
+        assert torch.equal(outs[0][1], outs[1][1])
+    want = torch.nn.functional.layer_norm(x, (K,), gain, lb, eps=1e-5).bfloat16().float() @ W.float().T
+    if bias is not None:
+        want = torch.relu(want + bias)
+    assert (outs[0][0].float() - want).abs().max().item() < 5e-2 * (K / 256) ** 0.5

@@ -11,7 +11,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2207_05851_b200 import _native as N  # noqa: E402
 
-M = 640
+import os
+M = int(os.environ.get("M", "640"))
 shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024),
           "out_proj": (32000, 1024)}
 import os
@@ -40,6 +41,11 @@ for name, (Nn, K) in shapes.items():
         out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
         epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None,
                          0, None, 0, None, 0, 1, None, 0, None, 0)
+    if os.environ.get("LNIN"):  # input LayerNorm (prologue at small M)
+        xin = torch.randn(M, K, device="cuda")
+        gin, bin_ = torch.ones(K, device="cuda"), torch.zeros(K, device="cuda")
+        epi.ln_in, epi.ln_in_ld, epi.ln_in_gain, epi.ln_in_bias, epi.ln_in_eps = (
+            xin.data_ptr(), K, gin.data_ptr(), bin_.data_ptr(), 1e-5)
     for na, cs in cfgs:
         N.call("skb_gemm_force_sw", 2, na, cs)
         buf = (C.c_ulonglong * (1024 * 16))()
@@ -57,7 +63,7 @@ for name, (Nn, K) in shapes.items():
         cols = [0, 2, 3, 5, 1, 8, 9, 10, 4, 11, 12, 13, 14, 6]
         rel = (t[:, cols] - t0) / 1e3
         labels = ["entry", "postwait", "stage0", "accready", "epi/partial", "csync", "recv",
-                  "summed", "stored", "flushed", "stats", "ln_ticket", "ln_rows", "exit"]
+                  "summed", "stored", "flushed", "stats", "ln_ticket/ln_in_done", "ln_rows/mma_xready", "exit"]
         print(f"{name} na={na} cs={cs} ctas={len(t)} sms={len(set(t[:, 7]))}")
         for j, lab in enumerate(labels):
             col = rel[:, j]
