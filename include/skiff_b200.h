@@ -203,6 +203,24 @@ int skb_self_attention_step(int R, int H, int dh, const void *qkv, int ld_qkv, i
                             int ctx_dtype, void *stream);
 
 /*
+ * Step plan for the self-attention of all decoder layers (model.py:559-566
+ * reads the same per-row K/V history in every layer): for each group of
+ * rows_per_group rows (a sentence's beam) the distinct (slot, position)
+ * cache entries on the rows' ancestor paths at step *step, with a row mask
+ * per entry.  plan: caller-owned device buffer of skb_attn_plan_bytes().
+ */
+size_t skb_attn_plan_bytes(int R, int rows_per_group, int S_max);
+int skb_attn_plan(int R, int rows_per_group, int S_max, const int *anc, const int *step,
+                  void *plan, void *stream);
+/* skb_self_attention_step over a step plan instead of the ancestor table   */
+/* (bitwise equal); bf16, d_h = 64, rows_per_group <= 16, else             */
+/* SKB_ERR_UNSUPPORTED.                                                     */
+int skb_self_attention_step_planned(int R, int H, int dh, const void *qkv, int ld_qkv,
+                                    int qkv_dtype, void *kc, void *vc, int cache_dtype, int S_max,
+                                    const void *plan, const int *step, int rows_per_group,
+                                    void *ctx, int ldc, int ctx_dtype, void *stream);
+
+/*
  * Cross-attention for one step (model.py:568-573): q [R, ldq]; row r reads
  * sentence row_sent[r] of the per-sentence encoder K/V memory
  * kv [B*L, ld_kv] (K at column offset koff, V at voff), masked past

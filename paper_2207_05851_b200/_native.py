@@ -68,6 +68,10 @@ SIGNATURES = {
     "skb_embed_target": [i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp],
     "skb_embed_source": [i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],
     "skb_encoder_attention": [i32, i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp],
+    "skb_attn_plan_bytes": [i32, i32, i32],
+    "skb_attn_plan": [i32, i32, i32, vp, vp, vp, vp],
+    "skb_self_attention_step_planned": [i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp, vp, i32,
+                                        vp, i32, i32, vp],
     "skb_self_attention_step": [i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp, vp, i32, vp,
                                 i32, i32, vp],
     "skb_cross_attention_step": [i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, i32, i32, vp,
@@ -103,7 +107,8 @@ def lib():
             except AttributeError:
                 continue  # reported as missing by tests/test_native_lib.py
             fn.argtypes = args
-            fn.restype = C.c_char_p if name in ("skb_version", "skb_last_error") else C.c_int
+            fn.restype = (C.c_char_p if name in ("skb_version", "skb_last_error")
+                          else C.c_size_t if name == "skb_attn_plan_bytes" else C.c_int)
         _lib = L
     return _lib
 

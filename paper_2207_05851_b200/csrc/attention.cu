@@ -1048,11 +1048,34 @@ __device__ unsigned long long g_attn_trace[4096 * 8];
   } while (0)
 #endif
 
-template <int DH, int HG, int GW>
+// Step plan (skb_attn_plan): the walk below depends only on the ancestor
+// table and t — the same for all layers and head groups — so it can be done
+// once per step.  Per sentence: E, then [EMAX] slot-or-(-1-row) sources,
+// positions and row masks (bit i: entry on row i's path), in the walk's
+// entry order (so planned and unplanned attention are bitwise equal).
+struct AttnPlanView {
+  const int *E;           // [nb]
+  const short *src;       // [nb][EMAX]
+  const short *pos;       // [nb][EMAX]
+  const unsigned short *mask;  // [nb][EMAX]
+};
+__host__ __device__ inline size_t attn_plan_off(int nb, int emax, int which) {
+  const size_t e = ((size_t)nb * 4 + 15) & ~size_t(15);
+  return e + (size_t)which * nb * emax * 2;
+}
+__device__ __forceinline__ AttnPlanView plan_view(const void *plan, int nb, int emax) {
+  const uint8_t *b = reinterpret_cast<const uint8_t *>(plan);
+  return {reinterpret_cast<const int *>(b), reinterpret_cast<const short *>(b + attn_plan_off(nb, emax, 0)),
+          reinterpret_cast<const short *>(b + attn_plan_off(nb, emax, 1)),
+          reinterpret_cast<const unsigned short *>(b + attn_plan_off(nb, emax, 2))};
+}
+
+template <int DH, int HG, int GW, bool PLAN = false>
 __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
     int R, int H, int G, const __nv_bfloat16 *__restrict__ qkv, int ld_qkv,
     __nv_bfloat16 *kc, __nv_bfloat16 *vc, int S_max, const int *__restrict__ anc,
-    const int *__restrict__ step, float scale, __nv_bfloat16 *__restrict__ ctx, int ldc, int cap) {
+    const int *__restrict__ step, float scale, __nv_bfloat16 *__restrict__ ctx, int ldc, int cap,
+    const void *__restrict__ plan = nullptr) {
   constexpr int RUN = HG * DH * 2;       // bytes of one entry's K (or V) for the CTA's heads
   constexpr int EP = RUN + 16;           // padded entry pitch in shared memory
   extern __shared__ __align__(128) uint8_t sm_tc[];
@@ -1101,66 +1124,82 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
                    : "memory");
     }
   };
-  // ---- walk, sweep 1: one 32-position block per warp (one position per
-  // lane): ancestor slots of the G rows, distinct slots per position (first
-  // row wins), block-local scan
-  for (int blk = warp; blk < nblk; blk += HG) {
-    const int p = blk * 32 + lane;
-    const bool valid = p <= t;
-    int sl[GW], loc[GW];
-#pragma unroll
-    for (int i = 0; i < GW; ++i) {
-      sl[i] = -2;
-      if (i < nr && valid) sl[i] = p == t ? -1 - (r0 + i) : __ldg(arow + (size_t)(r0 + i) * S_max + p);
+  unsigned short *emask = reinterpret_cast<unsigned short *>(ek);  // PLAN: [EMAX] row masks
+  int E;
+  if constexpr (PLAN) {
+    const int nb = (R + G - 1) / G, emax = G * S_max;
+    const AttnPlanView pv = plan_view(plan, nb, emax);
+    E = __ldg(pv.E + blockIdx.x);
+    const size_t o = (size_t)blockIdx.x * emax;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      esrc[e] = __ldg(pv.src + o + e);
+      epos[e] = __ldg(pv.pos + o + e);
+      emask[e] = __ldg(pv.mask + o + e);
     }
-    int u = 0;
-#pragma unroll
-    for (int i = 0; i < GW; ++i) {
-      int w = -1;
-#pragma unroll
-      for (int j = 0; j < i; ++j)
-        if (w < 0 && sl[j] == sl[i]) w = loc[j];
-      if (w < 0 && i < nr) {
-        w = u++;
-        if (valid) pent[p * GW + w] = (short)sl[i];
+    __syncthreads();
+  } else {
+    // ---- walk, sweep 1: one 32-position block per warp (one position per
+    // lane): ancestor slots of the G rows, distinct slots per position (first
+    // row wins), block-local scan
+    for (int blk = warp; blk < nblk; blk += HG) {
+      const int p = blk * 32 + lane;
+      const bool valid = p <= t;
+      int sl[GW], loc[GW];
+  #pragma unroll
+      for (int i = 0; i < GW; ++i) {
+        sl[i] = -2;
+        if (i < nr && valid) sl[i] = p == t ? -1 - (r0 + i) : __ldg(arow + (size_t)(r0 + i) * S_max + p);
       }
-      loc[i] = w < 0 ? 0 : w;
-      if (i < nr && valid) ploc[i * S_max + p] = (unsigned char)loc[i];
+      int u = 0;
+  #pragma unroll
+      for (int i = 0; i < GW; ++i) {
+        int w = -1;
+  #pragma unroll
+        for (int j = 0; j < i; ++j)
+          if (w < 0 && sl[j] == sl[i]) w = loc[j];
+        if (w < 0 && i < nr) {
+          w = u++;
+          if (valid) pent[p * GW + w] = (short)sl[i];
+        }
+        loc[i] = w < 0 ? 0 : w;
+        if (i < nr && valid) ploc[i * S_max + p] = (unsigned char)loc[i];
+      }
+      if (!valid) u = 0;
+      int incl = u;
+  #pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int nn = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += nn;
+      }
+      if (valid) {
+        pcnt[p] = (unsigned char)u;
+        pexcl[p] = (short)(incl - u);
+      }
+      if (lane == 31) bstart[blk + 1] = incl;
     }
-    if (!valid) u = 0;
-    int incl = u;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int nn = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += nn;
+    AT_STAMP(7);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bstart[0] = 0;
+      for (int b = 1; b <= nblk; ++b) bstart[b] += bstart[b - 1];
     }
-    if (valid) {
-      pcnt[p] = (unsigned char)u;
-      pexcl[p] = (short)(incl - u);
+    __syncthreads();
+    // ---- sweep 2: the entry list in position order; ekey = (position, local
+    // index) decides on-path membership later: entry e is on row i's path iff
+    // ploc[i][p(e)] == k(e)
+    for (int p = threadIdx.x; p <= t; p += blockDim.x) {
+      const int e0 = bstart[p >> 5] + pexcl[p];
+      const int u = pcnt[p];
+      for (int k = 0; k < u; ++k) {
+        esrc[e0 + k] = pent[p * GW + k];
+        epos[e0 + k] = (short)p;
+        ek[e0 + k] = (unsigned char)k;
+      }
     }
-    if (lane == 31) bstart[blk + 1] = incl;
+    __syncthreads();
+    E = bstart[nblk];
   }
-  AT_STAMP(7);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    bstart[0] = 0;
-    for (int b = 1; b <= nblk; ++b) bstart[b] += bstart[b - 1];
-  }
-  __syncthreads();
-  // ---- sweep 2: the entry list in position order; ekey = (position, local
-  // index) decides on-path membership later: entry e is on row i's path iff
-  // ploc[i][p(e)] == k(e)
-  for (int p = threadIdx.x; p <= t; p += blockDim.x) {
-    const int e0 = bstart[p >> 5] + pexcl[p];
-    const int u = pcnt[p];
-    for (int k = 0; k < u; ++k) {
-      esrc[e0 + k] = pent[p * GW + k];
-      epos[e0 + k] = (short)p;
-      ek[e0 + k] = (unsigned char)k;
-    }
-  }
-  __syncthreads();
-  const int E = bstart[nblk];
+
   // first pass: every warp copies every HG-th entry
   for (int e = warp; e < min(E, cap); e += HG) stage(e, esrc[e], epos[e]);
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1246,9 +1285,15 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
         const int ej = nt * 8 + tq * 2 + e;
         bool oka = false, okb = false;
         if (ej < n) {
-          const int pe = epos[eb + ej], ke = ek[eb + ej];
-          oka = rva && pla[pe] == ke;
-          okb = rvb && plb[pe] == ke;
+          if constexpr (PLAN) {
+            const unsigned mk = emask[eb + ej];
+            oka = rva && ((mk >> gq) & 1u);
+            okb = rvb && ((mk >> (gq + 8)) & 1u);
+          } else {
+            const int pe = epos[eb + ej], ke = ek[eb + ej];
+            oka = rva && pla[pe] == ke;
+            okb = rvb && plb[pe] == ke;
+          }
         }
         sc[nt][e] = oka ? sc[nt][e] * scale : -INFINITY;
         sc[nt][2 + e] = okb ? sc[nt][2 + e] * scale : -INFINITY;
@@ -1347,6 +1392,113 @@ static size_t self_tc_smem(int dh, int hg, int gw, int G, int S_max, int cap) {
   return (b + 127) & ~(size_t)127;
 }
 
+// ---- step plan (one CTA per sentence): the walk of k_self_attn_tc once per
+// step, with per-entry row masks; written to global memory for all layers.
+template <int GW>
+__global__ void __launch_bounds__(128) k_attn_plan(int R, int G, int S_max, const int *__restrict__ anc,
+                                                    const int *__restrict__ step, void *plan) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) uint8_t sm_pl[];
+  short *pent = reinterpret_cast<short *>(sm_pl);                      // [S_max][GW]
+  unsigned short *pmask = reinterpret_cast<unsigned short *>(pent + S_max * GW);  // [S_max][GW]
+  short *pexcl = reinterpret_cast<short *>(pmask + S_max * GW);        // [S_max]
+  int *bstart = reinterpret_cast<int *>(
+      (reinterpret_cast<uintptr_t>(pexcl + S_max) + 3) & ~uintptr_t(3));  // [nblk + 1]
+  unsigned char *pcnt = reinterpret_cast<unsigned char *>(bstart + (S_max + 31) / 32 + 2);  // [S_max]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x, r0 = b * G, nr = min(G, R - r0);
+  const int nb = (R + G - 1) / G, emax = G * S_max;
+  const int t = *step;
+  const int nblk = (t + 32) / 32;
+  const int *arow = anc + (size_t)(t & 1) * R * S_max;
+  for (int blk = warp; blk < nblk; blk += 4) {
+    const int p = blk * 32 + lane;
+    const bool valid = p <= t;
+    int sl[GW], loc[GW];
+#pragma unroll
+    for (int i = 0; i < GW; ++i) {
+      sl[i] = -2;
+      if (i < nr && valid) sl[i] = p == t ? -1 - (r0 + i) : __ldg(arow + (size_t)(r0 + i) * S_max + p);
+    }
+    int u = 0;
+#pragma unroll
+    for (int i = 0; i < GW; ++i) {
+      int w = -1;
+#pragma unroll
+      for (int j = 0; j < i; ++j)
+        if (w < 0 && sl[j] == sl[i]) w = loc[j];
+      if (w < 0 && i < nr) {
+        w = u++;
+        if (valid) {
+          pent[p * GW + w] = (short)sl[i];
+          pmask[p * GW + w] = 0;
+        }
+      }
+      loc[i] = w < 0 ? 0 : w;
+      if (i < nr && valid) pmask[p * GW + loc[i]] |= (unsigned short)(1u << i);
+    }
+    if (!valid) u = 0;
+    int incl = u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int nn = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += nn;
+    }
+    if (valid) {
+      pcnt[p] = (unsigned char)u;
+      pexcl[p] = (short)(incl - u);
+    }
+    if (lane == 31) bstart[blk + 1] = incl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bstart[0] = 0;
+    for (int q = 1; q <= nblk; ++q) bstart[q] += bstart[q - 1];
+  }
+  __syncthreads();
+  uint8_t *pb = reinterpret_cast<uint8_t *>(plan);
+  short *gsrc = reinterpret_cast<short *>(pb + attn_plan_off(nb, emax, 0)) + (size_t)b * emax;
+  short *gpos = reinterpret_cast<short *>(pb + attn_plan_off(nb, emax, 1)) + (size_t)b * emax;
+  unsigned short *gmask = reinterpret_cast<unsigned short *>(pb + attn_plan_off(nb, emax, 2)) + (size_t)b * emax;
+  for (int p = threadIdx.x; p <= t; p += blockDim.x) {
+    const int e0 = bstart[p >> 5] + pexcl[p];
+    const int u = pcnt[p];
+    for (int k = 0; k < u; ++k) {
+      gsrc[e0 + k] = pent[p * GW + k];
+      gpos[e0 + k] = (short)p;
+      gmask[e0 + k] = pmask[p * GW + k];
+    }
+  }
+  if (threadIdx.x == 0) reinterpret_cast<int *>(pb)[b] = bstart[nblk];
+}
+
+static size_t attn_plan_smem(int gw, int S_max) {
+  return (size_t)S_max * gw * 4 + (size_t)S_max * 2 + 4 + ((size_t)(S_max + 31) / 32 + 2) * 4 + S_max + 16;
+}
+
+extern "C" size_t skb_attn_plan_bytes(int R, int rows_per_group, int S_max) {
+  if (R <= 0 || rows_per_group <= 0 || S_max <= 0) return 0;
+  const int nb = (R + rows_per_group - 1) / rows_per_group;
+  return attn_plan_off(nb, rows_per_group * S_max, 3);
+}
+
+extern "C" int skb_attn_plan(int R, int rows_per_group, int S_max, const int *anc, const int *step,
+                             void *plan, void *stream) {
+  if (R <= 0 || rows_per_group < 1 || rows_per_group > 16 || S_max <= 0 || S_max > 32767)
+    return fail(SKB_ERR_SHAPE, "attn_plan: R=%d G=%d S_max=%d", R, rows_per_group, S_max);
+  if (attn_plan_smem(rows_per_group <= 8 ? 8 : 16, S_max) > 48 * 1024)
+    return fail(SKB_ERR_UNSUPPORTED, "attn_plan: S_max=%d too long", S_max);
+  const int nb = (R + rows_per_group - 1) / rows_per_group;
+  if (rows_per_group <= 8)
+    launch_k(k_attn_plan<8>, nb, 128, attn_plan_smem(8, S_max), as_stream(stream), R, rows_per_group,
+             S_max, anc, step, plan);
+  else
+    launch_k(k_attn_plan<16>, nb, 128, attn_plan_smem(16, S_max), as_stream(stream), R, rows_per_group,
+             S_max, anc, step, plan);
+  SKB_CHECK_LAUNCH("k_attn_plan");
+  return SKB_OK;
+}
+
 extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qkv, int ld_qkv,
                                      int qkv_dtype, const int *lengths, void *ctx, int ldc,
                                      int ctx_dtype, void *stream) {
@@ -1383,6 +1535,89 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
   return SKB_OK;
 }
 
+// Tensor-core self-attention launch (k_self_attn_tc); -1 if the shape or
+// dtypes do not fit it.  plan != nullptr selects the planned variant.
+static int launch_self_tc(int R, int H, int dh, const void *qkv, int ld_qkv, int qkv_dtype, void *kc,
+                          void *vc, int S_max, const int *anc, const int *step, int G2, void *ctx,
+                          int ldc, int ctx_dtype, const void *plan, void *stream) {
+  static int tc_mode = -1, tc_cap = 0, tc_hg = 0;
+  if (tc_mode < 0) {
+    const char *e = getenv("SKB_ATTN_TC");
+    tc_mode = e ? atoi(e) : 1;
+    e = getenv("SKB_ATTN_CAP");
+    tc_cap = e ? atoi(e) : 48;
+    if (tc_cap > 64) tc_cap = 64;  // one pass = at most 8 mma n-tiles
+    if (tc_cap < 16) tc_cap = 16;
+    e = getenv("SKB_ATTN_HG");
+    tc_hg = e ? atoi(e) : 4;
+  }
+  int hg = tc_hg;
+  while (hg > 1 && H % hg) hg >>= 1;
+  if (!(tc_mode && G2 >= 1 && G2 <= 16 && qkv_dtype == SKB_BF16 && ctx_dtype == SKB_BF16 && dh == 64 &&
+        ldc % 2 == 0 && ld_qkv % 8 == 0 && (hg == 2 || hg == 4 || hg == 8) &&
+        (reinterpret_cast<uintptr_t>(qkv) & 15) == 0 && (reinterpret_cast<uintptr_t>(kc) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(vc) & 15) == 0))
+    return -1;
+  const int gw = G2 <= 8 ? 8 : 16;
+  const size_t smem = self_tc_smem(64, hg, gw, G2, S_max, tc_cap);
+  dim3 g((R + G2 - 1) / G2, H / hg);
+  auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
+  auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
+  const float sc = attn_scale(dh);
+  auto go = [&](auto kern_fn) {
+    // per-kernel opt-in shared memory size (all instantiations share the
+    // function-pointer type, so key by address)
+    static std::mutex mu;
+    static std::unordered_map<const void *, size_t> set;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      size_t &cur = set[reinterpret_cast<const void *>(kern_fn)];
+      if (smem > cur) {
+        cudaFuncSetAttribute(kern_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cur = smem;
+      }
+    }
+    launch_k(kern_fn, g, 32 * hg, smem, as_stream(stream), R, H, G2,
+             reinterpret_cast<const __nv_bfloat16 *>(qkv), ld_qkv, k, v, S_max, anc, step, sc,
+             reinterpret_cast<__nv_bfloat16 *>(ctx), ldc, tc_cap, plan);
+  };
+  if (plan) {
+    if (gw == 16) {
+      if (hg == 8) go(k_self_attn_tc<64, 8, 16, true>);
+      else if (hg == 2) go(k_self_attn_tc<64, 2, 16, true>);
+      else go(k_self_attn_tc<64, 4, 16, true>);
+    } else {
+      if (hg == 8) go(k_self_attn_tc<64, 8, 8, true>);
+      else if (hg == 2) go(k_self_attn_tc<64, 2, 8, true>);
+      else go(k_self_attn_tc<64, 4, 8, true>);
+    }
+  } else if (gw == 16) {
+    if (hg == 8) go(k_self_attn_tc<64, 8, 16>);
+    else if (hg == 2) go(k_self_attn_tc<64, 2, 16>);
+    else go(k_self_attn_tc<64, 4, 16>);
+  } else {
+    if (hg == 8) go(k_self_attn_tc<64, 8, 8>);
+    else if (hg == 2) go(k_self_attn_tc<64, 2, 8>);
+    else go(k_self_attn_tc<64, 4, 8>);
+  }
+  SKB_CHECK_LAUNCH("k_self_attn_tc");
+  return 0;
+}
+
+extern "C" int skb_self_attention_step_planned(int R, int H, int dh, const void *qkv, int ld_qkv,
+                                               int qkv_dtype, void *kc, void *vc, int cache_dtype,
+                                               int S_max, const void *plan, const int *step,
+                                               int rows_per_group, void *ctx, int ldc, int ctx_dtype,
+                                               void *stream) {
+  if (R < 0 || H <= 0 || dh <= 0 || !plan) return fail(SKB_ERR_SHAPE, "self_attention_step_planned: shape");
+  if (R == 0) return SKB_OK;
+  if (cache_dtype != SKB_BF16 ||
+      launch_self_tc(R, H, dh, qkv, ld_qkv, qkv_dtype, kc, vc, S_max, nullptr, step, rows_per_group, ctx,
+                     ldc, ctx_dtype, plan, stream) != 0)
+    return fail(SKB_ERR_UNSUPPORTED, "self_attention_step_planned: needs the bf16 tensor-core path (d_h 64)");
+  return SKB_OK;
+}
+
 extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, int ld_qkv,
                                        int qkv_dtype, void *kc, void *vc, int cache_dtype, int S_max,
                                        const int *anc, const int *step, int rows_per_group,
@@ -1398,54 +1633,9 @@ extern "C" int skb_self_attention_step(int R, int H, int dh, const void *qkv, in
     auto *k = reinterpret_cast<__nv_bfloat16 *>(kc);
     auto *v = reinterpret_cast<__nv_bfloat16 *>(vc);
     const float sc = attn_scale(dh);
-    static int tc_mode = -1, tc_cap = 0, tc_hg = 0;
-    if (tc_mode < 0) {
-      const char *e = getenv("SKB_ATTN_TC");
-      tc_mode = e ? atoi(e) : 1;
-      e = getenv("SKB_ATTN_CAP");
-      tc_cap = e ? atoi(e) : 48;
-      if (tc_cap > 64) tc_cap = 64;  // one pass = at most 8 mma n-tiles
-      if (tc_cap < 16) tc_cap = 16;
-      e = getenv("SKB_ATTN_HG");
-      tc_hg = e ? atoi(e) : 4;
-    }
-    const int G2 = rows_per_group;
-    int hg = tc_hg;
-    while (hg > 1 && H % hg) hg >>= 1;
-    if (tc_mode && G2 >= 1 && G2 <= 16 && qkv_dtype == SKB_BF16 && ctx_dtype == SKB_BF16 &&
-        dh == 64 && ldc % 2 == 0 && ld_qkv % 8 == 0 && (hg == 2 || hg == 4 || hg == 8)) {
-      const int gw = G2 <= 8 ? 8 : 16;
-      const size_t smem = self_tc_smem(64, hg, gw, G2, S_max, tc_cap);
-      dim3 g((R + G2 - 1) / G2, H / hg);
-      auto go = [&](auto kern_fn) {
-        // per-kernel opt-in shared memory size (all instantiations share the
-        // function-pointer type, so key by address)
-        static std::mutex mu;
-        static std::unordered_map<const void *, size_t> set;
-        {
-          std::lock_guard<std::mutex> lk(mu);
-          size_t &cur = set[reinterpret_cast<const void *>(kern_fn)];
-          if (smem > cur) {
-            cudaFuncSetAttribute(kern_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cur = smem;
-          }
-        }
-        launch_k(kern_fn, g, 32 * hg, smem, as_stream(stream), R, H, G2,
-                 reinterpret_cast<const __nv_bfloat16 *>(qkv), ld_qkv, k, v, S_max, anc, step, sc,
-                 reinterpret_cast<__nv_bfloat16 *>(ctx), ldc, tc_cap);
-      };
-      if (gw == 16) {
-        if (hg == 8) go(k_self_attn_tc<64, 8, 16>);
-        else if (hg == 2) go(k_self_attn_tc<64, 2, 16>);
-        else go(k_self_attn_tc<64, 4, 16>);
-      } else {
-        if (hg == 8) go(k_self_attn_tc<64, 8, 8>);
-        else if (hg == 2) go(k_self_attn_tc<64, 2, 8>);
-        else go(k_self_attn_tc<64, 4, 8>);
-      }
-      SKB_CHECK_LAUNCH("k_self_attn_tc");
+    if (launch_self_tc(R, H, dh, qkv, ld_qkv, qkv_dtype, kc, vc, S_max, anc, step, rows_per_group, ctx,
+                       ldc, ctx_dtype, nullptr, stream) == 0)
       return SKB_OK;
-    }
     if (dh == 64)
       launch_k(k_self_attn_vec<64, 8>, grid, 32 * G, 0, as_stream(stream), R, H, qkv, ld_qkv,
                qkv_dtype, k, v, S_max, anc, step, sc, ctx, ldc, ctx_dtype);

@@ -83,6 +83,13 @@ class StepBuffers:
         self.fuse_ln = (cdt == torch.bfloat16 and d % 128 == 0 and d <= 1024 and D > 0
                         and os.environ.get("SKB_FUSE_LN", "0") == "1")
         self.ln_ctr = torch.zeros(3 * max(D, 1), (R + 15) // 16 + 1, dtype=I32, device=dev)
+        # per-step self-attention plan (skb_attn_plan), allocated on the first
+        # (eager) step once the group size is known
+        self.plan = None
+        self.plan_key = None
+        self.use_plan = (c.decoder_kind != SSRU and cdt == torch.bfloat16 and c.head_dim == 64
+                         and os.environ.get("SKB_ATTN_PLAN", "1") != "0"
+                         and os.environ.get("SKB_ATTN_TC", "1") != "0")
 
 
 def step_forward(model: Model, sb: StepBuffers) -> None:
@@ -109,6 +116,15 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
         (small batches) or as a launch right before it (identical bits)."""
         kern.gemm(sb.h, W, out, kind, bias, ln_in=None if h_ready else (sb.x, *ln), **kw)
 
+    plan = None
+    if sb.use_plan and D > 0 and 1 <= sb.group <= 16:
+        key = (R, sb.group, sb.S_max)
+        if sb.plan_key != key:
+            sb.plan = torch.empty(kern.attn_plan_bytes(R, sb.group, sb.S_max), dtype=torch.uint8,
+                                  device=sb.x.device)
+            sb.plan_key = key
+        kern.attn_plan(sb.anc, sb.step, sb.plan, R, sb.S_max, sb.group)
+        plan = sb.plan
     for li, Ly in enumerate(model.dec):
         nxt = model.dec[li + 1].ln_self if li + 1 < D else model.ln_final
         if c.decoder_kind == SSRU:
@@ -120,7 +136,7 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
         else:
             on_h(Ly.wqkv, sb.qkv, N.EPI_STORE, None, Ly.ln_self, fuse and li > 0)
             kern.self_attention_step(sb.qkv, sb.kc[li], sb.vc[li], sb.anc, sb.step, sb.ctx,
-                                     R, H, dh, sb.S_max, sb.group)
+                                     R, H, dh, sb.S_max, sb.group, plan=plan)
             resid(sb.ctx, Ly.wo, None, 3 * li, Ly.ln_cross)
             on_h(Ly.wq_c, sb.q, N.EPI_STORE, None, Ly.ln_cross, fuse)
         kern.cross_attention_step(sb.q, sb.ckv, li * 2 * d, li * 2 * d + d, sb.L, sb.row_sent,

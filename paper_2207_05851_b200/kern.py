@@ -113,10 +113,28 @@ def encoder_attention(qkv, lengths, ctx, B, L, H, dh):
     _count()
 
 
-def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max, group=1):
-    N.call("skb_self_attention_step", R, H, dh, qkv.data_ptr(), qkv.stride(0), dcode(qkv),
-           kc.data_ptr(), vc.data_ptr(), dcode(kc), S_max, anc.data_ptr(), step.data_ptr(),
-           group, ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max, group=1, plan=None):
+    """plan (from attn_plan) replaces the per-layer ancestor walk."""
+    if plan is not None:
+        N.call("skb_self_attention_step_planned", R, H, dh, qkv.data_ptr(), qkv.stride(0),
+               dcode(qkv), kc.data_ptr(), vc.data_ptr(), dcode(kc), S_max, plan.data_ptr(),
+               step.data_ptr(), group, ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+    else:
+        N.call("skb_self_attention_step", R, H, dh, qkv.data_ptr(), qkv.stride(0), dcode(qkv),
+               kc.data_ptr(), vc.data_ptr(), dcode(kc), S_max, anc.data_ptr(), step.data_ptr(),
+               group, ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+    _count()
+
+
+def attn_plan_bytes(R, group, S_max):
+    return int(N.lib().skb_attn_plan_bytes(R, group, S_max))
+
+
+def attn_plan(anc, step, plan, R, S_max, group):
+    """Per-step self-attention plan (distinct cache entries + row masks per
+    sentence), shared by every decoder layer."""
+    N.call("skb_attn_plan", R, group, S_max, anc.data_ptr(), step.data_ptr(), plan.data_ptr(),
+           stream())
     _count()
 
 

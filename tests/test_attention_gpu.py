@@ -71,6 +71,45 @@ def test_self_attention_grouped_matches_reference(G, t, dh, H, tree):
     assert torch.equal(vc[:, t].reshape(R, D), qkv[:, 2 * D:])
 
 
+@pytest.mark.parametrize("G,t,H", [(5, 0, 16), (5, 35, 16), (5, 69, 16), (1, 40, 8), (8, 79, 8),
+                                   (16, 63, 4), (3, 31, 4), (2, 32, 4)])
+@pytest.mark.parametrize("tree", [False, True])
+def test_self_attention_planned_bitwise(G, t, H, tree):
+    """One skb_attn_plan per step replaces every layer's ancestor walk: the
+    planned kernel stages the same entries in the same order, so its output
+    is bitwise equal to the unplanned one (and the cache write identical)."""
+    dh = 64
+    g = torch.Generator(device="cuda").manual_seed(t * 7 + G + H)
+    B, S = 7, 80
+    R, D = B * G, H * dh
+    qkv = torch.randn(R, 3 * D, device="cuda", generator=g).bfloat16()
+    kc0 = torch.randn(R, S, H, dh, device="cuda", generator=g).bfloat16()
+    vc0 = torch.randn(R, S, H, dh, device="cuda", generator=g).bfloat16()
+    anc = torch.zeros(2, R, S, dtype=torch.int32, device="cuda")
+    grp = torch.arange(R, device="cuda") // G
+    if tree:
+        hist = torch.arange(R, device="cuda")[:, None].repeat(1, S)
+        for p in range(1, S):
+            par = grp * G + torch.randint(0, max(1, G // 2), (R,), device="cuda", generator=g)
+            hist[:, :p] = hist[par, :p]
+        anc[t & 1] = hist.int()
+    else:
+        anc[t & 1] = (grp[:, None] * G + torch.randint(0, G, (R, S), device="cuda", generator=g)).int()
+    step = torch.tensor([t], dtype=torch.int32, device="cuda")
+    plan = torch.zeros(kern.attn_plan_bytes(R, G, S), dtype=torch.uint8, device="cuda")
+    kern.attn_plan(anc, step, plan, R, S, G)
+    outs = []
+    for use_plan in (False, True):
+        kc, vc = kc0.clone(), vc0.clone()
+        ctx = torch.zeros(R, D, device="cuda", dtype=torch.bfloat16)
+        kern.self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S, group=G,
+                                 plan=plan if use_plan else None)
+        torch.cuda.synchronize()
+        outs.append((ctx, kc, vc))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
+
+
 @pytest.mark.parametrize("G,L", [(5, 30), (1, 17), (4, 90)])
 def test_cross_attention_matches_reference(G, L):
     g = torch.Generator(device="cuda").manual_seed(L)
