@@ -801,12 +801,14 @@ __global__ void __launch_bounds__(32 * HG) k_cross_tc(
   constexpr int EP = RUN + 16;      // padded shared row pitch
   constexpr int CH = RUN / 16;      // 16-byte chunks per row
   extern __shared__ __align__(128) uint8_t sm_x[];
-  PDL_ENTRY();
+  // The encoder memory (kv), row_sent and lengths were written before the
+  // decode loop (long-completed grids): read them through L2 and stage K/V
+  // before griddepcontrol.wait; only q comes from the preceding kernel.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * G, nr = min(G, R - r0);
   const int h0 = blockIdx.y * HG;
-  const int b = row_sent ? row_sent[r0] : blockIdx.x;
-  const int len = lengths[b];
+  const int b = row_sent ? __ldcg(row_sent + r0) : blockIdx.x;
+  const int len = __ldcg(lengths + b);
   const int Lp = (L + 31) & ~31;
   uint8_t *Ks = sm_x;
   uint8_t *Vs = sm_x + (size_t)Lp * EP;
@@ -828,6 +830,7 @@ __global__ void __launch_bounds__(32 * HG) k_cross_tc(
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  PDL_ENTRY();
   // Q fragments of my head while the copies fly
   const int h = h0 + warp;
   const int gq = lane >> 2, tq = lane & 3;
@@ -1092,12 +1095,17 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
   short *pexcl = reinterpret_cast<short *>(
       (reinterpret_cast<uintptr_t>(pcnt + S_max) + 1) & ~uintptr_t(1));  // [S_max]
   AT_STAMP(0);
-  PDL_ENTRY();
+  // PLAN: the plan (written this step by k_attn_plan, which completed before
+  // the preceding GEMM passed its own grid-dependency wait) and the cached
+  // K/V of earlier positions do not depend on the preceding kernel, so they
+  // are read (through L2) and staged before griddepcontrol.wait; only this
+  // step's q/k/v rows wait for it.
+  if constexpr (!PLAN) PDL_ENTRY();
   AT_STAMP(1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * G, nr = min(G, R - r0);
   const int h0 = blockIdx.y * HG;
-  const int t = *step, D = H * DH;
+  const int t = __ldcg(step), D = H * DH;
   const int nblk = (t + 32) / 32;
   const int *arow = anc + (size_t)(t & 1) * R * S_max;
   const uint32_t ks_s = static_cast<uint32_t>(__cvta_generic_to_shared(Ks));
@@ -1129,14 +1137,20 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
   if constexpr (PLAN) {
     const int nb = (R + G - 1) / G, emax = G * S_max;
     const AttnPlanView pv = plan_view(plan, nb, emax);
-    E = __ldg(pv.E + blockIdx.x);
+    E = __ldcg(pv.E + blockIdx.x);
     const size_t o = (size_t)blockIdx.x * emax;
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-      esrc[e] = __ldg(pv.src + o + e);
-      epos[e] = __ldg(pv.pos + o + e);
-      emask[e] = __ldg(pv.mask + o + e);
+      esrc[e] = __ldcg(pv.src + o + e);
+      epos[e] = __ldcg(pv.pos + o + e);
+      emask[e] = __ldcg(pv.mask + o + e);
     }
     __syncthreads();
+    // first pass, cached entries (earlier steps) before the dependency wait
+    for (int e = warp; e < min(E, cap); e += HG)
+      if (esrc[e] >= 0) stage(e, esrc[e], epos[e]);
+    PDL_ENTRY();
+    for (int e = warp; e < min(E, cap); e += HG)
+      if (esrc[e] < 0) stage(e, esrc[e], epos[e]);
   } else {
     // ---- walk, sweep 1: one 32-position block per warp (one position per
     // lane): ancestor slots of the G rows, distinct slots per position (first
@@ -1201,7 +1215,8 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
   }
 
   // first pass: every warp copies every HG-th entry
-  for (int e = warp; e < min(E, cap); e += HG) stage(e, esrc[e], epos[e]);
+  if constexpr (!PLAN)
+    for (int e = warp; e < min(E, cap); e += HG) stage(e, esrc[e], epos[e]);
   asm volatile("cp.async.commit_group;" ::: "memory");
   AT_STAMP(2);
   // this step's k/v of my heads, for slot (row, t): loaded now (overlapping
