@@ -1412,7 +1412,10 @@ static size_t self_tc_smem(int dh, int hg, int gw, int G, int S_max, int cap) {
 template <int GW>
 __global__ void __launch_bounds__(128) k_attn_plan(int R, int G, int S_max, const int *__restrict__ anc,
                                                     const int *__restrict__ step, void *plan) {
-  PDL_ENTRY();
+  // Reads only the ancestor table and step (written by the reorder / step
+  // advance, which completed before the preceding embedding kernel passed
+  // its grid-dependency wait): no wait here; the consumers wait on this grid.
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t sm_pl[];
   short *pent = reinterpret_cast<short *>(sm_pl);                      // [S_max][GW]
   unsigned short *pmask = reinterpret_cast<unsigned short *>(pent + S_max * GW);  // [S_max][GW]
@@ -1423,7 +1426,7 @@ __global__ void __launch_bounds__(128) k_attn_plan(int R, int G, int S_max, cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x, r0 = b * G, nr = min(G, R - r0);
   const int nb = (R + G - 1) / G, emax = G * S_max;
-  const int t = *step;
+  const int t = __ldcg(step);
   const int nblk = (t + 32) / 32;
   const int *arow = anc + (size_t)(t & 1) * R * S_max;
   for (int blk = warp; blk < nblk; blk += 4) {
@@ -1433,7 +1436,7 @@ __global__ void __launch_bounds__(128) k_attn_plan(int R, int G, int S_max, cons
 #pragma unroll
     for (int i = 0; i < GW; ++i) {
       sl[i] = -2;
-      if (i < nr && valid) sl[i] = p == t ? -1 - (r0 + i) : __ldg(arow + (size_t)(r0 + i) * S_max + p);
+      if (i < nr && valid) sl[i] = p == t ? -1 - (r0 + i) : __ldcg(arow + (size_t)(r0 + i) * S_max + p);
     }
     int u = 0;
 #pragma unroll

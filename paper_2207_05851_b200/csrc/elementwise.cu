@@ -76,9 +76,16 @@ __global__ void __launch_bounds__(256) k_layernorm_reg(int rows, const float *__
                                                        int ldx, const float *__restrict__ gain,
                                                        const float *__restrict__ bias, float eps,
                                                        void *out, int ldo, int out_dtype) {
-  PDL_ENTRY();
   constexpr int d = NV * 128;
   const int warp = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  // gain / bias are parameters: loaded before the grid-dependency wait
+  float4 g[NV], bb[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    g[i] = __ldg(reinterpret_cast<const float4 *>(gain) + lane + 32 * i);
+    bb[i] = __ldg(reinterpret_cast<const float4 *>(bias) + lane + 32 * i);
+  }
+  PDL_ENTRY();
   if (warp >= rows) return;
   const float4 *xr = reinterpret_cast<const float4 *>(x + (size_t)warp * ldx);
   float4 v[NV];
@@ -95,14 +102,11 @@ __global__ void __launch_bounds__(256) k_layernorm_reg(int rows, const float *__
     q += (a * a + b * b) + (e * e + f * f);
   }
   const float inv = 1.0f / sqrtf(warp_sum(q) / (float)d + eps);
-  const float4 *g4 = reinterpret_cast<const float4 *>(gain);
-  const float4 *b4 = reinterpret_cast<const float4 *>(bias);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c4 = lane + 32 * i;
-    const float4 g = __ldg(g4 + c4), bb = __ldg(b4 + c4);
-    const float o0 = ((v[i].x - mu) * inv) * g.x + bb.x, o1 = ((v[i].y - mu) * inv) * g.y + bb.y;
-    const float o2 = ((v[i].z - mu) * inv) * g.z + bb.z, o3 = ((v[i].w - mu) * inv) * g.w + bb.w;
+    const float o0 = ((v[i].x - mu) * inv) * g[i].x + bb[i].x, o1 = ((v[i].y - mu) * inv) * g[i].y + bb[i].y;
+    const float o2 = ((v[i].z - mu) * inv) * g[i].z + bb[i].z, o3 = ((v[i].w - mu) * inv) * g[i].w + bb[i].w;
     if (out_dtype == SKB_F32) {
       reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + (size_t)warp * ldo)[c4] =
           make_float4(o0, o1, o2, o3);

@@ -195,7 +195,6 @@ __device__ __forceinline__ void row_sync(int row) {
 template <int MAXK, int SUB>
 __global__ void __launch_bounds__(MAXK * 32 * SUB)
     k_beam_step(const float *__restrict__ logits, int ld, int lp_in, skb_beam_state st) {
-  PDL_ENTRY();
   extern __shared__ __align__(16) uint8_t beam_smem[];
   using Smem = BeamSmem<MAXK, SUB>;
   Smem &sm = *reinterpret_cast<Smem *>(beam_smem);
@@ -207,16 +206,21 @@ __global__ void __launch_bounds__(MAXK * 32 * SUB)
   const int R = st.B * K;
   const int b = blockIdx.x;
   const int r = b * K + i;
-  const int t = *st.step;
+  // The search state (step, done, alive count, scores; prefix tables) was
+  // last written by this kernel / the step advance of the previous step,
+  // grids long completed: read it through L2 before the grid-dependency
+  // wait, which only the logits (preceding output GEMM) need.
+  const int t = __ldcg(st.step);
   const int nf = st.n_factors;
   const int G = (U + 31) >> 5;
   TP(0);
-  // independent state loads issued together (one round trip)
-  const int done = st.done[b];
-  const int nalive = st.n_alive[b];
-  const int plen = st.prefix_len[b];
-  const int mlen = st.max_len[b];
+  const int done = __ldcg(st.done + b);
+  const int nalive = __ldcg(st.n_alive + b);
+  const int plen = __ldcg(st.prefix_len + b);
+  const int mlen = __ldcg(st.max_len + b);
+  const double s_row = i < nalive ? __ldcg(st.score + b * K + i) : 0.0;
   if (done) return;
+  PDL_ENTRY();
   const bool final_force = (t == mlen - 1) && (t >= plen);
   const int fcol = t < plen ? st.prefix_col[(size_t)b * st.P + t] : (final_force ? st.eos_col : -1);
 
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(MAXK * 32 * SUB)
     const bool do_topk = fcol < 0;
     const bool need_argmax = final_force;
     const int kk = K < MAXK ? K : MAXK;
-    const double s_r = st.score[r];
+    const double s_r = s_row;
     const bool use_part = !lp_in && st.lse_part != nullptr;
     const bool staged = use_part && st.stage_partials;
     const float2 *gpart = use_part ? reinterpret_cast<const float2 *>(st.lse_part) + (size_t)r * st.lse_ld
