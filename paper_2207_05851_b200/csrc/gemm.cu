@@ -1584,6 +1584,16 @@ static int pick_cs(int N, int K) {
   const int nk = (K + tc::BK - 1) / tc::BK;
   const int n_wt = (N + 127) / 128;
   if (nk >= 48 && n_wt <= 16) return 4;
+  // SKB_CS_SMALLN=2|4 also splits the narrow K = 1024 shapes (wo, wo_c):
+  // still a function of (N, K) only, a latency / throughput trade-off —
+  // measured on B200: 4 gives batch-1 greedy 21.4 ms (from 23.5) but costs
+  // 16 % of the multi-stream throughput (cluster reduction at M = 640).
+  static int small_n = -1;
+  if (small_n < 0) {
+    const char *e = getenv("SKB_CS_SMALLN");
+    small_n = e ? atoi(e) : 1;
+  }
+  if (small_n > 1 && n_wt <= 8 && nk >= 16) return small_n;
   return 1;
 }
 
