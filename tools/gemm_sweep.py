@@ -18,6 +18,9 @@ from paper_2207_05851_b200 import _native as N  # noqa: E402
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 640
 SHAPES = {"qkv": (3072, 1024), "wo": (1024, 1024), "ffn1": (4096, 1024), "ffn2": (1024, 4096),
           "out_proj": (32000, 1024)}
+import os
+if os.environ.get("SHAPES"):
+    SHAPES = {k: SHAPES[k] for k in os.environ["SHAPES"].split(",")}
 REPS = 24
 dev = "cuda"
 ws = torch.empty(32 << 20, device=dev)
@@ -74,7 +77,7 @@ for name, (Nn, K) in SHAPES.items():
     print(json.dumps(out_rows[-1]), flush=True)
     cfgs = [("tc auto", 1, 0, 0), ("sw auto", 2, 0, 0)]
     for na in (32, 48, 64, 80, 96, 128, 160, 256):
-        for cs in ((1, 4) if K >= 4096 else (1,)):
+        for cs in ((1, 2, 4) if K >= 4096 else (1,)):
             if cs > 1 and na % (4 * cs):
                 continue
             cfgs.append((f"sw na{na} cs{cs}", 2, na, cs))
