@@ -450,15 +450,28 @@ def run_ours(args):
     if not args.no_e2e:
         settings = SearchSettings(beam=K, length_alpha=args.alpha)
         host_inputs = [[SentenceInput(tokens=s) for s in sents(500 + s)] for s in range(args.steps)]
-        translate(model, vocabs, host_inputs[0][:8], settings)
+        # warm-up through the same API (kernels, descriptors); the timed call
+        # still creates its batch-shape workspaces and captures their graphs
+        # (SKB_E2E_WARM_BATCHES=n pre-warms n full batches instead)
+        from paper_2207_05851_b200 import engine as _eng
+        _eng.DECODE_STREAMS = n_streams
+        nw = int(os.environ.get("SKB_E2E_WARM_BATCHES", "0"))
+        warm = [SentenceInput(tokens=s) for w in range(nw) for s in sents(900 + w)] or \
+            [SentenceInput(tokens=s) for s in sents(900)[:8]]
+        translate(model, vocabs, warm, settings, max_rows=B * K)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        # one translate() call per n_streams batches: decode_jobs runs its
-        # 128-sentence batches concurrently on n_streams streams
+        # translate() over all the step batches' sentences at once (the way a
+        # caller hands the reference its input list): decode_jobs splits them
+        # into 128-sentence batches and keeps n_streams of them in flight,
+        # preparing the next batch on the host while the GPU decodes.
+        # SKB_E2E_CALL_SENTS=n splits the input into calls of n sentences.
         from paper_2207_05851_b200 import engine as _eng
         _eng.DECODE_STREAMS = n_streams
-        groups = [sum(host_inputs[g:g + n_streams], []) for g in range(0, len(host_inputs), n_streams)]
+        flat = sum(host_inputs, [])
+        per_call = int(os.environ.get("SKB_E2E_CALL_SENTS", "0")) or len(flat)
+        groups = [flat[g:g + per_call] for g in range(0, len(flat), per_call)]
         e0.record()
         for inp in groups:
             recs = translate(model, vocabs, inp, settings, max_rows=B * K)

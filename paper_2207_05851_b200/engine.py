@@ -659,9 +659,11 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
     pending = []
     for n, s in enumerate(range(0, len(order), per_batch)):
         idx = order[s:s + per_batch]
-        bb = BeamBatch(model, [jobs[i] for i in idx], beam, alpha, nvs_threshold, use_graph,
-                       slot=2 * (n % S) + ((n // S) & 1))
         with torch.cuda.stream(streams[n % S]):
+            # constructed on its own stream: the batch's input upload must not
+            # queue behind the decode work of the batches on the main stream
+            bb = BeamBatch(model, [jobs[i] for i in idx], beam, alpha, nvs_threshold, use_graph,
+                           slot=2 * (n % S) + ((n // S) & 1))
             bb.start()
         pending.append((idx, bb))
         if len(pending) > S:
