@@ -37,9 +37,14 @@ import os
 for t in [int(x) for x in os.environ.get('TS', '10,35,60').split(',')]:
     step = torch.tensor([t], dtype=torch.int32, device=dev)
 
+    plan = None
+    if os.environ.get("PLAN", "1") == "1":  # the engine's path: one step plan for all layers
+        plan = torch.empty(kern.attn_plan_bytes(R, K, S), dtype=torch.uint8, device=dev)
+        kern.attn_plan(anc, step, plan, R, S, K)
+
     def run():
         for kc, vc in caches:
-            kern.self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S, group=K)
+            kern.self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S, group=K, plan=plan)
     run()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
