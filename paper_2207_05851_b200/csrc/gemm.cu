@@ -1899,7 +1899,14 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   if (ln_fused && (!epi->ln_gain || !epi->ln_bias || !epi->ln_counter || N % 128 || N > 1024 ||
                    epi->ln_ldo % 4))
     return fail(SKB_ERR_CONFIG, "gemm: fused LayerNorm needs gain/bias/counter, N %% 128 == 0 <= 1024");
-  if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || M <= 1024)) {
+  // Swap-AB kernel unless M is large and K long (measured on B200,
+  // tools/tcsw_check.py: it beats the M-major kernel 1.3-2x up to M = 3840
+  // except the K = 4096 residual GEMM beyond ~2.5k rows).  LOGITS always
+  // takes it: the two kernels' GEMM results are bitwise equal, but their
+  // log-softmax partials are reduced in different orders, so one kernel for
+  // every M keeps a sentence's scores independent of its batch.
+  const bool sw_pref = epi->kind == SKB_EPI_LOGITS || M <= 2560 || K < 4096;
+  if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || sw_pref)) {
     const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);
     fused_ln = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr;

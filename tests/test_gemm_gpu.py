@@ -355,3 +355,25 @@ def test_gemm_input_layernorm(gemm_path, M, kind, Nn, K):
     if bias is not None:
         want = torch.relu(want + bias)
     assert (outs[0][0].float() - want).abs().max().item() < 5e-2 * (K / 256) ** 0.5
+
+
+def test_logits_partials_batch_invariant_default_dispatch(gemm_path):
+    """With the library's own kernel choice, a row's logits and log-softmax
+    partials do not depend on how many rows share the call (5 rows vs 1100
+    rows: different kernels would reduce the partials in different orders)."""
+    from paper_2207_05851_b200 import kern
+    N.call("skb_gemm_force_sw", 0, 0, 0)  # default dispatch for this test
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, Nn, K = 1100, 8000, 1024
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(Nn, K, device="cuda", generator=g) * 0.05).bfloat16()
+    G = (Nn + 31) // 32
+    res = []
+    for rows in (A, A[700:705]):
+        o = torch.zeros(rows.shape[0], Nn, device="cuda")
+        part = torch.zeros(rows.shape[0], 2 * G, device="cuda")
+        kern.gemm(rows, W, o, N.EPI_LOGITS, lse_part=part)
+        torch.cuda.synchronize()
+        res.append((o, part))
+    assert torch.equal(res[0][0][700:705], res[1][0])
+    assert torch.equal(res[0][1][700:705], res[1][1])
