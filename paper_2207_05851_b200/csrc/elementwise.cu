@@ -137,6 +137,31 @@ __global__ void k_embed_target(int rows, int d, const int *__restrict__ tok,
   x[(size_t)r * d + c] = v;
 }
 
+// Vectorised variant (d % 4 == 0, 16-byte aligned tables): one warp per row
+// quarter-chunk, float4 per thread; several rows per CTA.
+__global__ void __launch_bounds__(256) k_embed_target4(int rows, int d, const int *__restrict__ tok,
+                                                       const float *__restrict__ E,
+                                                       const float *__restrict__ pe,
+                                                       const int *__restrict__ step, int n_factors,
+                                                       const int *__restrict__ ftok,
+                                                       const float *const *__restrict__ ftables,
+                                                       float *__restrict__ x) {
+  PDL_ENTRY();
+  const int d4 = d >> 2;
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)rows * d4) return;
+  const int r = (int)(i / d4), c4 = (int)(i - (long)r * d4);
+  const int t = *step;
+  float4 v = reinterpret_cast<const float4 *>(E + (size_t)tok[r] * d)[c4];
+  const float4 p = reinterpret_cast<const float4 *>(pe + (size_t)t * d)[c4];
+  v.x = v.x + p.x; v.y = v.y + p.y; v.z = v.z + p.z; v.w = v.w + p.w;
+  for (int k = 0; k < n_factors; ++k) {
+    const float4 f = reinterpret_cast<const float4 *>(ftables[k] + (size_t)ftok[k * rows + r] * d)[c4];
+    v.x = v.x + f.x; v.y = v.y + f.y; v.z = v.z + f.z; v.w = v.w + f.w;
+  }
+  reinterpret_cast<float4 *>(x + (size_t)r * d)[c4] = v;
+}
+
 // ----------------------------------------------------- source embedding
 struct SrcFactors {
   int n;
@@ -236,6 +261,16 @@ extern "C" int skb_embed_target(int rows, int d, const int *tok, const float *E,
                                 const float *const *ftables, float *x, void *stream) {
   if (rows < 0 || d <= 0) return fail(SKB_ERR_SHAPE, "embed_target: rows=%d d=%d", rows, d);
   if (rows == 0) return SKB_OK;
+  // (factor tables: device allocations with d-float rows, aligned like E)
+  const bool vec = d % 4 == 0 && ((reinterpret_cast<uintptr_t>(E) | reinterpret_cast<uintptr_t>(pe) |
+                                   reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  if (vec) {
+    const long n4 = (long)rows * (d / 4);
+    launch_k(k_embed_target4, (unsigned)((n4 + 255) / 256), 256, 0, as_stream(stream), rows, d, tok, E,
+             pe, step, n_factors, ftok, ftables, x);
+    SKB_CHECK_LAUNCH("k_embed_target4");
+    return SKB_OK;
+  }
   dim3 grid((d + 255) / 256, rows);
   launch_k(k_embed_target, grid, 256, 0, as_stream(stream), rows, d, tok, E, pe, step, n_factors, ftok,
                                                       ftables, x);
