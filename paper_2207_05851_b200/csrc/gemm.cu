@@ -1920,7 +1920,8 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
     if (epi->ln_in) {
       // input LayerNorm in the prologue while each CTA's share is small;
       // else one LayerNorm launch writes A first (identical bits)
-      if (cs == 1 && M <= sw::lnx_max_rows() && K % 128 == 0 && K <= 1024 && epi->kind != SKB_EPI_RESID &&
+      if (cs == 1 && M <= sw::lnx_max_rows() && (long)na * K * 2 <= 64 * 1024 && K % 128 == 0 &&
+          K <= 1024 && epi->kind != SKB_EPI_RESID &&
           epi->kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(epi->ln_in) & 15) == 0 &&
           epi->ln_in_ld % 4 == 0) {
         ep.lnx = epi->ln_in;
