@@ -1906,13 +1906,16 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   if (ln_fused && (!epi->ln_gain || !epi->ln_bias || !epi->ln_counter || N % 128 || N > 1024 ||
                    epi->ln_ldo % 4))
     return fail(SKB_ERR_CONFIG, "gemm: fused LayerNorm needs gain/bias/counter, N %% 128 == 0 <= 1024");
-  // Swap-AB kernel unless M is large and K long (measured on B200,
-  // tools/tcsw_check.py: it beats the M-major kernel 1.3-2x up to M = 3840
-  // except the K = 4096 residual GEMM beyond ~2.5k rows).  LOGITS always
-  // takes it: the two kernels' GEMM results are bitwise equal, but their
-  // log-softmax partials are reduced in different orders, so one kernel for
-  // every M keeps a sentence's scores independent of its batch.
-  const bool sw_pref = epi->kind == SKB_EPI_LOGITS || M <= 2560 || K < 4096;
+  // The swap-AB kernel serves every M (measured on B200, tools/tcsw_check.py:
+  // 1.3-2x faster than the M-major kernel up to M = 3840, except the
+  // K = 4096 residual GEMM beyond ~2.5k rows, 69 vs 51 us).  One kernel for
+  // every M is what keeps a sentence's numbers independent of its batch:
+  // the kernels' plain GEMM results are bitwise equal, but the swap-AB one
+  // splits K = 4096 over a 4-CTA cluster (a different fp32 summation order)
+  // and reduces the LOGITS partials in another order — with an M threshold
+  // the encoder's FFN2 of a large batch (B*L rows) and the log-softmax of a
+  // large decode batch took the other kernel (tools/invariance_check.py).
+  const bool sw_pref = true;
   if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || sw_pref)) {
     const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);

@@ -137,3 +137,24 @@ def test_concurrent_stream_batches_identical(precision):
     finally:
         engine.DECODE_STREAMS = old
     assert [(r.text, r.score) for r in out[1]] == [(r.text, r.score) for r in out[3]]
+
+
+def test_batch_invariance_at_scale():
+    """test_search.py:400-405 at the benchmark model's size (bf16): a batch
+    whose encoder sees > 2560 rows (B*L) and whose decoder runs several
+    streams of R = 640 rows, against the same sentences one at a time
+    (R = beam, prologue-LayerNorm GEMMs).  Every GEMM, the split-K FFN2 and
+    the log-softmax partials must take the same reduction order."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
+    model, vocabs = bench.build_model("bf16")
+    rng = np.random.default_rng(7)
+    sents = [[f"w{i}" for i in rng.integers(0, 31996, size=int(n))] for n in rng.integers(1, 121, size=160)]
+    st = SearchSettings(beam=5, length_alpha=1.0)
+    big = translate(model, vocabs, [SentenceInput(tokens=s) for s in sents], st, max_rows=640)
+    for i in (0, 41, 97, 159):
+        one = translate(model, vocabs, [SentenceInput(tokens=sents[i])], st)[0]
+        assert one.text == big[i].text and one.score == big[i].score, (i, one.score, big[i].score)
