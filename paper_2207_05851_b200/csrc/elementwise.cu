@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_layernorm_reg(int rows, const float *__
                                                        const float *__restrict__ bias, float eps,
                                                        void *out, int ldo, int out_dtype) {
   constexpr int d = NV * 128;
-  const int warp = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   // gain / bias are parameters: loaded before the grid-dependency wait
   float4 g[NV], bb[NV];
 #pragma unroll
@@ -242,8 +242,15 @@ extern "C" int skb_layernorm(int rows, int d, const float *x, int ldx, const flo
                          reinterpret_cast<uintptr_t>(gain) | reinterpret_cast<uintptr_t>(bias)) & 15) == 0;
   const int blocks = (rows + 7) / 8;
   cudaStream_t s = as_stream(stream);
+  static int lw = -1;  // warps (rows) per CTA of the d = 1024 kernel, SKB_LN_WARPS
+  if (lw < 0) {
+    const char *e = getenv("SKB_LN_WARPS");
+    lw = e ? atoi(e) : 4;  // 4 measured best at R = 640 (more SMs share the rows)
+    if (lw < 1 || lw > 8) lw = 8;
+  }
   if (aligned && d == 1024)
-    launch_k(k_layernorm_reg<8>, blocks, 256, 0, s, rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
+    launch_k(k_layernorm_reg<8>, (rows + lw - 1) / lw, 32 * lw, 0, s, rows, x, ldx, gain, bias, eps, out,
+             ldo, out_dtype);
   else if (aligned && d == 512)
     launch_k(k_layernorm_reg<4>, blocks, 256, 0, s, rows, x, ldx, gain, bias, eps, out, ldo, out_dtype);
   else if (aligned && d == 256)
