@@ -1260,7 +1260,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     mbar_wait(tfull, 0);
-    if (ep.late_trigger && warp == 2 && lane == 0) pdl_trigger();
+    if (ep.late_trigger == 1 && warp == 2 && lane == 0) pdl_trigger();  // (2: only at exit)
     if (warp == 2 && lane == 0) SW_STAMP(5);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
