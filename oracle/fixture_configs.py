@@ -106,6 +106,15 @@ SEARCH_CASES = [
          inputs=[dict(tokens=["w1", "w2"], target_prefix=["w3"],
                       target_prefix_factors=[["F0_1"]])]
          + _inputs(_sentences(14, 5, W10))),
+    # prefix-factor streams longer than the surface prefix (the factor of
+    # output token j is emitted at step j + 1, search.py:261-272)
+    dict(name="factored_long_factor_prefix", config="factored", beam=3,
+         inputs=[dict(tokens=["w1", "w2", "w6"], target_prefix=["w3"],
+                      target_prefix_factors=[["F0_0", "F0_1", "F0_0"]]),
+                 dict(tokens=["w4"], target_prefix_factors=[["F0_1", "F0_1"]])]),
+    dict(name="factored_long_factor_prefix_greedy", config="factored", beam=1,
+         inputs=[dict(tokens=["w1", "w2", "w6"], target_prefix=["w3"],
+                      target_prefix_factors=[["F0_0", "F0_1", "F0_0"]])]),
     dict(name="ssru_greedy", config="ssru", beam=1, inputs=_inputs(_sentences(15, 6, W36))),
     dict(name="ssru_beam4", config="ssru", beam=4, alpha=0.6,
          inputs=_inputs(_sentences(16, 6, W36))),
@@ -119,3 +128,59 @@ SEARCH_CASES = [
     dict(name="tiny_beam5", config="tiny", beam=5,
          inputs=_inputs(_sentences(17, 2, W7996, lo=6, hi=10))),
 ]
+
+
+# ----------------------------------------------------------------- scale
+# The BASELINE.json configs the bench measures, for the
+# reference-generated beam traces in tests/golden/scale_*.npz: the GPU tests
+# teacher-force the product's bench kernels along these traces.
+BIG66 = dict(src_vocab_size=32000, trg_vocab_size=32000, d_model=1024, heads=16, ff_dim=4096,
+             encoder_layers=6, decoder_layers=6, decoder_kind="self_attention", max_seq_len=128)
+BASE66 = dict(BIG66, d_model=512, heads=8, ff_dim=2048)
+BIG_SSRU = dict(BIG66, encoder_layers=20, decoder_layers=2, decoder_kind="ssru")
+
+SCALE_CONFIGS = {"big": dict(seed=13, config=BIG66),
+                 "base": dict(seed=13, config=BASE66),
+                 "big_ssru": dict(seed=13, config=BIG_SSRU)}
+
+# (name, config, beam, alpha, source lengths, shortlist top-k or None)
+SCALE_TRACES = [
+    dict(name="big_beam5", config="big", beam=5, alpha=1.0, lengths=[30, 19], seed=101),
+    dict(name="big_greedy", config="big", beam=1, alpha=1.0, lengths=[30], seed=102),
+    dict(name="base_beam5", config="base", beam=5, alpha=1.0, lengths=[30, 13], seed=103),
+    dict(name="big_ssru_beam5_sl200", config="big_ssru", beam=5, alpha=1.0, lengths=[30, 24],
+         seed=104, shortlist=200),
+    dict(name="big_ssru_greedy_sl200", config="big_ssru", beam=1, alpha=1.0, lengths=[30],
+         seed=105, shortlist=200),
+]
+# log-prob rows kept per trace (the rest of the trace keeps only fed tokens
+# and parents): early steps, the middle, and the last (forced-EOS) step
+SCALE_KEEP_STEPS = (0, 1, 2, 7, 23, 41, "last")
+SCALE_TOPN, SCALE_RANDN = 16, 256
+# base 6-6 beam 5: whole-record fp32 parity subsample (north star: >= 99 %
+# of output sequences identical in fp32 mode)
+BASE_RECORDS = dict(config="base", beam=5, alpha=1.0, n=6, seed=106, lo=4, hi=30)
+
+
+def scale_sentences(seed, lengths, V):
+    """SURVEY §8d synthetic sources: ids uniform in 4..V-1, tokens w{id-4}."""
+    rng = np.random.default_rng(seed)
+    return [[f"w{int(i)}" for i in rng.integers(0, V - 4, size=n)] for n in lengths]
+
+
+def synthetic_shortlist_rows(V: int, k: int = 200, seed: int = 7) -> dict:
+    """every source id 4..V-1 gets k distinct target ids drawn
+    from 4..V-1 with default_rng(seed) (first k distinct of an oversampled
+    draw, kept in draw order, returned sorted as Shortlist rows are).
+    Shared by the golden generator, the tests and bench.py."""
+    rng = np.random.default_rng(seed)
+    draw = rng.integers(4, V, size=(V - 4, k + k // 2 + 16))
+    rows = {}
+    for i in range(V - 4):
+        u, first = np.unique(draw[i], return_index=True)
+        pick = u[np.argsort(first)][:k]
+        if pick.size < k:  # pragma: no cover - oversampling makes this vanishingly rare
+            extra = np.setdiff1d(np.arange(4, V), pick)[: k - pick.size]
+            pick = np.concatenate([pick, extra])
+        rows[i + 4] = np.sort(pick).astype(np.int64)
+    return rows

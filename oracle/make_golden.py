@@ -20,6 +20,14 @@ on seeded inputs:
   * beam_trace_<cfg>.npz — per-step lp, alive scores and picks of a beam run,
                     captured by wrapping Model.decode_step and
                     DecodeState.select_rows (never editing the reference)
+  * scale_<trace>.npz — the same capture at the BENCH configs (big 6-6,
+                    base 6-6, big 20-2 SSRU + top-200 shortlist; beam 5 and
+                    greedy): every step's fed tokens and parents, and at a few
+                    steps the log-probs of each row's top-16 columns plus 256
+                    random active columns (the full rows would be MBs); the
+                    final hypothesis.  `python oracle/make_golden.py scale`
+  * records_base.json — translate() records of the base 6-6 beam-5
+                    subsample (fp32 whole-sequence parity)
 
 The oracle (oracle/skiff_oracle.py) is then checked against these files by
 tests/test_oracle_golden.py; the CUDA path is checked against the oracle and
@@ -41,7 +49,10 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 GOLDEN = ROOT / "tests" / "golden"
 sys.path.insert(0, str(ROOT))
-from oracle.fixture_configs import CONFIGS, SEARCH_CASES, make_words  # noqa: E402
+from oracle.fixture_configs import (BASE_RECORDS, CONFIGS, SCALE_CONFIGS,  # noqa: E402
+                                    SCALE_KEEP_STEPS, SCALE_RANDN, SCALE_TOPN, SCALE_TRACES,
+                                    SEARCH_CASES, make_words, scale_sentences,
+                                    synthetic_shortlist_rows)
 
 
 def import_reference():
@@ -59,7 +70,7 @@ def import_reference():
 
 def ref_model(name):
     from skiff.model import Model, ModelConfig, SourceFactorSpec, TargetFactorSpec
-    spec = CONFIGS[name]
+    spec = CONFIGS[name] if name in CONFIGS else SCALE_CONFIGS[name]
     cfg = dict(spec["config"])
     cfg["source_factor_specs"] = [SourceFactorSpec(*s) for s in cfg.get("source_factor_specs", [])]
     cfg["target_factor_specs"] = [TargetFactorSpec(v) for v in cfg.get("target_factor_specs", [])]
@@ -68,7 +79,7 @@ def ref_model(name):
 
 def ref_vocabs(name):
     from skiff.vocab import FACTOR_SPECIALS, SPECIALS, Vocabulary
-    spec = CONFIGS[name]
+    spec = CONFIGS[name] if name in CONFIGS else SCALE_CONFIGS[name]
     cfg = spec["config"]
     src = Vocabulary(SPECIALS + make_words(cfg["src_vocab_size"] - 4))
     trg = Vocabulary(SPECIALS + make_words(cfg["trg_vocab_size"] - 4))
@@ -266,15 +277,134 @@ def gen_beam_traces():
         np.savez_compressed(GOLDEN / f"beam_trace_{name}.npz", **out)
 
 
+def _capture(m, vocabs, inp, beam, alpha, restriction):
+    """Run the reference's own greedy_search / beam_search on one sentence,
+    recording every decode_step's fed tokens and log-probs and every
+    select_rows' parents (wrapping, never editing, the reference)."""
+    import skiff.kernels as K
+    from skiff.model import DecodeState, Model
+    from skiff.search import beam_search, greedy_search
+    rec = {"lp": [], "fed": [], "parents": [], "active": None}
+    orig_step, orig_sel = Model.decode_step, DecodeState.select_rows
+
+    def step(self, state, prev_ids, prev_factor_ids):
+        out = orig_step(self, state, prev_ids, prev_factor_ids)
+        rec["lp"].append(K.log_softmax(out.surface).data.copy())
+        rec["fed"].append(np.asarray(prev_ids).copy())
+        rec["active"] = out.active_ids
+        return out
+
+    def sel(self, idx):
+        rec["parents"].append(np.asarray(idx).copy())
+        return orig_sel(self, idx)
+
+    Model.decode_step, DecodeState.select_rows = step, sel
+    try:
+        if beam == 1:
+            hyp = greedy_search(m, vocabs, inp, restriction, alpha)
+        else:
+            hyp = beam_search(m, vocabs, inp, beam, restriction, alpha)
+    finally:
+        Model.decode_step, DecodeState.select_rows = orig_step, orig_sel
+    return hyp, rec
+
+
+def gen_scale(only=None):
+    """Beam traces at the bench configs, subset-compressed."""
+    import time
+    from skiff.search import SentenceInput, ShortlistRestriction
+    from skiff.shortlist import Shortlist
+    models = {}
+    for tr in SCALE_TRACES:
+        if only and tr["name"] not in only:
+            continue
+        t0 = time.time()
+        if tr["config"] not in models:
+            models.clear()
+            models[tr["config"]] = (ref_model(tr["config"]), ref_vocabs(tr["config"]))
+        m, vocabs = models[tr["config"]]
+        V = m.config.trg_vocab_size
+        K = tr["beam"]
+        restriction = None
+        if tr.get("shortlist"):
+            restriction = ShortlistRestriction(Shortlist(synthetic_shortlist_rows(V, tr["shortlist"])))
+        out = {}
+        for s, toks in enumerate(scale_sentences(tr["seed"], tr["lengths"], V)):
+            hyp, rec = _capture(m, vocabs, SentenceInput(tokens=toks), K, tr["alpha"], restriction)
+            T = len(rec["lp"])
+            active = rec["active"]
+            fed = np.full((T, K), -1, np.int32)
+            par = np.full((T, K), -1, np.int32)
+            nrows = np.zeros(T, np.int32)
+            for t in range(T):
+                f = rec["fed"][t]
+                fed[t, :len(f)] = f
+                nrows[t] = len(f)
+                if t < len(rec["parents"]):
+                    par[t, :len(rec["parents"][t])] = rec["parents"][t]
+            keep = sorted({T - 1 if k == "last" else k for k in SCALE_KEEP_STEPS if k == "last" or k < T})
+            rng = np.random.default_rng(tr["seed"] * 1000 + s)
+            A = rec["lp"][0].shape[1]
+            top_col = np.zeros((len(keep), K, SCALE_TOPN), np.int32)
+            top_lp = np.zeros((len(keep), K, SCALE_TOPN), np.float32)
+            rnd_col = np.zeros((len(keep), SCALE_RANDN), np.int32)
+            rnd_lp = np.zeros((len(keep), K, SCALE_RANDN), np.float32)
+            for i, t in enumerate(keep):
+                lp = rec["lp"][t]
+                cols = np.sort(rng.choice(A, size=SCALE_RANDN, replace=False))
+                rnd_col[i] = cols
+                for r in range(lp.shape[0]):
+                    # top-N by (lp desc, column asc): stable on ties
+                    o = np.lexsort((np.arange(A), -lp[r]))[:SCALE_TOPN]
+                    top_col[i, r], top_lp[i, r] = o, lp[r, o]
+                    rnd_lp[i, r] = lp[r, cols]
+            tok_of = (lambda c: active[c]) if active is not None else (lambda c: c)
+            pre = f"s{s}_"
+            out.update({pre + "src": np.array(vocabs.src_vocab.encode(toks), np.int32),
+                        pre + "fed": fed, pre + "parents": par, pre + "nrows": nrows,
+                        pre + "keep": np.array(keep, np.int32),
+                        pre + "top_tok": tok_of(top_col).astype(np.int32), pre + "top_lp": top_lp,
+                        pre + "rnd_tok": tok_of(rnd_col).astype(np.int32), pre + "rnd_lp": rnd_lp,
+                        pre + "hyp_tokens": np.array(hyp.tokens, np.int32),
+                        pre + "hyp_logprob": np.array(hyp.logprob),
+                        pre + "hyp_steps": np.array(hyp.steps),
+                        pre + "hyp_forced": np.array(hyp.forced_eos)})
+            if active is not None:
+                out[pre + "active"] = np.asarray(active, np.int32)
+        out["n_sentences"] = np.array(len(tr["lengths"]))
+        np.savez_compressed(GOLDEN / f"scale_{tr['name']}.npz", **out)
+        print(f"scale {tr['name']}: {time.time() - t0:.1f} s", flush=True)
+
+
+def gen_base_records():
+    """translate() records, base 6-6 beam 5, for whole-sequence fp32 parity."""
+    from skiff.search import SearchSettings, SentenceInput, translate
+    br = BASE_RECORDS
+    m, vocabs = ref_model(br["config"]), ref_vocabs(br["config"])
+    V = m.config.trg_vocab_size
+    rng = np.random.default_rng(br["seed"])
+    lengths = [int(x) for x in rng.integers(br["lo"], br["hi"] + 1, size=br["n"])]
+    sents = scale_sentences(br["seed"], lengths, V)
+    recs = translate(m, vocabs, [SentenceInput(tokens=t) for t in sents],
+                     SearchSettings(beam=br["beam"], length_alpha=br["alpha"]))
+    (GOLDEN / "records_base.json").write_text(json.dumps(
+        dict(inputs=sents, records=_records_to_json(recs)), indent=0))
+
+
 def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
     tmp = import_reference()
     try:
-        gen_kernels()
-        gen_params()
-        gen_steps()
-        gen_search()
-        gen_beam_traces()
+        if len(sys.argv) > 1 and sys.argv[1] == "scale":
+            gen_scale(set(sys.argv[2:]) or None)
+            if len(sys.argv) == 2:
+                gen_base_records()
+        else:
+            gen_kernels()
+            gen_params()
+            gen_steps()
+            gen_search()
+            gen_beam_traces()
     finally:
         shutil.rmtree(tmp, ignore_errors=True)
     for p in sorted(GOLDEN.iterdir()):

@@ -23,6 +23,8 @@ import math
 from dataclasses import dataclass, field
 
 import os
+import weakref
+from collections import OrderedDict
 
 import numpy as np
 import torch
@@ -171,6 +173,16 @@ class ChunkResult:
     forced_eos: bool
 
 
+def _check_source_ids(c, ids: np.ndarray, fids: np.ndarray) -> None:
+    """Embedding lookups are unchecked on the device: range-check the
+    surface ids and every source-factor stream against its table."""
+    if (ids < 0).any() or (ids >= c.src_vocab_size).any():
+        raise ShapeError(f"ids out of range [0, {c.src_vocab_size}) for embedding table")
+    for k, spec in enumerate(c.source_factor_specs):
+        if (fids[k] < 0).any() or (fids[k] >= spec.vocab_size).any():
+            raise ShapeError(f"source factor {k} ids out of range [0, {spec.vocab_size})")
+
+
 def _encode_batch(model: Model, jobs: list[ChunkJob]):
     c = model.config
     B = len(jobs)
@@ -189,8 +201,7 @@ def _encode_batch(model: Model, jobs: list[ChunkJob]):
     ids_d = torch.from_numpy(ids.reshape(-1)).to(dev)
     fids_d = torch.from_numpy(fids.reshape(max(nsf, 1), -1)).to(dev)
     len_d = torch.from_numpy(lengths).to(dev)
-    if (ids < 0).any() or (ids >= c.src_vocab_size).any():
-        raise ShapeError(f"ids out of range [0, {c.src_vocab_size}) for embedding table")
+    _check_source_ids(c, ids, fids)
     enc = model.encode_device(ids_d, fids_d if nsf else None, len_d, B, L)
     return enc, len_d, B, L
 
@@ -360,13 +371,13 @@ class DecodeWorkspace:
         kern.launches = before  # capture does not launch
         return g
 
-    def run(self, use_graph: bool = True, poll: bool = True) -> int:
-        """Encode + decode S_max steps (stopping early, one chunk late, once
-        every sentence is done).  Returns the number of steps run."""
+    def run(self, S_run: int, use_graph: bool = True, poll: bool = True) -> int:
+        """Encode + decode S_run <= S_max steps (stopping early, one chunk
+        late, once every sentence is done).  Returns the number of steps run."""
         if not use_graph:
             self.encode()
             steps = 0
-            while steps < self.S_max:
+            while steps < S_run:
                 self.one_step()
                 steps += 1
             return steps
@@ -386,8 +397,8 @@ class DecodeWorkspace:
                                              "launches_chunk")
         done_host = torch.zeros(1, dtype=I32, pin_memory=True)
         ev = None
-        while steps < self.S_max:
-            if self.graph_n is not None and self.S_max - steps >= self.CHUNK:
+        while steps < S_run:
+            if self.graph_n is not None and S_run - steps >= self.CHUNK:
                 self.graph_n.replay()
                 kern.launches += self.launches_chunk
                 steps += self.CHUNK
@@ -395,7 +406,7 @@ class DecodeWorkspace:
                 self.graph_1.replay()
                 kern.launches += self.launches_step
                 steps += 1
-            if poll and steps < self.S_max:
+            if poll and steps < S_run:
                 # early exit for finished batches, checked one chunk late so the
                 # host never stalls the GPU pipeline
                 if ev is not None and ev.query() and int(done_host[0]) >= self.B:
@@ -439,18 +450,43 @@ class DecodeWorkspace:
         return toks, facs, steps, forced, lp.numpy()
 
 
-_WS_CACHE: dict = {}
-_WS_MAX = 16
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+# Workspaces per model (dropped with the model), least recently used first,
+# bounded by device bytes (SKB_WS_BYTES, default 24 GB of the 180 GB).
+_WS_CACHE: "weakref.WeakKeyDictionary[Model, OrderedDict]" = weakref.WeakKeyDictionary()
+_WS_BYTES = int(float(os.environ.get("SKB_WS_BYTES", 24e9)))
+
+
+def _ws_bytes(ws) -> int:
+    seen, tot = set(), 0
+    for v in list(vars(ws).values()) + list(vars(ws.sb).values()) + list(ws.enc_bufs.values()):
+        if isinstance(v, torch.Tensor) and v.is_cuda and v.data_ptr() not in seen:
+            seen.add(v.data_ptr())
+            tot += v.numel() * v.element_size()
+    return tot
 
 
 def _workspace(model, key, *args):
-    ws = _WS_CACHE.get((id(model), key))
-    if ws is None:
-        if len(_WS_CACHE) >= _WS_MAX:
-            _WS_CACHE.pop(next(iter(_WS_CACHE)))
-        ws = DecodeWorkspace(model, *args)
-        _WS_CACHE[(id(model), key)] = ws
+    per = _WS_CACHE.setdefault(model, OrderedDict())
+    ws = per.get(key)
+    if ws is not None:
+        per.move_to_end(key)
+        return ws
+    ws = DecodeWorkspace(model, *args)
+    ws.nbytes = _ws_bytes(ws)
+    per[key] = ws
+    total = sum(w.nbytes for p in _WS_CACHE.values() for w in p.values())
+    while total > _WS_BYTES and len(per) > 1:
+        _, old = per.popitem(last=False)  # an in-flight batch keeps its own reference
+        total -= old.nbytes
     return ws
+
+
+def clear_workspaces() -> None:
+    _WS_CACHE.clear()
 
 
 class BeamBatch:
@@ -477,8 +513,19 @@ class BeamBatch:
         L = max(len(j.src_ids) for j in jobs)
         self.B, self.L, self.R = B, L, B * beam
         max_len = np.array([2 * len(j.src_ids) + 10 for j in jobs], dtype=np.int32)
-        self.S_max = int(max_len.max())
-        self.P = max(1, max(len(j.prefix_ids) for j in jobs))
+        # steps this batch runs (the longest chunk's 2L+10 cap, search.py:231-232)
+        self.S_run = int(max_len.max())
+        # the prefix tables hold the surface prefix AND every prefix-factor
+        # stream (a factor stream may reach past the surface prefix)
+        P = max([1] + [len(j.prefix_ids) for j in jobs]
+                + [len(f) for j in jobs for f in j.prefix_factor_ids[:nf]])
+        # Workspace shape buckets (reused across batches of similar shape):
+        # padded source width to a multiple of 8 (the encoder's pad bias
+        # hides the extra positions; pe rows cover it, Model.pe_rows), prefix
+        # width to a multiple of 8; step capacity follows the padded width.
+        self.L_ws = min(_round_up(L, 8), model.pe_rows)
+        self.P = _round_up(P, 8)
+        self.S_max = 2 * self.L_ws + 10
         self._max_len = max_len
         self.ws = None
         self.steps_run = 0
@@ -495,11 +542,15 @@ class BeamBatch:
         if restricted:
             actives = [a if a is not None else np.arange(V, dtype=np.int64) for a in actives]
             U_ids = np.unique(np.concatenate(actives)).astype(np.int64)
-            U = int(U_ids.size)
+            U_real = int(U_ids.size)
+            # union width bucketed to 256 columns: the padding columns repeat
+            # the last id and are never set in any sentence's column mask
+            U = min(_round_up(U_real, 256), max(V, U_real))
         else:
             U = V
-        key = (B, L, self.S_max, K, P, U, self.alpha, restricted, self.slot, kern.concurrency)
-        ws = _workspace(model, key, B, L, self.S_max, K, P, U, self.alpha, restricted)
+        Lw = self.L_ws
+        key = (B, Lw, K, P, U, self.alpha, restricted, self.slot, kern.concurrency)
+        ws = _workspace(model, key, B, Lw, self.S_max, K, P, U, self.alpha, restricted)
         self.ws = ws
         # this batch's inputs: own pinned staging + own device copy (several
         # batches of one shape can be staged before any of them runs)
@@ -509,9 +560,9 @@ class BeamBatch:
         for k, n in ws.in_sizes.items():
             h[k] = self.in_host[off:off + n]
             off += n
-        ids = h["ids"].numpy().reshape(B, L)
+        ids = h["ids"].numpy().reshape(B, Lw)
         ids[:] = 0
-        fids = h["fids"].numpy().reshape(max(nsf, 1), B, L)
+        fids = h["fids"].numpy().reshape(max(nsf, 1), B, Lw)
         fids[:] = 0
         lengths = h["lengths"].numpy()
         for b, j in enumerate(jobs):
@@ -520,8 +571,7 @@ class BeamBatch:
             lengths[b] = n
             for k in range(nsf):
                 fids[k, b, :n] = j.src_factor_ids[k]
-        if (ids < 0).any() or (ids >= c.src_vocab_size).any():
-            raise ShapeError(f"ids out of range [0, {c.src_vocab_size}) for embedding table")
+        _check_source_ids(c, ids, fids)
         h["max_len"].numpy()[:] = self._max_len
         h["prefix_len"].numpy()[:] = [len(j.prefix_ids) for j in jobs]
         pcol = h["prefix_col"].numpy().reshape(B, P)
@@ -530,7 +580,9 @@ class BeamBatch:
         pfac[:] = -1
         col_of = None
         if restricted:
-            h["col_token"].numpy()[:] = U_ids.astype(np.int32)
+            ct = h["col_token"].numpy()
+            ct[:U_real] = U_ids.astype(np.int32)
+            ct[U_real:] = U_ids[-1]
             mask = h["mask"].numpy().view(np.uint32).reshape(B, -1)
             mask[:] = 0
             for b, a in enumerate(actives):
@@ -608,7 +660,7 @@ class BeamBatch:
         torch.cuda.current_stream().wait_event(self.in_ready)
         ws.in_dev.copy_(self.in_dev, non_blocking=True)   # device-resident inputs
         ws.reset()
-        self.steps_run = ws.run(self.use_graph)
+        self.steps_run = ws.run(self.S_run, self.use_graph)
         ws.enqueue_collect()
 
     def finish(self) -> list[ChunkResult]:
@@ -643,17 +695,24 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
         return []
     order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i].src_ids))
     per_batch = max(1, max_rows // beam)
-    results: list[ChunkResult | None] = [None] * len(jobs)
     # Batches run concurrently on DECODE_STREAMS CUDA streams (batch n on
     # stream n % S); on each stream batch n+S is prepared and launched before
     # batch n is read back, so a stream alternates two workspaces.
+    with torch.cuda.device(model.device):
+        return _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_graph)
+
+
+def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_graph):
+    results: list[ChunkResult | None] = [None] * len(jobs)
     n_batches = (len(order) + per_batch - 1) // per_batch
     S = max(1, min(DECODE_STREAMS, n_batches))
     kern.set_concurrency(S)
-    if len(_STREAMS) < S:
-        _STREAMS.extend(torch.cuda.Stream() for _ in range(S - len(_STREAMS)))
+    pool = _STREAMS.setdefault(model.device.index if model.device.index is not None
+                               else torch.cuda.current_device(), [])
+    if len(pool) < S:
+        pool.extend(torch.cuda.Stream() for _ in range(S - len(pool)))
     main = torch.cuda.current_stream()
-    streams = [main] + _STREAMS[1:S]
+    streams = [main] + pool[1:S]
     for st in streams[1:]:
         st.wait_stream(main)
     pending = []
@@ -679,7 +738,7 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
 
 
 DECODE_STREAMS = int(os.environ.get("SKB_STREAMS", "3"))  # concurrent decode batches per device (serving mode; 3 measured best on B200)
-_STREAMS: list = []
+_STREAMS: dict = {}  # device index -> decode streams
 
 
 # =========================================================== model protocol

@@ -14,7 +14,6 @@ from . import _native as N
 
 launches = 0
 concurrency = 1  # decode streams sharing the device (GEMM tile sizing; see set_concurrency)
-_splitk = None  # (workspace fp32, counters int32) shared by all GEMMs of a device
 
 
 def set_concurrency(n: int) -> None:
@@ -25,13 +24,6 @@ def set_concurrency(n: int) -> None:
     if n != concurrency:
         N.call("skb_set_concurrency", int(n))
         concurrency = int(n)
-
-
-def set_splitk_workspace(ws, counters) -> None:
-    """Split-K scratch for the tcgen05 GEMM (fp32 partial tiles + zeroed
-    per-tile counters).  Calls on one stream may share it."""
-    global _splitk
-    _splitk = (ws, counters)
 
 
 def _count(n: int = 1) -> None:

@@ -80,10 +80,6 @@ class Model:
             N.call("skb_set_device", self.device.index)
         self.cdt = torch.bfloat16 if precision == "bf16" else torch.float32
         self.quantized: dict = {}
-        if precision == "bf16":
-            # split-K scratch of the tcgen05 GEMM: 32 MB of fp32 partial tiles
-            kern.set_splitk_workspace(torch.empty(8 << 20, device=self.device),
-                                      torch.zeros(8192, dtype=torch.int32, device=self.device))
         self._upload(params)
         self.params = params
 
@@ -109,7 +105,10 @@ class Model:
                                           dtype=torch.int64, device=self.device)
         self.trg_ftab_ptrs = torch.tensor([t.data_ptr() for t in self.trg_factor_tables] or [0],
                                           dtype=torch.int64, device=self.device)
-        self.pe_src = f32(positional_encoding(c.max_seq_len, c.surface_embed_dim))
+        # source positions: max_seq_len rounded up to 8 (the engine pads a
+        # batch's source width to a multiple of 8; encode_device checks it)
+        self.pe_rows = (c.max_seq_len + 7) // 8 * 8
+        self.pe_src = f32(positional_encoding(self.pe_rows, c.surface_embed_dim))
         self.max_steps = 2 * c.max_seq_len + 10  # model.py:543-544
         self.pe_trg = f32(positional_encoding(self.max_steps, d))
 
@@ -187,6 +186,9 @@ class Model:
         int32.  Returns enc fp32 [B*L, d]."""
         c = self.config
         d, H, dh = c.d_model, c.heads, c.head_dim
+        if L > self.pe_rows:
+            # embed_source reads one positional-encoding row per position
+            raise ShapeError(f"source width {L} exceeds the model's {c.max_seq_len} positions")
         n = B * L
         dev, cdt = self.device, self.cdt
         bufs = bufs or self.encoder_buffers(n)

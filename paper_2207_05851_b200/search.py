@@ -380,7 +380,8 @@ class ProtocolSearch:
                 raise ConfigError(f"token id {tok} missing from the restricted vocabulary")
             return c
 
-        P = max(1, len(job.prefix_ids))
+        # the prefix tables hold the surface prefix and every factor stream
+        P = max([1, len(job.prefix_ids)] + [len(f) for f in job.prefix_factor_ids[:nf]])
         z = lambda n, dt=torch.int32: torch.zeros(n, dtype=dt, device=dev)  # noqa: E731
         bufs = dict(
             len_pen=torch.tensor([float(s) ** self.alpha if s else 1.0 for s in range(max_len + 1)],
