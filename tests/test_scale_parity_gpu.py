@@ -117,7 +117,10 @@ def forced_engine_run(model, tr, sents, copies):
     restricted = actives[0] is not None
     if restricted:
         U_ids = np.unique(np.concatenate(actives))
-        assert U_ids.size == sb.logits.shape[1]
+        # the union vocabulary (bucketed width: padding columns masked out)
+        ct = ws.inp["col_token"].cpu().numpy()
+        assert U_ids.size <= sb.logits.shape[1] == ct.size
+        np.testing.assert_array_equal(ct[:U_ids.size], U_ids)
     T = max(len(s["nrows"]) for s in sents)
     worst = [0.0] * n
     checked = [0] * n
