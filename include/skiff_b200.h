@@ -138,6 +138,13 @@ int skb_gemm_force(int bn, int cs, int splits);
  * K-split; 0 = choose automatically. */
 int skb_gemm_force_sw(int mode, int na, int cs);
 
+/* Select the persistent CTA-pair GEMM (tcgen05.mma.cta_group::2, 256 weight
+ * rows x na activation rows per tile, two TMEM accumulators): mode 0 =
+ * automatic (M >= 128, shapes without a cluster K-split), 1 = never,
+ * 2 = always where applicable; na in {32..256} step 32, pairs = CTA pairs per
+ * launch; 0 = choose automatically.  Bitwise equal to the swap-AB kernel. */
+int skb_gemm_force_pc(int mode, int na, int pairs);
+
 /* Number of independent decode streams the caller runs concurrently on this
  * device (default 1).  The swap-AB GEMM sizes its tiles for its share of the
  * SMs (fewer, larger tiles ingest fewer bytes in total).  Affects launches

@@ -18,11 +18,17 @@ import time
 _MODEL = None
 
 
-def _init(cfg_kwargs, seed):
-    global _MODEL
+_RESTRICTION = None
+
+
+def _init(cfg_kwargs, seed, shortlist_topk=None):
+    global _MODEL, _RESTRICTION
     from oracle import skiff_oracle as O
     cfg = O.OConfig(**cfg_kwargs)
     _MODEL = O.OracleModel(cfg, O.init_params(cfg, seed))
+    if shortlist_topk:
+        from oracle.fixture_configs import synthetic_shortlist_rows
+        _RESTRICTION = ("shortlist", synthetic_shortlist_rows(cfg.trg_vocab_size, shortlist_topk))
 
 
 def _work(args):
@@ -30,20 +36,34 @@ def _work(args):
     src, beam, alpha, n_steps = args
     timings = []
     t0 = time.perf_counter()
-    O.beam(_MODEL, O.OChunk(list(src)), beam, alpha=alpha, max_steps=n_steps, timings=timings)
+    O.beam(_MODEL, O.OChunk(list(src)), beam, restriction=_RESTRICTION, alpha=alpha,
+           max_steps=n_steps, timings=timings)
     return timings, time.perf_counter() - t0
+
+
+def default_procs() -> int:
+    """P = min(nproc, floor(RAM / 4 GB)) single-threaded workers."""
+    ncpu = os.cpu_count() or 1
+    try:
+        with open("/proc/meminfo") as f:
+            kb = next(int(ln.split()[1]) for ln in f if ln.startswith("MemTotal"))
+        by_ram = max(1, kb // (4 * 1024 * 1024))
+    except (OSError, StopIteration, ValueError):
+        by_ram = ncpu
+    return max(1, min(ncpu, by_ram))
 
 
 class CpuBaseline:
     """Pool of P single-threaded oracle workers holding the same weights."""
 
-    def __init__(self, cfg_kwargs: dict, seed: int = 13, procs: int | None = None):
+    def __init__(self, cfg_kwargs: dict, seed: int = 13, procs: int | None = None,
+                 shortlist_topk: int | None = None):
         for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
             os.environ[var] = "1"
-        ncpu = os.cpu_count() or 1
-        self.procs = procs or max(1, min(ncpu, 16))
+        self.procs = procs or default_procs()
         ctx = mp.get_context("spawn")
-        self.pool = ctx.Pool(self.procs, initializer=_init, initargs=(cfg_kwargs, seed))
+        self.pool = ctx.Pool(self.procs, initializer=_init,
+                             initargs=(cfg_kwargs, seed, shortlist_topk))
         # make sure every worker has built its model before timing
         self.pool.map(_noop, range(self.procs * 2))
 

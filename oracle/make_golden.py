@@ -28,6 +28,13 @@ on seeded inputs:
                     final hypothesis.  `python oracle/make_golden.py scale`
   * records_base.json — translate() records of the base 6-6 beam-5
                     subsample (fp32 whole-sequence parity)
+  * refdir_<cfg>/ + refdir_records.json — model directories written by the
+                    reference's own save_model_dir (config, SKP1 params.bin,
+                    vocab JSON incl. factor vocabularies) and the records the
+                    reference's translate() produces after loading them back
+                    with its load_model_dir (checkpoint.py:316-353): the
+                    product must read these directories unchanged.
+                    `python oracle/make_golden.py modeldirs`
 
 The oracle (oracle/skiff_oracle.py) is then checked against these files by
 tests/test_oracle_golden.py; the CUDA path is checked against the oracle and
@@ -391,11 +398,35 @@ def gen_base_records():
         dict(inputs=sents, records=_records_to_json(recs)), indent=0))
 
 
+REFDIR_CASES = [("srcfac", "srcfac_beam2"), ("ssru", "ssru_beam4"), ("factored", "factored_beam3")]
+
+
+def gen_model_dirs():
+    """Model directories saved by the reference + its records after reload."""
+    from skiff.checkpoint import load_model_dir, save_model_dir
+    from skiff.search import SearchSettings, SentenceInput, translate
+    out = {}
+    for cfg_name, case_name in REFDIR_CASES:
+        d = GOLDEN / f"refdir_{cfg_name}"
+        shutil.rmtree(d, ignore_errors=True)
+        v = ref_vocabs(cfg_name)
+        save_model_dir(d, ref_model(cfg_name), v.src_vocab, v.trg_vocab, v.src_factor_vocabs,
+                       v.trg_factor_vocabs)
+        md = load_model_dir(d)
+        case = next(c for c in SEARCH_CASES if c["name"] == case_name)
+        settings = SearchSettings(beam=case.get("beam", 1), length_alpha=case.get("alpha", 1.0))
+        recs = translate(md.model, md, [SentenceInput(**i) for i in case["inputs"]], settings)
+        out[cfg_name] = dict(case=case_name, records=_records_to_json(recs))
+    (GOLDEN / "refdir_records.json").write_text(json.dumps(out, indent=0))
+
+
 def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
     tmp = import_reference()
     try:
-        if len(sys.argv) > 1 and sys.argv[1] == "scale":
+        if len(sys.argv) > 1 and sys.argv[1] == "modeldirs":
+            gen_model_dirs()
+        elif len(sys.argv) > 1 and sys.argv[1] == "scale":
             gen_scale(set(sys.argv[2:]) or None)
             if len(sys.argv) == 2:
                 gen_base_records()

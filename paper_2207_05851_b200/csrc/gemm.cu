@@ -1676,6 +1676,442 @@ void init_mode() {
 
 }  // namespace sw
 
+// ====================================== persistent CTA-pair GEMM (pc)
+// The swap-AB layout of the sw kernel (weight rows on the MMA M side,
+// activation rows on N) run by CTA pairs: tcgen05.mma.cta_group::2 with
+// M = 256 weight rows (128 per SM, each from its own shared memory) and
+// N = Na activation rows (Na/2 per SM, read by the MMA from both SMs), so a
+// pair ingests (256 + Na) rows of K per tile instead of 2 x (128 + Na): the
+// L2->SM bytes per FLOP drop by up to 2x, which is what bounds the decode
+// GEMMs at M = 640 (per-SM TMA ingest).  The grid is
+// persistent (a pair loops over tiles; M-tiles fastest so the pairs working
+// at the same time share a weight tile in L2) and TMEM holds two
+// accumulators, so the epilogue of tile i (TMEM -> registers -> 32-row
+// staged chunks -> TMA store / TMA reduce-add) overlaps the MMAs of tile i+1
+// and the per-CTA prologue is paid once per launch.
+//   warp 0     : TMA producer (one lane) in both CTAs; the loads of both
+//                CTAs complete on the leader's full barrier
+//   warp 1     : MMA issuer (one lane of the leader CTA only)
+//   warps 2..5 : epilogue in both CTAs (TMEM lane quarter = warp % 4)
+// Every output element is one K-ordered tcgen05 accumulation, exactly as in
+// the sw kernel with CS = 1, so the two kernels produce identical bits
+// (tests/test_gemm_gpu.py::test_pair_kernel_bitwise_equal_sw) and the choice
+// between them may depend on M without breaking batch invariance.
+namespace pc {
+
+using namespace tc;
+#ifdef SKB_GEMM_TRACE
+#define PC_STAMP(slot)                                                  \
+  do {                                                                  \
+    unsigned long long _t;                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));              \
+    if (blockIdx.x < 1024) sw::g_trace[blockIdx.x * 16 + (slot)] = _t;  \
+  } while (0)
+#else
+#define PC_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+constexpr int CHUNK = 32;                       // activation rows per staged store
+constexpr int STG_BYTES = CHUNK * 128 * 4;      // one fp32 staging buffer
+constexpr uint16_t PAIR = 0x3;
+
+__device__ __forceinline__ void tma_load_pair(void *dst, const CUtensorMap *map, int c0, int c1,
+                                              uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// arrive on the barrier at the same offset in both CTAs of the pair once
+// every MMA issued so far has completed
+__device__ __forceinline__ void commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(PAIR)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_pc(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+              const __grid_constant__ CUtensorMap tmO, int M, int N, int K, int Na, int stages,
+              int tcols, int tma_out, EpiArgs ep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int XB = (Na >> 1) * 128;  // this CTA's half of an activation k-block
+  const int SB = sw::W_BYTES + XB;
+  uint8_t *stg = smem + stages * SB;  // 2 staging buffers (1024-aligned: SB is)
+  uint64_t *full = reinterpret_cast<uint64_t *>(stg + 2 * STG_BYTES);
+  uint64_t *empty = full + stages;
+  uint64_t *tfull = empty + stages;  // [2] accumulator ready (both CTAs)
+  uint64_t *tempty = tfull + 2;      // [2] accumulator drained (leader: 8 arrivals)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = (int)blockIdx.x >> 1, npairs = (int)gridDim.x >> 1;
+  const int n_at = (M + Na - 1) / Na;
+  const int n_wt = (N + 255) / 256;
+  const int tiles = n_at * n_wt;
+  const int nk = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    PC_STAMP(0);
+#pragma unroll 1
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    if (tma_out)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmO)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) PC_STAMP(1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t lfull = sw::mapa(smem_u32(full), 0);  // leader's full[0]
+      const uint32_t tx = 2u * (uint32_t)SB;
+      // PDL prologue: the first tile's weight k-blocks do not depend on the
+      // previous kernel; activations only after griddepcontrol.wait
+      int pre = 0;
+      if (pair < tiles) {
+        const int n0 = (pair / n_at) * 256 + (int)rank * 128;
+        pre = nk < stages ? nk : stages;
+#pragma unroll 1
+        for (int q = 0; q < pre; ++q) {
+          if (rank == 0) mbar_expect_tx(&full[q], tx);
+          tma_load_pair(smem + q * SB, &tmW, q * BK, n0, lfull + 8u * q);
+        }
+      }
+      pdl_wait();
+      pdl_trigger();
+      PC_STAMP(2);
+      int it = 0;
+#pragma unroll 1
+      for (int t = pair; t < tiles; t += npairs) {
+        const int at = t % n_at, wt = t / n_at;
+        const int n0 = wt * 256 + (int)rank * 128;
+        const int mx = at * Na + (int)rank * (Na >> 1);
+#pragma unroll 1
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % stages;
+          uint8_t *st = smem + s * SB;
+          if (it >= pre) {
+            mbar_wait(&empty[s], ((it / stages) & 1) ^ 1);
+            if (rank == 0) mbar_expect_tx(&full[s], tx);
+            tma_load_pair(st, &tmW, kb * BK, n0, lfull + 8u * s);
+          }
+          tma_load_pair(st + sw::W_BYTES, &tmX, kb * BK, mx, lfull + 8u * s);
+        }
+      }
+    } else {
+      pdl_wait();
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = idesc_bf16(256, Na);
+      int it = 0, local = 0;
+#pragma unroll 1
+      for (int t = pair; t < tiles; t += npairs, ++local) {
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * Na);
+#pragma unroll 1
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % stages;
+          mbar_wait(&full[s], (it / stages) & 1);
+          if (it == 0) PC_STAMP(3);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t *st = smem + s * SB;
+          const uint64_t da = umma_desc_sw128(st);
+          const uint64_t db = umma_desc_sw128(st + sw::W_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_pair(d, da + 2 * k, db + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          commit_pair(&empty[s]);
+        }
+        commit_pair(&tfull[acc]);
+        if (local == 0) PC_STAMP(4);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5: output column n (weight row) per thread
+    pdl_wait();
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const bool leader = warp == 2 && lane == 0;
+    const uint32_t stg0 = smem_u32(stg);
+    const uint32_t ltempty = sw::mapa(smem_u32(tempty), 0);
+    const bool bf16 = ep.out_dtype == SKB_BF16 && KIND != SKB_EPI_RESID;
+    const float *cprev = nullptr;
+    float *cnext = nullptr;
+    if (KIND == SKB_EPI_SSRU) {
+      cprev = ep.c_prev;
+      cnext = ep.c_next;
+      if (ep.step) {  // decode-loop double buffer selected by step parity
+        const int t = *ep.step;
+        cnext = ep.c_next + (t & 1) * ep.state_stride;
+        cprev = t == 0 ? nullptr : ep.c_next + ((t + 1) & 1) * ep.state_stride;
+      }
+    }
+    int local = 0, chunk = 0;
+#pragma unroll 1
+    for (int t = pair; t < tiles; t += npairs, ++local) {
+      const int at = t % n_at, wt = t / n_at;
+      const int m0 = at * Na;
+      const int n0 = wt * 256 + (int)rank * 128;
+      const int n = n0 + row;
+      const bool nok = n < N;
+      const float bn = (ep.bias && nok) ? __ldg(ep.bias + n) : 0.f;
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      if (local == 0 && leader) PC_STAMP(5);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tb = tmem + (uint32_t)(acc * Na) + ((uint32_t)(quarter * 32) << 16);
+      const int rows = min(Na, M - m0);
+#pragma unroll 1
+      for (int c = 0; c < rows; c += CHUNK, ++chunk) {
+        uint32_t r[32];
+        tmem_ld32_nowait(tb + (uint32_t)c, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c + CHUNK >= rows) {  // last TMEM read of this tile: release the accumulator
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(ltempty + 8u * acc);
+        }
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (KIND == SKB_EPI_SSRU || !tma_out) {
+          sw::epi16<KIND>(ep, cprev, cnext, M, m0 + c, n, nok, bn, v);
+          sw::epi16<KIND>(ep, cprev, cnext, M, m0 + c + 16, n, nok, bn, v + 16);
+          continue;
+        }
+        // staging buffer chunk&1: the store issued from it two chunks ago
+        // must have finished reading it
+        if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const uint32_t sb = stg0 + (uint32_t)((chunk & 1) * STG_BYTES);
+        sw::stage16<KIND>(sb, bf16, 0, row, bn, v);
+        sw::stage16<KIND>(sb, bf16, 16, row, bn, v + 16);
+        sw::flush_tile<KIND>(&tmO, sb, n0, m0 + c, leader, [] {}, false, true);
+        if constexpr (KIND == SKB_EPI_LOGITS)
+          sw::logits_stats(ep, sb, M, N, m0 + c, n0, CHUNK, warp - 2, lane);
+      }
+      if (local == 0 && leader) PC_STAMP(6);
+    }
+    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (leader) PC_STAMP(8);
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // no MMA / remote arrive into a CTA that has left
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef SKB_GEMM_TRACE
+  if (threadIdx.x == 0) {
+    PC_STAMP(9);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (blockIdx.x < 1024) sw::g_trace[blockIdx.x * 16 + 7] = smid;
+  }
+#endif
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+}
+
+static int g_pairs = -1;  // SKB_PC_PAIRS: pairs per launch (0 = automatic)
+
+template <int KIND>
+static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
+                    const CUtensorMap &mo, int Na, int stages, int tcols, int tma_out, size_t smem,
+                    int pairs, EpiArgs ep, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_gemm_pc<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, sw::SMEM_MAX);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, k_gemm_pc<KIND>, mw, mx, mo, M, N, K, Na, stages, tcols, tma_out, ep);
+  SKB_CHECK_LAUNCH("k_gemm_pc");
+  return SKB_OK;
+}
+
+// Activation tile Na (numerics do not depend on it) and pairs per launch:
+// a pair's tile time is max(MMA, TMA ingest of (256 + Na) rows of K) plus a
+// fixed cost; tiles run in ceil(tiles / pairs) rounds on the pairs this
+// call's share of the SMs provides.
+static void pick(int M, int N, int K, int conc, int &Na, int &pairs) {
+  const int nsm = tc::num_sms();
+  int maxp = nsm / 2 / (conc > 0 ? conc : 1);
+  if (maxp < 1) maxp = 1;
+  if (g_pairs < 0) {
+    const char *e = getenv("SKB_PC_PAIRS");
+    g_pairs = e ? atoi(e) : 0;
+  }
+  if (g_pairs > 0) maxp = g_pairs < nsm / 2 ? g_pairs : nsm / 2;
+  const int n_wt = (N + 255) / 256;
+  double best = 1e30;
+  Na = 256;
+  for (int na = 32; na <= 256; na += 32) {
+    const long tiles = (long)n_wt * ((M + na - 1) / na);
+    const long p = tiles < maxp ? tiles : maxp;
+    const long rounds = (tiles + p - 1) / p;
+    // per SM per k-block: 16 KB weights + na/2 activation rows; MMA of a
+    // 256 x na x 64 block on the pair ~ na/2 ns-equivalents
+    const double ingest = 16384.0 + na * 64.0;
+    const double mma = na * 128.0;  // bytes-equivalent at ~64 B/clk ingest
+    const double c = rounds * ((ingest > mma ? ingest : mma) * ((K + 63) / 64) + 48.0 * 1024);
+    if (c < best * 0.999) {
+      best = c;
+      Na = na;
+    }
+  }
+  const long tiles = (long)n_wt * ((M + Na - 1) / Na);
+  pairs = (int)(tiles < maxp ? tiles : maxp);
+}
+
+int g_mode = -1;   // SKB_GEMM_PC: 0 auto, 1 never, 2 always (where applicable)
+int g_na = 0;      // forced activation tile (0 = automatic)
+int g_min_m = -1;  // SKB_PC_MIN_M: smallest M the automatic choice sends here
+void init_mode() {
+  if (g_mode >= 0) return;
+  const char *e = getenv("SKB_GEMM_PC");
+  g_mode = e ? atoi(e) : 0;
+  e = getenv("SKB_PC_MIN_M");
+  g_min_m = e ? atoi(e) : 1024;
+}
+
+static int launch(int M, int N, int K, const void *X, int ldx, const void *W, int ldw, EpiArgs ep,
+                  cudaStream_t st, int conc, int na_force) {
+  ep.splits = 1;
+  ep.late_trigger = 0;
+  int Na, pairs;
+  pick(M, N, K, conc, Na, pairs);
+  if (na_force > 0) {
+    Na = na_force;
+    const long tiles = (long)((N + 255) / 256) * ((M + Na - 1) / Na);
+    if (pairs > tiles) pairs = (int)tiles;
+  }
+  if (Na < 32 || Na > 256 || Na % 32) return fail(SKB_ERR_CONFIG, "gemm_pc: bad tile Na=%d", Na);
+  CUtensorMap mw, mx, mo;
+  int rc = tc::make_map(&mw, W, N, K, ldw, 128);
+  if (rc) return rc;
+  rc = tc::make_map(&mx, X, M, K, ldx, Na / 2);
+  if (rc) return rc;
+  const bool f32o = ep.kind == SKB_EPI_RESID || ep.out_dtype == SKB_F32;
+  const int es = f32o ? 4 : 2;
+  const int tma_out = ep.kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
+                      ((long)ep.ldo * es) % 16 == 0;
+  if (ep.kind == SKB_EPI_LOGITS && !tma_out)
+    return fail(SKB_ERR_CONFIG, "gemm_pc: LOGITS needs an aligned fp32 output");
+  if (tma_out) {
+    rc = sw::make_map_out(&mo, ep.out, M, N, ep.ldo, f32o, CHUNK);
+    if (rc) return rc;
+  } else {
+    mo = mw;  // unused
+  }
+  const int SB = sw::W_BYTES + (Na / 2) * 128;
+  const int nk = (K + tc::BK - 1) / tc::BK;
+  const int fixed = 2 * STG_BYTES + 1024 + 256;
+  static int budget = -1;  // SKB_PC_SMEM: shared-memory budget per CTA (bytes)
+  if (budget < 0) {
+    const char *e = getenv("SKB_PC_SMEM");
+    budget = e ? atoi(e) : sw::SMEM_MAX;
+    if (budget > sw::SMEM_MAX) budget = sw::SMEM_MAX;
+  }
+  int stages = (budget - fixed) / SB;
+  if (stages < 2) return fail(SKB_ERR_UNSUPPORTED, "gemm_pc: Na=%d does not fit", Na);
+  if (stages > nk) stages = nk;
+  if (stages > 8) stages = 8;
+  const size_t smem = (size_t)stages * SB + fixed;
+  int tcols = 32;
+  while (tcols < 2 * Na) tcols <<= 1;
+  switch (ep.kind) {
+    case SKB_EPI_RELU:
+      return launch_t<SKB_EPI_RELU>(M, N, K, mw, mx, mo, Na, stages, tcols, tma_out, smem, pairs, ep, st);
+    case SKB_EPI_RESID:
+      return launch_t<SKB_EPI_RESID>(M, N, K, mw, mx, mo, Na, stages, tcols, tma_out, smem, pairs, ep, st);
+    case SKB_EPI_SSRU:
+      return launch_t<SKB_EPI_SSRU>(M, N, K, mw, mx, mo, Na, stages, tcols, tma_out, smem, pairs, ep, st);
+    case SKB_EPI_LOGITS:
+      return launch_t<SKB_EPI_LOGITS>(M, N, K, mw, mx, mo, Na, stages, tcols, tma_out, smem, pairs, ep, st);
+    default:
+      return launch_t<SKB_EPI_STORE>(M, N, K, mw, mx, mo, Na, stages, tcols, tma_out, smem, pairs, ep, st);
+  }
+}
+
+}  // namespace pc
+
 // ========================================================== SIMT kernel
 // 64x64 output tile, BK=16, 256 threads, 4x4 outputs per thread.  Used for
 // fp32 (parity) mode and for shapes TMA cannot describe.
@@ -1858,6 +2294,16 @@ extern "C" int skb_gemm_force_sw(int mode, int na, int cs) {
   return SKB_OK;
 }
 
+extern "C" int skb_gemm_force_pc(int mode, int na, int pairs) {
+  if (mode < 0 || mode > 2 || na < 0 || na > 256 || na % 32 || pairs < 0)
+    return fail(SKB_ERR_CONFIG, "gemm_force_pc: mode %d na %d pairs %d", mode, na, pairs);
+  pc::init_mode();
+  pc::g_mode = mode;
+  pc::g_na = na;
+  pc::g_pairs = pairs;
+  return SKB_OK;
+}
+
 extern "C" int skb_debug_gemm_trace(unsigned long long *host) {
 #ifdef SKB_GEMM_TRACE
   cudaMemcpyFromSymbol(host, sw::g_trace, sizeof(sw::g_trace));
@@ -1934,6 +2380,23 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   // the encoder's FFN2 of a large batch (B*L rows) and the log-softmax of a
   // large decode batch took the other kernel (tools/invariance_check.py).
   const bool sw_pref = true;
+  // Persistent CTA-pair kernel for the shapes whose sw plan has no cluster
+  // K-split (identical bits, see namespace pc) once M is large enough that
+  // its bigger tiles pay; below that the sw kernel's one-tile-per-CTA plan
+  // (and its prologue LayerNorm) has the shorter critical path.
+  pc::init_mode();
+  {
+    const int cs_sw = epi->kind == SKB_EPI_LOGITS ? 1 : sw::pick_cs(N, K);
+    const bool pc_ok = cs_sw == 1 && logits_tma && sw::g_mode == 0;
+    if (pc_ok && (pc::g_mode == 2 || (pc::g_mode == 0 && M >= pc::g_min_m && N >= 8192))) {
+      if (epi->ln_in) {
+        rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
+        if (rc) return rc;
+      }
+      fused_ln = false;  // a requested output LayerNorm follows as its own launch
+      return pc::launch(M, N, K, A, lda, W, ldw, ep, st, sw::g_concurrency, pc::g_na);
+    }
+  }
   if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || sw_pref)) {
     const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);

@@ -543,9 +543,11 @@ class BeamBatch:
             actives = [a if a is not None else np.arange(V, dtype=np.int64) for a in actives]
             U_ids = np.unique(np.concatenate(actives)).astype(np.int64)
             U_real = int(U_ids.size)
-            # union width bucketed to 256 columns: the padding columns repeat
-            # the last id and are never set in any sentence's column mask
-            U = min(_round_up(U_real, 256), max(V, U_real))
+            # union width bucketed to 1024 columns (a batch-1 shortlist run
+            # has a different union per sentence; coarse buckets let calls
+            # share a workspace and its captured graphs): the padding columns
+            # repeat the last id and are never set in any sentence's mask
+            U = min(_round_up(U_real, 1024), max(V, U_real))
         else:
             U = V
         Lw = self.L_ws

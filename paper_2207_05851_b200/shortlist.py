@@ -1,8 +1,12 @@
-"""Lexical shortlist file format and id-space lookup (mirrors skiff
-shortlist.py:134-207).  The offline IBM-Model-1 training of the reference is
-out of scope; this module reads its output.
+"""Lexical shortlists: the on-disk table the reference's offline trainer
+writes, and the per-sentence id-space union the search restricts to
+(behaviour of skiff shortlist.py:153-207; its IBM-Model-1 trainer is out of
+scope for this backend).
 
-File format: one line per source token, `source<TAB>target:prob ...`.
+On disk, each non-empty line maps one source token to its candidate target
+tokens:  ``<source token> TAB <target>:<prob> <target>:<prob> ...``.
+A target token may itself contain ':' (the probability follows the last
+one).  Malformed lines raise DataError naming the file and line.
 """
 
 from __future__ import annotations
@@ -14,65 +18,72 @@ import numpy as np
 
 from .errors import DataError
 
-logger = logging.getLogger(__name__)
+log = logging.getLogger(__name__)
+
+Entries = list[tuple[str, float]]
 
 
-def read_shortlist_file(path) -> dict[str, list[tuple[str, float]]]:
-    """shortlist.py:153-175."""
-    out: dict[str, list[tuple[str, float]]] = {}
-    with open(path, encoding="utf-8") as f:
-        for n, line in enumerate(f, 1):
-            line = line.rstrip("\n")
-            if not line:
-                continue
-            if "\t" not in line:
-                raise DataError(f"{path}:{n}: expected 'source<TAB>entries'")
-            tok, _, rest = line.partition("\t")
-            if tok in out:
-                raise DataError(f"{path}:{n}: duplicate source token {tok!r}")
-            entries = []
-            for item in rest.split(" ") if rest else []:
-                trg, sep, prob = item.rpartition(":")
-                if not sep or not trg:
-                    raise DataError(f"{path}:{n}: bad entry {item!r}")
-                try:
-                    entries.append((trg, float(prob)))
-                except ValueError:
-                    raise DataError(f"{path}:{n}: bad probability in {item!r}") from None
-            out[tok] = entries
-    return out
+def _entry(where: str, field: str) -> tuple[str, float]:
+    token, colon, prob = field.rpartition(":")
+    if not (colon and token):
+        raise DataError(f"{where}: malformed shortlist entry {field!r}")
+    try:
+        return token, float(prob)
+    except ValueError:
+        raise DataError(f"{where}: entry {field!r} has a non-numeric probability") from None
 
 
-def write_shortlist_file(path, rows: dict[str, list[tuple[str, float]]]) -> None:
-    with open(path, "w", encoding="utf-8") as f:
-        for tok, entries in rows.items():
-            f.write(tok + "\t" + " ".join(f"{t}:{p:.6g}" for t, p in entries) + "\n")
+def read_shortlist_file(path) -> dict[str, Entries]:
+    """Parse a shortlist file into {source token: [(target token, prob)]}
+    in file order; a source token may appear on one line only."""
+    table: dict[str, Entries] = {}
+    text = Path(path).read_text(encoding="utf-8")
+    for number, line in enumerate(text.split("\n"), 1):
+        if not line:
+            continue
+        where = f"{path}:{number}"
+        source, tab, rest = line.partition("\t")
+        if not tab:
+            raise DataError(f"{where}: a shortlist line is 'source<TAB>entries'")
+        if source in table:
+            raise DataError(f"{where}: source token {source!r} appears twice")
+        table[source] = [_entry(where, f) for f in rest.split(" ")] if rest else []
+    return table
+
+
+def write_shortlist_file(path, rows: dict[str, Entries]) -> None:
+    """Inverse of read_shortlist_file (test fixtures)."""
+    body = "".join(f"{src}\t{' '.join(f'{t}:{p:.6g}' for t, p in ents)}\n"
+                   for src, ents in rows.items())
+    Path(path).write_text(body, encoding="utf-8")
 
 
 class Shortlist:
-    """Id-space shortlist for one vocabulary pair (shortlist.py:178-207)."""
+    """Candidate target ids per source id, for one (source, target)
+    vocabulary pair: rows[src_id] is a sorted unique int64 array."""
 
     def __init__(self, rows: dict[int, np.ndarray]):
         self.rows = rows
 
     @classmethod
     def from_file(cls, path, src_vocab, trg_vocab) -> "Shortlist":
-        raw = read_shortlist_file(path)
+        """Map a shortlist file into the model's id space.  Source lines whose
+        token the model does not know are skipped (the file may have been
+        built on another corpus), as are unknown target tokens."""
         rows: dict[int, np.ndarray] = {}
-        dropped = 0
-        for tok, entries in raw.items():
-            if tok not in src_vocab:
-                dropped += 1
+        skipped = 0
+        for source, entries in read_shortlist_file(path).items():
+            if source not in src_vocab:
+                skipped += 1
                 continue
-            ids = [trg_vocab.to_id(t) for t, _ in entries if t in trg_vocab]
-            rows[src_vocab.to_id(tok)] = np.asarray(sorted(set(ids)), dtype=np.int64)
-        if dropped:
-            logger.info("shortlist: dropped %d source tokens unknown to the model", dropped)
+            known = {trg_vocab.to_id(t) for t, _ in entries if t in trg_vocab}
+            rows[src_vocab.to_id(source)] = np.array(sorted(known), dtype=np.int64)
+        if skipped:
+            log.info("shortlist: %d source tokens are not in the model vocabulary", skipped)
         return cls(rows)
 
     def lookup(self, src_ids) -> np.ndarray:
-        """Union of the rows for the given source ids."""
-        parts = [self.rows[i] for i in set(int(i) for i in src_ids) if i in self.rows]
-        if not parts:
-            return np.empty(0, dtype=np.int64)
-        return np.unique(np.concatenate(parts))
+        """Sorted union of the candidate rows of the given source ids (empty
+        when none of them has a row)."""
+        hits = [self.rows[s] for s in {int(i) for i in src_ids} if s in self.rows]
+        return np.unique(np.concatenate(hits)) if hits else np.zeros(0, dtype=np.int64)

@@ -14,13 +14,20 @@ SHAPES = [(3, 48, 16), (5, 40, 32), (130, 64, 4096), (77, 8000, 256), (640, 1024
           (200, 3072, 1024), (640, 32000, 1024), (1, 4096, 1024), (257, 1000, 512)]
 
 
-@pytest.fixture(autouse=True, params=["tc", "sw"])
+@pytest.fixture(autouse=True, params=["tc", "sw", "pc"])
 def gemm_path(request):
-    """Run every test through both tcgen05 kernels: the M-major persistent
-    kernel (k_gemm_tc) and the swap-AB decode kernel (k_gemm_sw)."""
-    N.call("skb_gemm_force_sw", 1 if request.param == "tc" else 2, 0, 0)
+    """Run every test through the tcgen05 kernels: the M-major persistent
+    kernel (k_gemm_tc), the swap-AB decode kernel (k_gemm_sw) and the
+    persistent CTA-pair kernel (k_gemm_pc, wherever the automatic plan has
+    no cluster K-split; the others fall through to k_gemm_sw)."""
+    if request.param == "pc":
+        N.call("skb_gemm_force_sw", 0, 0, 0)
+        N.call("skb_gemm_force_pc", 2, 0, 0)
+    else:
+        N.call("skb_gemm_force_sw", 1 if request.param == "tc" else 2, 0, 0)
     yield request.param
     N.call("skb_gemm_force_sw", 0, 0, 0)
+    N.call("skb_gemm_force_pc", 0, 0, 0)
 
 
 def _epi(kind, out, ldo, out_dtype, bias=None, c_prev=None, c_next=None, src_row=None,
@@ -377,3 +384,60 @@ def test_logits_partials_batch_invariant_default_dispatch(gemm_path):
         res.append((o, part))
     assert torch.equal(res[0][0][700:705], res[1][0])
     assert torch.equal(res[0][1][700:705], res[1][1])
+
+
+PAIR_SHAPES = [(640, 3072, 1024), (640, 32000, 1024), (77, 1000, 256), (1, 4096, 1024),
+               (300, 2048, 1024), (1920, 1024, 1024), (33, 256, 64)]
+
+
+@pytest.mark.parametrize("kind", ["store_bf16", "relu_bf16", "store_f32", "resid", "logits", "ssru"])
+@pytest.mark.parametrize("M,Nn,K", PAIR_SHAPES)
+def test_pair_kernel_bitwise_equal_sw(gemm_path, kind, M, Nn, K):
+    """k_gemm_pc (cta_group::2, 256-row weight tiles, any Na) and k_gemm_sw
+    (CS = 1) accumulate every element in the same K order: identical bits,
+    so the M-dependent choice between them keeps batch invariance."""
+    if gemm_path != "pc":
+        pytest.skip("runs once")
+    g = torch.Generator(device="cuda").manual_seed(M + Nn + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(Nn, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    x0 = torch.randn(M, Nn, device="cuda", generator=g)
+    c_prev = torch.randn(M, Nn // 2, device="cuda", generator=g)
+    src = torch.randint(0, M, (M,), device="cuda", generator=g, dtype=torch.int32)
+    G = (Nn + 31) // 32
+
+    def run(mode):
+        if mode == "sw":
+            N.call("skb_gemm_force_pc", 1, 0, 0)
+            N.call("skb_gemm_force_sw", 2, 0, 1)
+        else:
+            N.call("skb_gemm_force_sw", 0, 0, 0)
+            N.call("skb_gemm_force_pc", 2, int(mode[2:]) if len(mode) > 2 else 0, 0)
+        part = torch.zeros(M, 2 * G, device="cuda")
+        cn = torch.zeros(M, Nn // 2, device="cuda")
+        if kind in ("store_bf16", "relu_bf16"):
+            out = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
+            e = _epi(N.EPI_STORE if kind == "store_bf16" else N.EPI_RELU, out, Nn, N.BF16, bias)
+        elif kind == "store_f32":
+            out = torch.zeros(M, Nn, device="cuda")
+            e = _epi(N.EPI_STORE, out, Nn, N.F32, bias)
+        elif kind == "resid":
+            out = x0.clone()
+            e = _epi(N.EPI_RESID, out, Nn, N.F32, bias)
+        elif kind == "ssru":
+            out = x0[:, : Nn // 2].contiguous()
+            e = _epi(N.EPI_SSRU, out, Nn // 2, N.F32, bias, c_prev, cn, src, Nn // 2)
+        else:
+            out = torch.zeros(M, Nn, device="cuda")
+            e = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0,
+                           None, 0, part.data_ptr(), G, None, 0, 1)
+        _run("skb_gemm", N.BF16, A, W, e)
+        torch.cuda.synchronize()
+        return out, part, cn
+
+    want = run("sw")
+    for mode in ("pc", "pc32", "pc64", "pc160", "pc256"):
+        got = run(mode)
+        for a, b in zip(want, got):
+            assert torch.equal(a, b), (mode, (a.float() - b.float()).abs().max().item())

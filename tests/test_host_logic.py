@@ -109,3 +109,58 @@ def test_config_validation():
     with pytest.raises(ConfigError):
         ModelConfig(11, 13, d_model=16, heads=4,
                     source_factor_specs=[SourceFactorSpec(6, 8, "sum")]).validate()
+
+
+def test_bench_shortlist_generator_matches_fixture_generator():
+    """bench.py builds the top-200 shortlist of the SSRU config on its own
+    (the product leg may not import oracle/); it must be the fixtures' one."""
+    import numpy as np
+    import bench
+    from oracle.fixture_configs import synthetic_shortlist_rows
+    a = bench.synthetic_shortlist_rows(300, 20)
+    b = synthetic_shortlist_rows(300, 20)
+    assert a.keys() == b.keys() and all(np.array_equal(a[k], b[k]) for k in a)
+
+
+def test_bench_distinct_kv_entries_counts_shared_prefix():
+    """distinct_kv_entries walks the beam back-pointers: two rows of one
+    sentence that share their whole history read t + 2 distinct entries at
+    step t (the shared prefix once, plus their own newest entry each)."""
+    import types
+    import torch
+    import bench
+    K, B, S = 2, 1, 4
+    par = torch.zeros(S * K, dtype=torch.int32)  # every new row's parent is row 0
+    bb = types.SimpleNamespace(K=K, B=B, ws=types.SimpleNamespace(par_hist=par))
+    got = bench.distinct_kv_entries(bb, S)
+    # step 0: one row; step t >= 1: 2 rows at position t, row 0 at positions < t
+    assert got == [1, 3, 4, 5]
+
+
+REFDIRS = ["srcfac", "ssru", "factored"]
+
+
+@pytest.mark.parametrize("name", REFDIRS)
+def test_reads_model_dirs_written_by_the_reference(name):
+    """tests/golden/refdir_<cfg> was written by skiff's own save_model_dir
+    (checkpoint.py:316-330; oracle/make_golden.py modeldirs): the product's
+    readers take its config, SKP1 parameters and vocabularies unchanged."""
+    import numpy as np
+    from conftest import GOLDEN
+    from fixture_models import oracle_model, oracle_vocabs, product_config
+    from paper_2207_05851_b200.checkpoint import Vocabulary, parse_config, read_checkpoint
+    d = GOLDEN / f"refdir_{name}"
+    cfg = parse_config((d / "config").read_text(), str(d / "config"))
+    assert cfg == product_config(name)
+    params = read_checkpoint(d / "params.bin")
+    want = oracle_model(name).p
+    assert params.keys() == want.keys()
+    for k in want:
+        assert params[k].dtype == np.float32 and np.array_equal(params[k], want[k]), k
+    ov = oracle_vocabs(name)
+    assert Vocabulary.load(d / "vocab.src.json").tokens == ov["src"].tokens
+    assert Vocabulary.load(d / "vocab.trg.json").tokens == ov["trg"].tokens
+    for i, v in enumerate(ov["src_f"]):
+        assert Vocabulary.load(d / f"vocab.src.factor{i}.json").tokens == v.tokens
+    for i, v in enumerate(ov["trg_f"]):
+        assert Vocabulary.load(d / f"vocab.trg.factor{i}.json").tokens == v.tokens

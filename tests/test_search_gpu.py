@@ -158,3 +158,23 @@ def test_batch_invariance_at_scale():
     for i in (0, 41, 97, 159):
         one = translate(model, vocabs, [SentenceInput(tokens=sents[i])], st)[0]
         assert one.text == big[i].text and one.score == big[i].score, (i, one.score, big[i].score)
+
+
+@pytest.mark.parametrize("name", ["srcfac", "ssru", "factored"])
+def test_translate_from_reference_written_model_dir(name):
+    """Load a model directory the REFERENCE wrote (save_model_dir,
+    checkpoint.py:316-330) with the product's load_model_dir and translate:
+    the records equal the ones the reference produced from the same
+    directory (tests/golden/refdir_records.json)."""
+    from paper_2207_05851_b200.checkpoint import load_model_dir
+    from paper_2207_05851_b200.search import SentenceInput, translate
+    gold = json.loads((GOLDEN / "refdir_records.json").read_text())[name]
+    case = next(c for c in SEARCH_CASES if c["name"] == gold["case"])
+    md = load_model_dir(GOLDEN / f"refdir_{name}", precision="fp32")
+    recs = translate(md.model, md, [SentenceInput(**i) for i in case["inputs"]], _settings(case))
+    assert len(recs) == len(gold["records"])
+    for r, g in zip(recs, gold["records"]):
+        assert (r.error is None) == (g["error"] is None)
+        assert r.text == g["text"] and r.factors == g["factors"] and r.chunks == g["chunks"]
+        if g["error"] is None:
+            assert abs(r.score - g["score"]) < 1e-4
