@@ -145,6 +145,26 @@ int skb_gemm_force_sw(int mode, int na, int cs);
  * launch; 0 = choose automatically.  Bitwise equal to the swap-AB kernel. */
 int skb_gemm_force_pc(int mode, int na, int pairs);
 
+/*
+ * INT8 feed-forward path (replaces skiff quant.py:40-53 quantize_rows,
+ * :65-78 _gemm_i8_numba, :99-104 quantize_activations and :121-132
+ * QuantizedLinear.__call__).
+ *
+ * skb_quantize_rows: per-row symmetric int8 quantization of fp32 rows,
+ * scale = max|row| / 127 (1 for a zero row), q = clip(round-half-away(x /
+ * scale), -127, 127); bit-identical to the reference's float32 arithmetic.
+ * Used offline for weights and per step for activations.
+ *
+ * skb_gemm_i8: acc = A . W^T in exact int32 (tcgen05 kind::i8), then
+ * out = (float(acc) * a_scale[m]) * w_scale[n] followed by the epilogue
+ * (STORE / RELU with bias, or RESID x += ... + bias).  A [M, lda] and
+ * W [N, ldw] int8 K-major, K % 16 == 0, 16-byte aligned.
+ */
+int skb_quantize_rows(int rows, int k, const float *x, int ldx, void *q, int ldq, float *scales,
+                      void *stream);
+int skb_gemm_i8(int M, int N, int K, const void *A, int lda, const float *a_scale, const void *W,
+                int ldw, const float *w_scale, const skb_epilogue *epi, void *stream);
+
 /* Number of independent decode streams the caller runs concurrently on this
  * device (default 1).  The swap-AB GEMM sizes its tiles for its share of the
  * SMs (fewer, larger tiles ingest fewer bytes in total).  Affects launches

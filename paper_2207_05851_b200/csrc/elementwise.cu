@@ -377,3 +377,49 @@ extern "C" int skb_set_device(int device) {
   if (e != cudaSuccess) return fail(SKB_ERR_LAUNCH, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
   return SKB_OK;
 }
+
+// ------------------------------------------------- int8 row quantization
+// quant.py:40-53 (weights, offline) and :99-104 (activations, per call):
+// scale = max|row| / 127 (1 for an all-zero row), q = clip(round half away
+// from zero (x / scale), -127, 127).  Every operation is the reference's
+// float32 operation (IEEE division, |v| + 0.5 rounded, then floor), so the
+// integers and scales are bit-identical.  One CTA per row.
+namespace skb {
+__global__ void __launch_bounds__(128) k_quantize_rows(int rows, int k, const float *__restrict__ x,
+                                                       int ldx, int8_t *__restrict__ q, int ldq,
+                                                       float *__restrict__ scales) {
+  PDL_ENTRY();
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const float *xr = x + (size_t)r * ldx;
+  float m = 0.f;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) m = fmaxf(m, fabsf(xr[c]));
+  m = warp_max(m);
+  __shared__ float wm[4];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = fmaxf(fmaxf(wm[0], wm[1]), fmaxf(wm[2], wm[3]));
+  const float scale = m > 0.f ? __fdiv_rn(m, 127.0f) : 1.0f;
+  if (threadIdx.x == 0) scales[r] = scale;
+  int8_t *qr = q + (size_t)r * ldq;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    const float v = __fdiv_rn(xr[c], scale);
+    float a = floorf(__fadd_rn(fabsf(v), 0.5f));
+    a = fminf(a, 127.0f);
+    qr[c] = (int8_t)(v < 0.f ? -(int)a : (int)a);
+  }
+}
+}  // namespace skb
+
+extern "C" int skb_quantize_rows(int rows, int k, const float *x, int ldx, void *q, int ldq,
+                                 float *scales, void *stream) {
+  if (rows < 0 || k <= 0 || ldx < k || ldq < k)
+    return fail(SKB_ERR_SHAPE, "quantize_rows: rows=%d k=%d ldx=%d ldq=%d", rows, k, ldx, ldq);
+  if (k > (1 << 31) / (127 * 127))
+    return fail(SKB_ERR_CONFIG, "quantize_rows: inner extent %d would overflow int32 accumulation", k);
+  if (rows == 0) return SKB_OK;
+  launch_k(k_quantize_rows, rows, 128, 0, as_stream(stream), rows, k, x, ldx,
+           reinterpret_cast<int8_t *>(q), ldq, scales);
+  SKB_CHECK_LAUNCH("k_quantize_rows");
+  return SKB_OK;
+}

@@ -56,6 +56,10 @@ struct EpiArgs {
   const float *lnx_b;
   float lnx_eps;
   int late_trigger;  // swap-AB kernel: release dependents once the accumulator is ready
+  // int8 GEMM (skb_gemm_i8): per-row scales of the int8 activations [M] and
+  // weights [N]; out = (f32(acc) * a_scale[m]) * w_scale[n] (+bias ...)
+  const float *a_scale;
+  const float *w_scale;
 };
 
 // Partial log-softmax statistics of `cnt` consecutive logits of row m
@@ -270,6 +274,28 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+// Instruction descriptor, kind::i8: s8 x s8 -> s32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_s8(int M, int N) {
+  return (2u << 4)                      // c_format = S32
+         | (1u << 7)                    // a_format = signed 8-bit
+         | (1u << 10)                   // b_format = signed 8-bit
+         | ((uint32_t)(N >> 3) << 17)   // n_dim
+         | ((uint32_t)(M >> 4) << 24);  // m_dim
+}
+
+// K = 32 int8 per instruction: the same 32-byte step through the SW128 atom
+// as K = 16 bf16, so the smem pipeline is byte-for-byte the bf16 one.
+__device__ __forceinline__ void umma_s8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
@@ -668,10 +694,11 @@ struct MapKeyHash {
 
 // Tensor maps are host-side descriptors; cache them per (pointer, shape) so
 // steady-state calls (and CUDA-graph capture) cost no re-encoding.
-static int make_map(CUtensorMap *out, const void *ptr, int rows, int cols, int ld, int box_rows) {
+static int make_map(CUtensorMap *out, const void *ptr, int rows, int cols, int ld, int box_rows,
+                    bool i8 = false) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  MapKey key{ptr, rows, cols, ld, box_rows};
+  MapKey key{ptr, rows, cols, i8 ? -ld : ld, box_rows};
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
@@ -682,11 +709,13 @@ static int make_map(CUtensorMap *out, const void *ptr, int rows, int cols, int l
   }
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(SKB_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  // one box row = one 128-byte swizzle atom: 64 bf16 or 128 int8 elements
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * (i8 ? 1 : 2)};
+  cuuint32_t box[2] = {(cuuint32_t)(i8 ? 2 * BK : BK), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+  CUresult r = fn(out, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void *>(ptr), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SKB_ERR_LAUNCH, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -1092,7 +1121,7 @@ __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int
 //   warps 2..5 : epilogue, TMEM lane quarter = warp % 4
 // grid (weight tiles x activation tiles, CS), cluster (1, CS): the CS CTAs
 // of a cluster share the output tile and split K.
-template <int KIND, int CS, bool LNX = false>
+template <int KIND, int CS, bool LNX = false, bool I8 = false>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_sw(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
               const __grid_constant__ CUtensorMap tmO, int M, int N, int K, int Na, int stages,
@@ -1122,7 +1151,8 @@ __global__ void __launch_bounds__(192, 1)
   const int n_at = (M + Na - 1) / Na;
   const int at = (int)blockIdx.x % n_at, wt = (int)blockIdx.x / n_at;
   const int m0 = at * Na, n0 = wt * 128;
-  const int nk = (K + BK - 1) / BK;
+  constexpr int KBE = I8 ? 2 * BK : BK;  // elements per 128-byte k-block
+  const int nk = (K + KBE - 1) / KBE;
   const int kb0 = rank * nk / CS, kb1 = (rank + 1) * nk / CS;
   const int nkc = kb1 - kb0;
   int tcols = 32;
@@ -1169,14 +1199,14 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
       for (int q = 0; q < pre; ++q) {
         mbar_expect_tx(&full[q], sbx);
-        if (ldbg != 5) tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * BK, n0, &full[q]);
+        if (ldbg != 5) tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * KBE, n0, &full[q]);
       }
       pdl_wait();
       if (!ep.late_trigger) pdl_trigger();
       SW_STAMP(2);
 #pragma unroll 1
       for (int q = 0; q < pre; ++q)
-        if (ldbg != 4 && !lnx) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * BK, m0, &full[q]);
+        if (ldbg != 4 && !lnx) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * KBE, m0, &full[q]);
 #pragma unroll 1
       for (int it = pre; it < nkc; ++it) {
         const int s = it % stages;
@@ -1184,8 +1214,8 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t *st = smem + s * SB;
         mbar_expect_tx(&full[s], sbx);
-        if (ldbg != 5) tma_load_2d(st, &tmW, (kb0 + it) * BK, n0, &full[s]);
-        if (ldbg != 4 && !lnx) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * BK, m0, &full[s]);
+        if (ldbg != 5) tma_load_2d(st, &tmW, (kb0 + it) * KBE, n0, &full[s]);
+        if (ldbg != 4 && !lnx) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * KBE, m0, &full[s]);
       }
     } else {
       pdl_wait();
@@ -1193,7 +1223,7 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     pdl_wait();
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, Na);
+      const uint32_t idesc = I8 ? idesc_s8(128, Na) : idesc_bf16(128, Na);
       if (lnx) {
         mbar_wait(xready, 0);
         SW_STAMP(14);
@@ -1208,8 +1238,12 @@ __global__ void __launch_bounds__(192, 1)
         const uint64_t da = umma_desc_sw128(st);
         const uint64_t db = umma_desc_sw128(lnx ? panel + (size_t)(kb0 + it) * Na * 128 : st + W_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (it > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < BK / 16; ++k) {
+          if constexpr (I8)
+            umma_s8(tmem, da + 2 * k, db + 2 * k, idesc, (it > 0 || k > 0) ? 1u : 0u);
+          else
+            umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (it > 0 || k > 0) ? 1u : 0u);
+        }
         umma_commit(&empty[s]);
       }
       umma_commit(tfull);
@@ -1274,6 +1308,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t stg = smem_u32(smem) + (uint32_t)stg_off;
       const bool bf16 = ep.out_dtype == SKB_BF16 && KIND != SKB_EPI_RESID;
 #pragma unroll 1
+      const float wsc = (I8 && nok) ? __ldg(ep.w_scale + n) : 0.f;
       for (int c = 0; c < Na && m0 + c < M; c += 16) {
         float v[16];
         if (dbg != 2)
@@ -1281,6 +1316,16 @@ __global__ void __launch_bounds__(192, 1)
         else
           for (int i = 0; i < 16; ++i) v[i] = (float)i;
         if (dbg == 1) continue;
+        if constexpr (I8) {
+          // quant.py:124-128: (float32(acc) * a_scale) * w_scale, each
+          // product rounded on its own (no FMA), the bias added after
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int m = m0 + c + i;
+            const float as = m < M ? __ldg(ep.a_scale + m) : 0.f;
+            v[i] = __fmul_rn(__fmul_rn(__int2float_rn(__float_as_int(v[i])), as), wsc);
+          }
+        }
         if (KIND != SKB_EPI_SSRU && tma_out)
           stage16<KIND>(stg, bf16, c, row, bn, v);
         else
@@ -1452,13 +1497,13 @@ static int make_map_out(CUtensorMap *out, const void *ptr, int rows, int cols, i
   return SKB_OK;
 }
 
-template <int KIND, int CS, bool LNX = false>
+template <int KIND, int CS, bool LNX = false, bool I8 = false>
 static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
                     const CUtensorMap &mo, int Na, int stages, int stg_off, int tma_out,
                     size_t smem, EpiArgs ep, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_sw<KIND, CS, LNX>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaFuncSetAttribute(k_gemm_sw<KIND, CS, LNX, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     attr_set = true;
   }
   const int n_wt = (N + 127) / 128, n_at = (M + Na - 1) / Na;
@@ -1483,7 +1528,7 @@ static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMa
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS, LNX>, mw, mx, mo, M, N, K, Na, stages, stg_off,
+  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS, LNX, I8>, mw, mx, mo, M, N, K, Na, stages, stg_off,
                      tma_out, ep);
   SKB_CHECK_LAUNCH("k_gemm_sw");
   return SKB_OK;
@@ -1513,7 +1558,7 @@ static int launch_k2(int M, int N, int K, const CUtensorMap &mw, const CUtensorM
 extern int g_concurrency;
 
 static int launch(int M, int N, int K, const void *X, int ldx, const void *W, int ldw, EpiArgs ep,
-                  cudaStream_t st, int Na, int CS) {
+                  cudaStream_t st, int Na, int CS, bool i8 = false) {
   ep.splits = 1;
   // When the dependent grid launches (PDL trigger): right after this grid's
   // own dependency wait with one decode stream (the next kernel's CTAs become
@@ -1538,16 +1583,19 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   if (Na < 16 || Na > 256 || Na % 16 || !(CS == 1 || CS == 2 || CS == 4) ||
       (CS > 1 && Na % (4 * CS)))
     return fail(SKB_ERR_CONFIG, "gemm_sw: bad tile Na=%d CS=%d", Na, CS);
+  if (i8 && (CS != 1 || ep.lnx || ep.ln_out || ep.kind == SKB_EPI_SSRU || ep.kind == SKB_EPI_LOGITS))
+    return fail(SKB_ERR_CONFIG, "gemm_sw: the int8 path has no K split, LayerNorm, SSRU or LOGITS epilogue");
   CUtensorMap mw, mx;
-  int rc = tc::make_map(&mw, W, N, K, ldw, 128);
+  int rc = tc::make_map(&mw, W, N, K, ldw, 128, i8);
   if (rc) return rc;
-  rc = tc::make_map(&mx, X, M, K, ldx, Na);
+  rc = tc::make_map(&mx, X, M, K, ldx, Na, i8);
   if (rc) return rc;
   const bool lnx = ep.lnx != nullptr;
   if (lnx && (CS != 1 || K % 128 || K > 1024 || ep.kind == SKB_EPI_RESID || ep.kind == SKB_EPI_SSRU))
     return fail(SKB_ERR_CONFIG, "gemm_sw: prologue LayerNorm needs CS=1, K %% 128 == 0 <= 1024");
   const int SB = lnx ? W_BYTES : W_BYTES + Na * 128;
-  const int nk = (K + tc::BK - 1) / tc::BK;
+  const int kbe = i8 ? 2 * tc::BK : tc::BK;
+  const int nk = (K + kbe - 1) / kbe;
   const int nkc = (nk + CS - 1) / CS;
   const int panel_bytes = lnx ? nk * Na * 128 : 0;
   // TMA-store epilogue: the output tile is staged in the (drained) ring
@@ -1582,6 +1630,13 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
     if (rc) return rc;
   } else {
     mo = mw;  // unused
+  }
+  if (i8) {
+    if (ep.kind == SKB_EPI_RELU)
+      return launch_t<SKB_EPI_RELU, 1, false, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+    if (ep.kind == SKB_EPI_RESID)
+      return launch_t<SKB_EPI_RESID, 1, false, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+    return launch_t<SKB_EPI_STORE, 1, false, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
   }
   switch (ep.kind) {
     case SKB_EPI_RELU:
@@ -2210,6 +2265,8 @@ static EpiArgs to_args(const skb_epilogue *e) {
   a.lnx_b = e->ln_in_bias;
   a.lnx_eps = e->ln_in_eps;
   a.late_trigger = 0;
+  a.a_scale = nullptr;
+  a.w_scale = nullptr;
   return a;
 }
 
@@ -2292,6 +2349,33 @@ extern "C" int skb_gemm_force_sw(int mode, int na, int cs) {
   sw::g_na = na;
   sw::g_cs = cs;
   return SKB_OK;
+}
+
+// int8 GEMM for the quantized feed-forward layers (quant.py:65-132):
+// acc[m, n] = sum_k A[m, k] * W[n, k] exactly in int32 (tcgen05 kind::i8),
+// then out = (float32(acc) * a_scale[m]) * w_scale[n] with the epilogue's
+// bias / ReLU / residual add.  A, W int8 K-major; K % 16 == 0.
+extern "C" int skb_gemm_i8(int M, int N, int K, const void *A, int lda, const float *a_scale,
+                           const void *W, int ldw, const float *w_scale, const skb_epilogue *epi,
+                           void *stream) {
+  if (M < 0 || N <= 0 || K <= 0) return fail(SKB_ERR_SHAPE, "gemm_i8: bad shape M=%d N=%d K=%d", M, N, K);
+  if (!A || !W || !a_scale || !w_scale || !epi || !epi->out) return fail(SKB_ERR_SHAPE, "gemm_i8: null operand");
+  if (K % 16 || lda % 16 || ldw % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
+      (reinterpret_cast<uintptr_t>(W) & 15))
+    return fail(SKB_ERR_CONFIG, "gemm_i8: K, leading dims and bases must be 16-byte aligned");
+  if (K > (1 << 31) / (127 * 127)) return fail(SKB_ERR_CONFIG, "gemm_i8: K=%d overflows int32", K);
+  if (epi->kind != SKB_EPI_STORE && epi->kind != SKB_EPI_RELU && epi->kind != SKB_EPI_RESID)
+    return fail(SKB_ERR_CONFIG, "gemm_i8: STORE, RELU or RESID epilogue only");
+  if (epi->kind == SKB_EPI_RESID && epi->out_dtype != SKB_F32)
+    return fail(SKB_ERR_CONFIG, "gemm_i8: residual target must be fp32");
+  g_last_launches = 1;
+  if (M == 0) return SKB_OK;
+  EpiArgs ep = to_args(epi);
+  ep.ln_out = nullptr;
+  ep.a_scale = a_scale;
+  ep.w_scale = w_scale;
+  const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, 1);
+  return sw::launch(M, N, K, A, lda, W, ldw, ep, as_stream(stream), na, 1, true);
 }
 
 extern "C" int skb_gemm_force_pc(int mode, int na, int pairs) {

@@ -73,6 +73,26 @@ def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_ro
     _count(N.lib().skb_last_launches())
 
 
+def quantize_rows(x, q, scales, rows=None):
+    """q (int8), scales (fp32) <- per-row symmetric quantization of fp32 x
+    (quant.py:40-53 / 99-104)."""
+    rows = x.shape[0] if rows is None else rows
+    N.call("skb_quantize_rows", rows, x.shape[1], x.data_ptr(), x.stride(0), q.data_ptr(),
+           q.stride(0), scales.data_ptr(), stream())
+    _count()
+
+
+def gemm_i8(qa, a_scale, qw, w_scale, out, kind=N.EPI_STORE, bias=None, *, M=None):
+    """out (or residual x) <- epilogue((f32(qa . qw^T) * a_scale) * w_scale)
+    with exact int32 accumulation (quant.py:121-132)."""
+    M = qa.shape[0] if M is None else M
+    Nn, K = qw.shape
+    epi = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), out.stride(0), dcode(out))
+    N.call("skb_gemm_i8", M, Nn, K, qa.data_ptr(), qa.stride(0), a_scale.data_ptr(),
+           qw.data_ptr(), qw.stride(0), w_scale.data_ptr(), C.byref(epi), stream())
+    _count()
+
+
 def layernorm(x, gain, bias, out, rows=None, eps=1e-5):
     rows = x.shape[0] if rows is None else rows
     N.call("skb_layernorm", rows, x.shape[1], x.data_ptr(), x.stride(0), gain.data_ptr(),

@@ -150,7 +150,7 @@ def test_batch_invariance_at_scale():
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     import bench
     from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
-    model, vocabs = bench.build_model("bf16")
+    model, vocabs, _ = bench.build_model("big")
     rng = np.random.default_rng(7)
     sents = [[f"w{i}" for i in rng.integers(0, 31996, size=int(n))] for n in rng.integers(1, 121, size=160)]
     st = SearchSettings(beam=5, length_alpha=1.0)

@@ -8,7 +8,7 @@ sys.path.insert(0, '.')
 import bench  # noqa: E402
 from paper_2207_05851_b200 import kern, engine  # noqa: E402
 
-model, vocabs = bench.build_model("bf16")
+model, vocabs, _ = bench.build_model("big")
 sents = bench.synth_sentences(128, 30, 32000, seed=13)
 bb = bench.make_batch(model, vocabs, sents, 5, 1.0)
 bb.use_graph = False

@@ -12,7 +12,7 @@ import bench  # noqa: E402
 from paper_2207_05851_b200 import engine  # noqa: E402
 from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate  # noqa: E402
 
-model, vocabs = bench.build_model("bf16")
+model, vocabs, _ = bench.build_model("big")
 inputs = [SentenceInput(tokens=s) for k in range(9) for s in bench.synth_sentences(128, 30, 32000, seed=500 + k)]
 settings = SearchSettings(beam=5, length_alpha=1.0)
 engine.DECODE_STREAMS = 3

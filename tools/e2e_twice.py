@@ -10,7 +10,7 @@ import bench  # noqa: E402
 from paper_2207_05851_b200 import engine  # noqa: E402
 from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate  # noqa: E402
 
-model, vocabs = bench.build_model("bf16")
+model, vocabs, _ = bench.build_model("big")
 settings = SearchSettings(beam=5, length_alpha=1.0)
 engine.DECODE_STREAMS = 3
 translate(model, vocabs, [SentenceInput(tokens=s) for s in bench.synth_sentences(8, 30, 32000, 1)], settings)

@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate  # noqa: E402
 
-model, vocabs = bench.build_model("bf16")
+model, vocabs, _ = bench.build_model("big")
 rng = np.random.default_rng(5)
 mk = lambda n: [f"w{i}" for i in rng.integers(0, 31996, size=n)]  # noqa: E731
 s = mk(25)

@@ -19,7 +19,7 @@ ap.add_argument("--beam", type=int, default=5)
 ap.add_argument("--src-len", type=int, default=30)
 ap.add_argument("--graph", action="store_true")
 a = ap.parse_args()
-model, vocabs = bench.build_model("bf16")
+model, vocabs, _ = bench.build_model("big")
 sents = bench.synth_sentences(a.batch, a.src_len, 32000, seed=13)
 bb = bench.make_batch(model, vocabs, sents, a.beam, 1.0)
 bb.use_graph = a.graph
