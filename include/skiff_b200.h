@@ -105,6 +105,10 @@ typedef struct skb_epilogue {
   const float *ln_in_gain;
   const float *ln_in_bias;
   float ln_in_eps;
+  /* Independent decode streams sharing the device while this call runs     */
+  /* (0 or 1 = this call has the GPU to itself): tiles are sized for a      */
+  /* 1/streams share of the SMs.  Never changes the numbers.                */
+  int streams;
 } skb_epilogue;
 
 /* Library identity / diagnostics */
@@ -126,7 +130,11 @@ int skb_tc_available(void);
 int skb_gemm(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
              int ldw, const skb_epilogue *epi, void *stream);
 
-/* Force the tcgen05 tile configuration of later skb_gemm calls (tests and
+/* Test / tuning overrides of the kernel choice (skb_gemm_force*): they hold
+ * for later skb_gemm calls made from the calling host thread only
+ * (thread-local); production callers never need them.
+ *
+ * Force the tcgen05 tile configuration of later skb_gemm calls (tests and
  * tuning): N-tile width bn in {64,128,256}, multicast cluster size cs in
  * {1,2,4}, split-K factor; 0 = choose automatically. */
 int skb_gemm_force(int bn, int cs, int splits);
@@ -140,7 +148,8 @@ int skb_gemm_force_sw(int mode, int na, int cs);
 
 /* Select the persistent CTA-pair GEMM (tcgen05.mma.cta_group::2, 256 weight
  * rows x na activation rows per tile, two TMEM accumulators): mode 0 =
- * automatic (M >= 128, shapes without a cluster K-split), 1 = never,
+ * automatic (M >= 1024 and N >= 8192, i.e. the output projection of large
+ * batches; shapes without a cluster K-split), 1 = never,
  * 2 = always where applicable; na in {32..256} step 32, pairs = CTA pairs per
  * launch; 0 = choose automatically.  Bitwise equal to the swap-AB kernel. */
 int skb_gemm_force_pc(int mode, int na, int pairs);
@@ -165,11 +174,6 @@ int skb_quantize_rows(int rows, int k, const float *x, int ldx, void *q, int ldq
 int skb_gemm_i8(int M, int N, int K, const void *A, int lda, const float *a_scale, const void *W,
                 int ldw, const float *w_scale, const skb_epilogue *epi, void *stream);
 
-/* Number of independent decode streams the caller runs concurrently on this
- * device (default 1).  The swap-AB GEMM sizes its tiles for its share of the
- * SMs (fewer, larger tiles ingest fewer bytes in total).  Affects launches
- * made (or graphs captured) after the call; numerics are unchanged. */
-int skb_set_concurrency(int streams);
 
 /* Same, forcing the SIMT path (for parity tests of the tcgen05 path). */
 int skb_gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,

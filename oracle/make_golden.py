@@ -35,6 +35,10 @@ on seeded inputs:
                     with its load_model_dir (checkpoint.py:316-353): the
                     product must read these directories unchanged.
                     `python oracle/make_golden.py modeldirs`
+  * quant.npz + quant_records.json — the int8 feed-forward path
+                    (quant.py): quantize_rows / QuantizedLinear outputs on
+                    seeded matrices, and translate() records of models
+                    swapped with quantize_model.  `... make_golden.py quant`
 
 The oracle (oracle/skiff_oracle.py) is then checked against these files by
 tests/test_oracle_golden.py; the CUDA path is checked against the oracle and
@@ -420,11 +424,49 @@ def gen_model_dirs():
     (GOLDEN / "refdir_records.json").write_text(json.dumps(out, indent=0))
 
 
+QUANT_CASES = ["toy_beam3", "tiny_greedy_16x32", "ssru_greedy", "tiny_beam5"]
+
+
+def gen_quant():
+    """quant.py on seeded matrices + translate records of quantized models."""
+    from skiff.kernels import Tensor
+    from skiff.quant import QuantizedLinear, quantize_model, quantize_rows
+    from skiff.search import SearchSettings, SentenceInput, translate
+    rng = np.random.default_rng(2024)
+    M, K1, N1 = 7, 256, 192
+    x = rng.standard_normal((M, K1)).astype(np.float32)
+    x[3] = 0.0                                      # all-zero row: scale 1
+    x[4, :5] = [0.5, -0.5, 1.5, -2.5, 127.0]        # ties at the rounding boundary
+    w1 = (rng.standard_normal((N1, K1)) * 0.05).astype(np.float32)
+    b1 = rng.standard_normal(N1).astype(np.float32)
+    w2 = (rng.standard_normal((K1, N1)) * 0.05).astype(np.float32)
+    b2 = rng.standard_normal(K1).astype(np.float32)
+    q1, s1 = quantize_rows(w1)
+    q2, s2 = quantize_rows(w2)
+    out1 = QuantizedLinear(q1, s1)(Tensor(x), Tensor(b1)).data
+    h2 = np.maximum(out1, 0).astype(np.float32)
+    out2 = QuantizedLinear(q2, s2)(Tensor(h2), Tensor(b2)).data
+    qx, sx = quantize_rows(x)
+    np.savez_compressed(GOLDEN / "quant.npz", x=x, w1=w1, b1=b1, w2=w2, b2=b2, q1=q1, s1=s1,
+                        q2=q2, s2=s2, out1=out1, out2=out2, qx=qx, sx=sx)
+    recs = {}
+    for name in QUANT_CASES:
+        case = next(c for c in SEARCH_CASES if c["name"] == name)
+        m, vocabs = ref_model(case["config"]), ref_vocabs(case["config"])
+        quantize_model(m)
+        settings = SearchSettings(beam=case.get("beam", 1), length_alpha=case.get("alpha", 1.0))
+        recs[name] = _records_to_json(translate(m, vocabs, [SentenceInput(**i) for i in case["inputs"]],
+                                                settings))
+    (GOLDEN / "quant_records.json").write_text(json.dumps(recs, indent=0))
+
+
 def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
     tmp = import_reference()
     try:
-        if len(sys.argv) > 1 and sys.argv[1] == "modeldirs":
+        if len(sys.argv) > 1 and sys.argv[1] == "quant":
+            gen_quant()
+        elif len(sys.argv) > 1 and sys.argv[1] == "modeldirs":
             gen_model_dirs()
         elif len(sys.argv) > 1 and sys.argv[1] == "scale":
             gen_scale(set(sys.argv[2:]) or None)

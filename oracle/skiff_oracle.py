@@ -780,3 +780,37 @@ def translate_text(model: OracleModel, vocabs: dict, inputs: list[dict], beam_si
             recs.append(dict(text="", score=0.0, factors=[], chunks=0, forced_eos=False,
                              error=str(e)))
     return recs
+
+
+# ------------------------------------------------------------------ int8
+# quant.py:33-132 — dynamic int8 feed-forward.  The integer product is exact,
+# the rescale is (float32(acc) * a_scale) * w_scale, each product rounded in
+# float32, then + bias.
+
+def round_half_away(x):
+    """quant.py:33-37: ties away from zero, in the input's float32."""
+    return np.sign(x) * np.floor(np.abs(x) + 0.5)
+
+
+def quantize_rows(w):
+    """quant.py:40-53 (weights) / 99-104 (activations, same rule)."""
+    w = np.asarray(w, dtype=F32)
+    maxabs = np.abs(w).max(axis=1)
+    scales = np.where(maxabs > 0, maxabs / 127.0, 1.0).astype(F32)
+    q = np.clip(round_half_away(w / scales[:, None]), -127, 127).astype(np.int8)
+    return q, scales
+
+
+def gemm_i8(qx, qw):
+    """quant.py:60-78: (m, k) int8 . (n, k)^T int8 -> (m, n) int32, exact."""
+    return qx.astype(np.int32) @ qw.astype(np.int32).T
+
+
+def quantized_linear(x, q, scales, bias=None):
+    """quant.py:121-132: QuantizedLinear.__call__ on float32 rows."""
+    flat = np.ascontiguousarray(np.asarray(x, dtype=F32).reshape(-1, x.shape[-1]))
+    qx, a_scales = quantize_rows(flat)
+    out = gemm_i8(qx, q).astype(F32) * a_scales[:, None] * np.asarray(scales, F32)[None, :]
+    if bias is not None:
+        out = out + np.asarray(bias, F32)
+    return out.reshape(x.shape[:-1] + (q.shape[0],))

@@ -35,7 +35,7 @@ class Epilogue(C.Structure):
                 ("splitk_counters_n", i32), ("ln_gain", vp), ("ln_bias", vp),
                 ("ln_eps", C.c_float), ("ln_out", vp), ("ln_ldo", i32), ("ln_counter", vp),
                 ("ln_in", vp), ("ln_in_ld", i32), ("ln_in_gain", vp), ("ln_in_bias", vp),
-                ("ln_in_eps", C.c_float)]
+                ("ln_in_eps", C.c_float), ("streams", i32)]
 
 
 class BeamState(C.Structure):
@@ -66,7 +66,6 @@ SIGNATURES = {
     "skb_gemm_force_pc": [i32, i32, i32],
     "skb_quantize_rows": [i32, i32, vp, i32, vp, i32, vp, vp],
     "skb_gemm_i8": [i32, i32, i32, vp, i32, vp, vp, i32, vp, C.POINTER(Epilogue), vp],
-    "skb_set_concurrency": [i32],
     "skb_layernorm": [i32, i32, vp, i32, vp, vp, C.c_float, vp, i32, i32, vp],
     "skb_embed_target": [i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp],
     "skb_embed_source": [i32, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp],

@@ -32,6 +32,7 @@ from .config import decoder_step_cost
 from .errors import CapabilityError, DataError, InputError, NumericError, SkiffError
 from .search import (NvsRestriction, SearchSettings, ShortlistRestriction, parse_input_line,
                      translate)
+from .quant import quantize_model
 from .shortlist import Shortlist
 
 log = logging.getLogger(__name__)
@@ -54,9 +55,10 @@ class ArgumentParser(argparse.ArgumentParser):
 
 # ------------------------------------------------------------------ helpers
 def _load(args):
-    if args.quantize:
-        raise CapabilityError("int8 feed-forward is not part of the B200 backend (bf16/fp32)")
-    return load_model_dir(args.model, precision=args.precision)
+    mdir = load_model_dir(args.model, precision=args.precision)
+    if args.quantize == "int8":  # cli.py:130-131 / 216-217
+        quantize_model(mdir.model)
+    return mdir
 
 
 def _show(config) -> int:
@@ -195,7 +197,8 @@ def cmd_reference_only(args) -> int:
 def _common(p, *, quantize=True):
     p.add_argument("-m", "--model", required=True, help="model directory")
     if quantize:
-        p.add_argument("--quantize", choices=["int8"], help="(not supported on this backend)")
+        p.add_argument("--quantize", choices=["int8"],
+                       help="int8 feed-forward layers (dynamic per-row quantization)")
     p.add_argument("--precision", choices=["bf16", "fp32"], default="bf16",
                    help="GEMM operand precision (fp32 = parity mode)")
     p.add_argument("--show-config", action="store_true")

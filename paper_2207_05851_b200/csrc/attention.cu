@@ -475,133 +475,6 @@ __global__ void __launch_bounds__(256, 3) k_self_attn_vec(
 static float attn_scale(int dh) { return (float)(1.0 / sqrt((double)dh)); }
 
 // ------------------------- grouped attention, bf16 K/V in shared memory
-// Same contract as k_attn_smem for bf16 operands with d_h in {32,64,128}:
-// the (sentence, head) K/V slice is copied raw (cp.async, 16 B) into shared
-// memory, and each warp serves one query row with DH/8 lanes per key (one
-// 16-byte LDS of K or V each, 32*8/DH keys per instruction), online softmax
-// over 32-key chunks.
-template <int DH>
-__global__ void __launch_bounds__(256) k_attn_smem_vec(
-    int R, int G, int H, const __nv_bfloat16 *q, int ldq, const __nv_bfloat16 *kv, int ld_kv,
-    int koff, int voff, int L, const int *row_sent, const int *lengths, float scale, void *ctx,
-    int ldc, int ctx_dtype) {
-  PDL_ENTRY();
-  constexpr int LPK = DH / 8;
-  constexpr int KPI = 32 / LPK;
-  constexpr int ITER = 32 / KPI;
-  extern __shared__ __align__(16) uint8_t av_smem[];
-  uint4 *Ks = reinterpret_cast<uint4 *>(av_smem);   // [L][LPK]
-  uint4 *Vs = Ks + (size_t)L * LPK;
-  const int g = blockIdx.x, h = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int row0 = g * G;
-  const int b = row_sent ? row_sent[row0] : g;
-  const int len = lengths[b];
-  for (int idx = threadIdx.x; idx < len * LPK; idx += blockDim.x) {
-    const int j = idx / LPK, c = idx - j * LPK;
-    const size_t kr = (size_t)(b * L + j) * ld_kv + h * DH + c * 8;
-    const uint32_t dk = static_cast<uint32_t>(__cvta_generic_to_shared(Ks + idx));
-    const uint32_t dv = static_cast<uint32_t>(__cvta_generic_to_shared(Vs + idx));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dk), "l"(kv + kr + koff) : "memory");
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dv), "l"(kv + kr + voff) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  const int sub = lane % LPK, grp = lane / LPK;
-  for (int i = warp; i < G; i += nw) {
-    const int r = row0 + i;
-    if (r >= R) break;
-    float q8[8];
-    {
-      const uint4 qv = *reinterpret_cast<const uint4 *>(q + (size_t)r * ldq + h * DH + sub * 8);
-      const __nv_bfloat162 *qp = reinterpret_cast<const __nv_bfloat162 *>(&qv);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 f = __bfloat1622float2(qp[u]);
-        q8[2 * u] = f.x * scale;  // fold 1/sqrt(d_h) into q (one multiply per dim)
-        q8[2 * u + 1] = f.y * scale;
-      }
-    }
-    float m_run = -INFINITY, l_run = 0.f;
-    float o8[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) o8[u] = 0.f;
-    for (int j0 = 0; j0 < len; j0 += 32) {
-      float sc[ITER];
-      float cmax = -INFINITY;
-#pragma unroll
-      for (int it = 0; it < ITER; ++it) {
-        const int j = j0 + it * KPI + grp;
-        float a = 0.f;
-        if (j < len) {
-          const uint4 kk = Ks[(size_t)j * LPK + sub];
-          const __nv_bfloat162 *kp = reinterpret_cast<const __nv_bfloat162 *>(&kk);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float2 f = __bfloat1622float2(kp[u]);
-            a = fmaf(q8[2 * u], f.x, a);
-            a = fmaf(q8[2 * u + 1], f.y, a);
-          }
-        }
-#pragma unroll
-        for (int o = LPK / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        sc[it] = j < len ? a : -INFINITY;
-        cmax = fmaxf(cmax, sc[it]);
-      }
-#pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-      const float mnew = fmaxf(m_run, cmax);
-      const float corr = m_run == -INFINITY ? 0.f : expf(m_run - mnew);
-      float psum = 0.f;
-#pragma unroll
-      for (int it = 0; it < ITER; ++it) {
-        sc[it] = sc[it] == -INFINITY ? 0.f : expf(sc[it] - mnew);
-        psum += sc[it];
-      }
-#pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
-      l_run = l_run * corr + psum;
-      m_run = mnew;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) o8[u] *= corr;
-#pragma unroll
-      for (int it = 0; it < ITER; ++it) {
-        const int j = j0 + it * KPI + grp;
-        if (j >= len) continue;
-        const uint4 vv = Vs[(size_t)j * LPK + sub];
-        const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&vv);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 f = __bfloat1622float2(vp[u]);
-          o8[2 * u] = fmaf(sc[it], f.x, o8[2 * u]);
-          o8[2 * u + 1] = fmaf(sc[it], f.y, o8[2 * u + 1]);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-#pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) o8[u] += __shfl_xor_sync(0xffffffffu, o8[u], o);
-    if (grp == 0) {
-      const float inv = 1.0f / l_run;
-      const size_t ob = (size_t)r * ldc + h * DH + sub * 8;
-      if (ctx_dtype == SKB_BF16) {
-        uint4 w;
-        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          __nv_bfloat162 pr = __floats2bfloat162_rn(o8[2 * u] * inv, o8[2 * u + 1] * inv);
-          wp[u] = *reinterpret_cast<uint32_t *>(&pr);
-        }
-        *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(ctx) + ob) = w;
-      } else {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) reinterpret_cast<float *>(ctx)[ob + u] = o8[u] * inv;
-      }
-    }
-  }
-}
 
 // ------------------- grouped attention on tensor cores (mma.sync, bf16)
 // One warp computes 16 query rows x one head with m16n8k16 MMAs: S = Q K^T
@@ -955,19 +828,10 @@ static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, 
     // tensor-core path: one warp per 16 query rows
     const int Lp = (L + 63) / 64 * 64;
     const size_t smem = (size_t)2 * Lp * (dh + 8) * sizeof(__nv_bfloat16);
-    static int use_mma = -1;
-    if (use_mma < 0) {
-      const char *e = getenv("SKB_ATTN_MMA");
-      use_mma = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (use_mma && smem <= 200 * 1024 && (dh == 64 || dh == 128 || dh == 32)) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_attn_mma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_attn_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_attn_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
+    if (smem <= 200 * 1024 && (dh == 64 || dh == 128 || dh == 32)) {
+      ensure_smem_fn(k_attn_mma<32>, 200 * 1024);
+      ensure_smem_fn(k_attn_mma<64>, 200 * 1024);
+      ensure_smem_fn(k_attn_mma<128>, 200 * 1024);
       const int tiles = (G + 15) / 16;
       const int nwm = tiles < 4 ? tiles : 4;
       dim3 grid((R + G - 1) / G, H);
@@ -985,29 +849,7 @@ static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, 
       return 0;
     }
   }
-  const int nw = G < 8 ? G : 8;
-  const size_t smem = (size_t)2 * L * dh * sizeof(__nv_bfloat16);
-  if (smem > 200 * 1024) return -1;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_smem_vec<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_attn_smem_vec<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_attn_smem_vec<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  dim3 grid((R + G - 1) / G, H);
-  auto *qb = reinterpret_cast<const __nv_bfloat16 *>(q) + qoff;
-  auto *kb = reinterpret_cast<const __nv_bfloat16 *>(kv);
-  if (dh == 64)
-    launch_k(k_attn_smem_vec<64>, grid, 32 * nw, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
-             row_sent, lengths, scale, ctx, ldc, ctx_dtype);
-  else if (dh == 32)
-    launch_k(k_attn_smem_vec<32>, grid, 32 * nw, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
-             row_sent, lengths, scale, ctx, ldc, ctx_dtype);
-  else
-    launch_k(k_attn_smem_vec<128>, grid, 32 * nw, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff,
-             L, row_sent, lengths, scale, ctx, ldc, ctx_dtype);
-  return 0;
+  return -1;  // longer than the tensor-core kernel's shared-memory budget
 }
 
 
@@ -1525,18 +1367,14 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
   if (attn_vec_ok(dh, qkv_dtype, qkv_dtype, qkv, ld_qkv, qkv, ld_qkv, H * dh, 2 * H * dh, 0) &&
       launch_attn_vec(B * L, L, H, dh, qkv, ld_qkv, 0, qkv, ld_qkv, H * dh, 2 * H * dh, L, nullptr,
                       lengths, attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream)) == 0) {
-    SKB_CHECK_LAUNCH("k_attn_smem_vec(encoder)");
+    SKB_CHECK_LAUNCH("k_attn_mma(encoder)");
     return SKB_OK;
   }
   {
     const int nw = L < 8 ? L : 8;
     const size_t smem = ((size_t)2 * L * (dh + 1) + (size_t)nw * dh) * sizeof(float);
     if (smem <= 200 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_attn_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
+      ensure_smem_fn(k_attn_smem, 200 * 1024);
       const int D = H * dh;
       dim3 g2(B, H);
       launch_k(k_attn_smem, g2, 32 * nw, smem, as_stream(stream), 
@@ -1585,16 +1423,7 @@ static int launch_self_tc(int R, int H, int dh, const void *qkv, int ld_qkv, int
   auto go = [&](auto kern_fn) {
     // per-kernel opt-in shared memory size (all instantiations share the
     // function-pointer type, so key by address)
-    static std::mutex mu;
-    static std::unordered_map<const void *, size_t> set;
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      size_t &cur = set[reinterpret_cast<const void *>(kern_fn)];
-      if (smem > cur) {
-        cudaFuncSetAttribute(kern_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cur = smem;
-      }
-    }
+    ensure_smem_fn(kern_fn, smem);
     launch_k(kern_fn, g, 32 * hg, smem, as_stream(stream), R, H, G2,
              reinterpret_cast<const __nv_bfloat16 *>(qkv), ld_qkv, k, v, S_max, anc, step, sc,
              reinterpret_cast<__nv_bfloat16 *>(ctx), ldc, tc_cap, plan);
@@ -1706,11 +1535,7 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
       (reinterpret_cast<uintptr_t>(q) & 3) == 0) {
     const size_t smem = (size_t)2 * ((L + 31) & ~31) * (4 * 64 * 2 + 16);
     if (smem <= 200 * 1024) {
-      static size_t set = 0;
-      if (smem > set) {
-        cudaFuncSetAttribute(k_cross_tc<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set = smem;
-      }
+      ensure_smem_fn(k_cross_tc<64, 4>, smem);
       dim3 g((R + G - 1) / G, H / 4);
       launch_k(k_cross_tc<64, 4>, g, 128, smem, as_stream(stream), R, G, H,
                reinterpret_cast<const __nv_bfloat16 *>(q), ldq,
@@ -1723,18 +1548,14 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
   if (attn_vec_ok(dh, q_dtype, kv_dtype, q, ldq, kv, ld_kv, koff, voff, 0) &&
       launch_attn_vec(R, G, H, dh, q, ldq, 0, kv, ld_kv, koff, voff, L, row_sent, lengths,
                       attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream)) == 0) {
-    SKB_CHECK_LAUNCH("k_attn_smem_vec(cross)");
+    SKB_CHECK_LAUNCH("k_attn_mma(cross)");
     return SKB_OK;
   }
   {
     const int nw = G < 8 ? G : 8;
     const size_t smem = ((size_t)2 * L * (dh + 1) + (size_t)nw * dh) * sizeof(float);
     if (smem <= 200 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_attn_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
+      ensure_smem_fn(k_attn_smem, 200 * 1024);
       dim3 g2((R + G - 1) / G, H);
       launch_k(k_attn_smem, g2, 32 * nw, smem, as_stream(stream), R, G, H, dh, q, ldq, q_dtype, 0, kv,
                                                             ld_kv, kv_dtype, koff, voff, L, row_sent,

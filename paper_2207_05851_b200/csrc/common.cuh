@@ -47,6 +47,13 @@ __device__ __forceinline__ void pdl_trigger() {
 
 bool pdl_enabled();
 
+// Raise a kernel's opt-in dynamic shared memory limit on the current device
+// (idempotent, thread-safe, per device).
+void ensure_smem(const void *kernel, size_t bytes);
+template <typename F> inline void ensure_smem_fn(F *kernel, size_t bytes) {
+  ensure_smem(reinterpret_cast<const void *>(kernel), bytes);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                             cudaStream_t stream, Args &&...args) {

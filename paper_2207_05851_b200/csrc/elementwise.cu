@@ -415,7 +415,7 @@ extern "C" int skb_quantize_rows(int rows, int k, const float *x, int ldx, void 
                                  float *scales, void *stream) {
   if (rows < 0 || k <= 0 || ldx < k || ldq < k)
     return fail(SKB_ERR_SHAPE, "quantize_rows: rows=%d k=%d ldx=%d ldq=%d", rows, k, ldx, ldq);
-  if (k > (1 << 31) / (127 * 127))
+  if (k > (int)(2147483648LL / (127 * 127)))
     return fail(SKB_ERR_CONFIG, "quantize_rows: inner extent %d would overflow int32 accumulation", k);
   if (rows == 0) return SKB_OK;
   launch_k(k_quantize_rows, rows, 128, 0, as_stream(stream), rows, k, x, ldx,

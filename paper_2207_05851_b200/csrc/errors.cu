@@ -2,6 +2,9 @@
 #include "common.cuh"
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace skb {
 
@@ -29,6 +32,21 @@ bool pdl_enabled() {
     on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
+}
+
+// Opt-in dynamic shared memory is a per-(kernel, device) attribute: raise it
+// once per device the kernel runs on (several devices may share a process).
+void ensure_smem(const void *kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  size_t &cur = done[{kernel, dev}];
+  if (bytes > cur) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cur = bytes;
+  }
 }
 
 }  // namespace skb

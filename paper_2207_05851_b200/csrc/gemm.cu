@@ -735,11 +735,7 @@ static int launch(int M, int N, int K, const void *A, int lda, const void *W, in
   if (rc) return rc;
   rc = make_map(&mb, W, N, K, ldw, BN);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
+  ensure_smem_fn(k_gemm_tc<BN, CS>, C::SMEM);
   const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
   const int nsm = num_sms();
   int grid;
@@ -779,7 +775,7 @@ static int launch(int M, int N, int K, const void *A, int lda, const void *W, in
 
 // tile-config overrides (tests / tuning): env SKB_GEMM_BN|CS|SPLITS at load,
 // or skb_gemm_force() at run time; 0 = automatic
-int g_force_bn = -1, g_force_cs = 0, g_force_s = 0;
+thread_local int g_force_bn = -1, g_force_cs = 0, g_force_s = 0;  // test/tuning overrides
 void init_forces() {
   if (g_force_bn >= 0) return;
   const char *e = getenv("SKB_GEMM_BN");
@@ -1501,11 +1497,7 @@ template <int KIND, int CS, bool LNX = false, bool I8 = false>
 static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
                     const CUtensorMap &mo, int Na, int stages, int stg_off, int tma_out,
                     size_t smem, EpiArgs ep, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_sw<KIND, CS, LNX, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
-    attr_set = true;
-  }
+  ensure_smem_fn(k_gemm_sw<KIND, CS, LNX, I8>, SMEM_MAX);
   const int n_wt = (N + 127) / 128, n_at = (M + Na - 1) / Na;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_wt * n_at, CS);
@@ -1555,10 +1547,9 @@ static int launch_k2(int M, int N, int K, const CUtensorMap &mw, const CUtensorM
   return launch_t<KIND, 1>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
 }
 
-extern int g_concurrency;
 
 static int launch(int M, int N, int K, const void *X, int ldx, const void *W, int ldw, EpiArgs ep,
-                  cudaStream_t st, int Na, int CS, bool i8 = false) {
+                  cudaStream_t st, int Na, int CS, int conc, bool i8 = false) {
   ep.splits = 1;
   // When the dependent grid launches (PDL trigger): right after this grid's
   // own dependency wait with one decode stream (the next kernel's CTAs become
@@ -1572,7 +1563,7 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
     const char *e = getenv("SKB_PDL_LATE");
     late_env = e ? atoi(e) : -1;
   }
-  ep.late_trigger = late_env >= 0 ? late_env : (g_concurrency > 1 ? 1 : 0);
+  ep.late_trigger = late_env >= 0 ? late_env : (conc > 1 ? 1 : 0);
 #ifdef SKB_GEMM_TRACE
   {
     const char *e = getenv("SKB_SW_DBG");
@@ -1681,12 +1672,11 @@ static int pick_cs(int N, int K) {
 // CTAs co-reside per SM (113 KB ring), each streams (128 + Na) rows of K,
 // plus a fixed per-CTA cost worth ~160 rows; CTA slots beyond one wave
 // cost proportionally.
-int g_concurrency = 1;  // independent decode streams sharing the GPU (skb_set_concurrency)
 
-static int pick_na(int M, int N, int CS) {
+static int pick_na(int M, int N, int CS, int conc) {
   // with several decode streams in flight each GEMM gets a share of the SMs:
   // fewer, larger tiles ingest fewer bytes in total
-  const int slots = 2 * tc::num_sms() / (g_concurrency > 0 ? g_concurrency : 1);
+  const int slots = 2 * tc::num_sms() / (conc > 0 ? conc : 1);
   const int n_wt = (N + 127) / 128;
   const int na_max = CS > 1 ? 80 : 160;  // split-K partial + receive slots fit the ring
   static int na_floor = -1;
@@ -1722,7 +1712,7 @@ static int lnx_max_rows() {
   return v;
 }
 
-int g_mode = -1, g_na = 0, g_cs = 0;  // mode: 0 auto, 1 never, 2 always
+thread_local int g_mode = -1, g_na = 0, g_cs = 0;  // test overrides; mode: 0 auto, 1 never, 2 always
 void init_mode() {
   if (g_mode >= 0) return;
   const char *e = getenv("SKB_GEMM_SW");
@@ -2027,17 +2017,13 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
 }
 
-static int g_pairs = -1;  // SKB_PC_PAIRS: pairs per launch (0 = automatic)
+thread_local int g_pairs = -1;  // SKB_PC_PAIRS: pairs per launch (0 = automatic)
 
 template <int KIND>
 static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
                     const CUtensorMap &mo, int Na, int stages, int tcols, int tma_out, size_t smem,
                     int pairs, EpiArgs ep, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_pc<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, sw::SMEM_MAX);
-    attr_set = true;
-  }
+  ensure_smem_fn(k_gemm_pc<KIND>, sw::SMEM_MAX);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(192);
@@ -2095,9 +2081,9 @@ static void pick(int M, int N, int K, int conc, int &Na, int &pairs) {
   pairs = (int)(tiles < maxp ? tiles : maxp);
 }
 
-int g_mode = -1;   // SKB_GEMM_PC: 0 auto, 1 never, 2 always (where applicable)
-int g_na = 0;      // forced activation tile (0 = automatic)
-int g_min_m = -1;  // SKB_PC_MIN_M: smallest M the automatic choice sends here
+thread_local int g_mode = -1;   // SKB_GEMM_PC: 0 auto, 1 never, 2 always (where applicable)
+thread_local int g_na = 0;      // forced activation tile (0 = automatic)
+thread_local int g_min_m = -1;  // SKB_PC_MIN_M: smallest M the automatic choice sends here
 void init_mode() {
   if (g_mode >= 0) return;
   const char *e = getenv("SKB_GEMM_PC");
@@ -2337,12 +2323,6 @@ extern "C" int skb_gemm_force(int bn, int cs, int splits) {
   return SKB_OK;
 }
 
-extern "C" int skb_set_concurrency(int streams) {
-  if (streams < 1 || streams > 16) return fail(SKB_ERR_CONFIG, "concurrency %d out of [1, 16]", streams);
-  sw::g_concurrency = streams;
-  return SKB_OK;
-}
-
 extern "C" int skb_gemm_force_sw(int mode, int na, int cs) {
   sw::init_mode();
   sw::g_mode = mode;
@@ -2363,7 +2343,7 @@ extern "C" int skb_gemm_i8(int M, int N, int K, const void *A, int lda, const fl
   if (K % 16 || lda % 16 || ldw % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(W) & 15))
     return fail(SKB_ERR_CONFIG, "gemm_i8: K, leading dims and bases must be 16-byte aligned");
-  if (K > (1 << 31) / (127 * 127)) return fail(SKB_ERR_CONFIG, "gemm_i8: K=%d overflows int32", K);
+  if (K > (int)(2147483648LL / (127 * 127))) return fail(SKB_ERR_CONFIG, "gemm_i8: K=%d overflows int32", K);
   if (epi->kind != SKB_EPI_STORE && epi->kind != SKB_EPI_RELU && epi->kind != SKB_EPI_RESID)
     return fail(SKB_ERR_CONFIG, "gemm_i8: STORE, RELU or RESID epilogue only");
   if (epi->kind == SKB_EPI_RESID && epi->out_dtype != SKB_F32)
@@ -2374,8 +2354,9 @@ extern "C" int skb_gemm_i8(int M, int N, int K, const void *A, int lda, const fl
   ep.ln_out = nullptr;
   ep.a_scale = a_scale;
   ep.w_scale = w_scale;
-  const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, 1);
-  return sw::launch(M, N, K, A, lda, W, ldw, ep, as_stream(stream), na, 1, true);
+  const int conc = epi->streams > 0 ? epi->streams : 1;
+  const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, 1, conc);
+  return sw::launch(M, N, K, A, lda, W, ldw, ep, as_stream(stream), na, 1, conc, true);
 }
 
 extern "C" int skb_gemm_force_pc(int mode, int na, int pairs) {
@@ -2469,6 +2450,7 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   // its bigger tiles pay; below that the sw kernel's one-tile-per-CTA plan
   // (and its prologue LayerNorm) has the shorter critical path.
   pc::init_mode();
+  const int conc = epi->streams > 0 ? epi->streams : 1;  // decode streams sharing the GPU
   {
     const int cs_sw = epi->kind == SKB_EPI_LOGITS ? 1 : sw::pick_cs(N, K);
     const bool pc_ok = cs_sw == 1 && logits_tma && sw::g_mode == 0;
@@ -2478,12 +2460,12 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
         if (rc) return rc;
       }
       fused_ln = false;  // a requested output LayerNorm follows as its own launch
-      return pc::launch(M, N, K, A, lda, W, ldw, ep, st, sw::g_concurrency, pc::g_na);
+      return pc::launch(M, N, K, A, lda, W, ldw, ep, st, conc, pc::g_na);
     }
   }
   if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || sw_pref)) {
     const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
-    const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs);
+    const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs, conc);
     fused_ln = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr;
     if (epi->ln_in) {
       // input LayerNorm in the prologue while each CTA's share is small;
@@ -2498,7 +2480,7 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
         if (rc) return rc;
       }
     }
-    return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs);
+    return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs, conc);
   }
   if (epi->ln_in) {
     rc = ln_before(in_dtype, M, K, A, lda, epi, stream);

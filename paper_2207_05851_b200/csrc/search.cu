@@ -666,8 +666,7 @@ extern "C" int skb_beam_step(const float *logits, int ld_logits, int lp_in, cons
   sv.stage_partials = (sv.lse_part != nullptr && part_bytes <= 160 * 1024) ? 1 : 0;
   auto go = [&](auto kern_ptr, size_t base_smem, int threads) {
     const size_t smem = ((base_smem + 15) & ~size_t(15)) + (sv.stage_partials ? part_bytes : 0);
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kern_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) ensure_smem_fn(kern_ptr, smem);
     launch_k(kern_ptr, sv.B, threads, smem, s, logits, ld_logits, lp_in, sv);
   };
   // SUB warps per beam row (<= 1024 threads, register budget of the

@@ -83,7 +83,12 @@ class StepBuffers:
         # Off by default: measured on B200 the separate LayerNorm launch is
         # faster once several decode streams overlap (4510 vs 3510 sent/s).
         self.fuse_ln = (cdt == torch.bfloat16 and d % 128 == 0 and d <= 1024 and D > 0
-                        and os.environ.get("SKB_FUSE_LN", "0") == "1")
+                        and os.environ.get("SKB_FUSE_LN", "0") == "1" and not model.quantized)
+        # int8 feed-forward scratch (quant.quantize_model)
+        self.int8 = None
+        if model.quantized:
+            from .quant import Int8Scratch
+            self.int8 = Int8Scratch(R, d, c.ff_dim, dev)
         self.ln_ctr = torch.zeros(3 * max(D, 1), (R + 15) // 16 + 1, dtype=I32, device=dev)
         # per-step self-attention plan (skb_attn_plan), allocated on the first
         # (eager) step once the group size is known
@@ -144,6 +149,10 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
         kern.cross_attention_step(sb.q, sb.ckv, li * 2 * d, li * 2 * d + d, sb.L, sb.row_sent,
                                   sb.lengths, sb.ctx, R, H, dh, sb.group)
         resid(sb.ctx, Ly.wo_c, None, 3 * li + 1, Ly.ln_ffn)
+        if getattr(Ly, "q1", None) is not None:  # int8 feed-forward (quant.py)
+            from .quant import ffn_int8
+            ffn_int8(Ly, sb.x, sb.int8, R)
+            continue
         on_h(Ly.w1, sb.f, N.EPI_RELU, Ly.b1, Ly.ln_ffn, fuse)
         resid(sb.f, Ly.w2, Ly.b2, 3 * li + 2, nxt)
     h_ready = fuse and D > 0

@@ -21,9 +21,9 @@ def set_concurrency(n: int) -> None:
     (tiles are sized for a 1/n share of the SMs).  Workspaces captured under
     another setting are not reused (the setting is part of their key)."""
     global concurrency
-    if n != concurrency:
-        N.call("skb_set_concurrency", int(n))
-        concurrency = int(n)
+    if not 1 <= int(n) <= 16:
+        raise ValueError(f"concurrency {n} out of [1, 16]")
+    concurrency = int(n)
 
 
 def _count(n: int = 1) -> None:
@@ -59,6 +59,7 @@ def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_ro
                      N.ptr(step), state_stride, N.ptr(lse_part),
                      lse_part.shape[1] // 2 if lse_part is not None else 0, N.ptr(mask),
                      mask.shape[1] if mask is not None else 0, rows_per_group)
+    epi.streams = concurrency
     if ln is not None:
         epi.ln_gain, epi.ln_bias = ln[0].data_ptr(), ln[1].data_ptr()
         epi.ln_eps = eps
@@ -88,6 +89,7 @@ def gemm_i8(qa, a_scale, qw, w_scale, out, kind=N.EPI_STORE, bias=None, *, M=Non
     M = qa.shape[0] if M is None else M
     Nn, K = qw.shape
     epi = N.Epilogue(kind, N.ptr(bias), out.data_ptr(), out.stride(0), dcode(out))
+    epi.streams = concurrency
     N.call("skb_gemm_i8", M, Nn, K, qa.data_ptr(), qa.stride(0), a_scale.data_ptr(),
            qw.data_ptr(), qw.stride(0), w_scale.data_ptr(), C.byref(epi), stream())
     _count()

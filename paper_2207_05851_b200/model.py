@@ -124,6 +124,7 @@ class Model:
                                         p[b + ".self_attn.wv"]], 0))
             L.wo = cw(p[b + ".self_attn.wo"])
             L.ln2 = norm(b + ".ffn_norm")
+            L.ln_ffn = L.ln2
             L.w1, L.b1 = cw(p[b + ".ffn.w1"]), f32(p[b + ".ffn.b1"])
             L.w2, L.b2 = cw(p[b + ".ffn.w2"]), f32(p[b + ".ffn.b2"])
             self.enc.append(L)
@@ -173,11 +174,15 @@ class Model:
         """Preallocated encoder work buffers for n = B*L positions."""
         c, dev, cdt = self.config, self.device, self.cdt
         d = c.d_model
-        return dict(x=torch.empty(n, d, device=dev), h=torch.empty(n, d, device=dev, dtype=cdt),
+        bufs = dict(x=torch.empty(n, d, device=dev), h=torch.empty(n, d, device=dev, dtype=cdt),
                     qkv=torch.empty(n, 3 * d, device=dev, dtype=cdt),
                     ctx=torch.empty(n, d, device=dev, dtype=cdt),
                     f=torch.empty(n, c.ff_dim, device=dev, dtype=cdt),
                     xc=torch.empty(n, d, device=dev, dtype=cdt))
+        if self.quantized:
+            from .quant import Int8Scratch
+            bufs["int8"] = Int8Scratch(n, d, c.ff_dim, dev)
+        return bufs
 
     def encode_device(self, ids: torch.Tensor, fids: torch.Tensor | None, lengths: torch.Tensor,
                       B: int, L: int, bufs: dict | None = None) -> torch.Tensor:
@@ -205,6 +210,12 @@ class Model:
             kern.gemm(h, Ly.wqkv, qkv)
             kern.encoder_attention(qkv, lengths, ctx, B, L, H, dh)
             kern.gemm(ctx, Ly.wo, x, N.EPI_RESID)
+            if getattr(Ly, "q1", None) is not None:  # int8 feed-forward (quant.py)
+                from .quant import Int8Scratch, ffn_int8
+                if bufs.get("int8") is None or bufs["int8"].h.shape[0] < n:
+                    bufs["int8"] = Int8Scratch(n, d, c.ff_dim, dev)
+                ffn_int8(Ly, x, bufs["int8"], n)
+                continue
             kern.layernorm(x, *Ly.ln2, h)
             kern.gemm(h, Ly.w1, f, N.EPI_RELU, Ly.b1)
             kern.gemm(f, Ly.w2, x, N.EPI_RESID, Ly.b2)

@@ -66,3 +66,16 @@ def test_bench_cli_reports_positive_rates(tmp_path, capsys):
     vals = dict(line.split(" = ") for line in capsys.readouterr().out.splitlines())
     assert set(vals) == {"sentences_per_sec", "tokens_per_sec", "decoder_step_cost"}
     assert all(float(v) > 0 for v in vals.values())
+
+
+@pytest.mark.gpu
+def test_translate_cli_quantized_int8(tmp_path, monkeypatch, capsys):
+    """`translate --quantize int8` (cli.py:130-131): the feed-forward layers
+    run on the int8 path and every line still gets a translation."""
+    from paper_2207_05851_b200 import cli
+    mdir = _save_toy(tmp_path)
+    monkeypatch.setattr(sys, "stdin", io.StringIO("w1 w2 w3\nw4 w5\n"))
+    capsys.readouterr()
+    assert cli.main(["translate", "-m", str(mdir), "--quantize", "int8", "--json"]) == 0
+    out = [json.loads(x) for x in capsys.readouterr().out.splitlines()]
+    assert len(out) == 2 and all("error" not in o for o in out)

@@ -118,7 +118,7 @@ def test_tiny_bf16_agreement_report():
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
 def test_concurrent_stream_batches_identical(precision):
     """decode_jobs runs its batches concurrently on several CUDA streams, with
-    GEMM tiles sized for the shared device (skb_set_concurrency).  Tile sizes
+    GEMM tiles sized for the shared device (skb_epilogue.streams).  Tile sizes
     never change numerics, so the records are identical to one stream."""
     from paper_2207_05851_b200 import engine
     from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
