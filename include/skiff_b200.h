@@ -169,6 +169,22 @@ int skb_gemm_force_pc(int mode, int na, int pairs);
  * (STORE / RELU with bias, or RESID x += ... + bias).  A [M, lda] and
  * W [N, ldw] int8 K-major, K % 16 == 0, 16-byte aligned.
  */
+/*
+ * Teacher-forced decoder pass (replaces skiff model.py:444-493
+ * forward_sequence): all B x T target positions at once.
+ * skb_causal_self_attention: multi-head self-attention of B sequences of T
+ * positions over a fused [B*T, 3*H*dh] Q|K|V buffer, query t attending to
+ * keys <= t (kernels.py:487-491 causal_mask); lengths [B] (device) bound the
+ * keys of each sequence.
+ * skb_ssru_scan: the SSRU recurrence along T (model.py:482-493) from the
+ * fp32 [B*T, 2d] interleaved gate GEMM output g; x += relu(c_t).
+ */
+int skb_causal_self_attention(int B, int T, int H, int dh, const void *qkv, int ld_qkv,
+                              int qkv_dtype, const int *lengths, void *ctx, int ldc, int ctx_dtype,
+                              void *stream);
+int skb_ssru_scan(int B, int T, int d, const float *g, int ldg, const float *bias, float *x, int ldx,
+                  void *stream);
+
 int skb_quantize_rows(int rows, int k, const float *x, int ldx, void *q, int ldq, float *scales,
                       void *stream);
 int skb_gemm_i8(int M, int N, int K, const void *A, int lda, const float *a_scale, const void *W,

@@ -65,6 +65,8 @@ SIGNATURES = {
     "skb_gemm_force_sw": [i32, i32, i32],
     "skb_gemm_force_pc": [i32, i32, i32],
     "skb_quantize_rows": [i32, i32, vp, i32, vp, i32, vp, vp],
+    "skb_causal_self_attention": [i32, i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp],
+    "skb_ssru_scan": [i32, i32, i32, vp, i32, vp, vp, i32, vp],
     "skb_gemm_i8": [i32, i32, i32, vp, i32, vp, vp, i32, vp, C.POINTER(Epilogue), vp],
     "skb_layernorm": [i32, i32, vp, i32, vp, vp, C.c_float, vp, i32, i32, vp],
     "skb_embed_target": [i32, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp],

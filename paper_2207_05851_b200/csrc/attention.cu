@@ -118,7 +118,8 @@ __device__ __forceinline__ const void *elem_ptr(const void *base, int dtype, siz
 __global__ void __launch_bounds__(256) k_encoder_attention(int B, int L, int H, int dh,
                                                            const void *qkv, int ld_qkv, int qkv_dtype,
                                                            const int *lengths, float scale,
-                                                           void *ctx, int ldc, int ctx_dtype) {
+                                                           void *ctx, int ldc, int ctx_dtype,
+                                                           int causal) {
   PDL_ENTRY();
   const int b = blockIdx.x / H, h = blockIdx.x % H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(256) k_encoder_attention(int B, int L, int H, 
   const size_t qrow = (size_t)(b * L + l) * ld_qkv;
   for (int c = lane; c < dh; c += 32) qs[warp][c] = load_f(qkv, qkv_dtype, qrow + h * dh + c);
   __syncwarp();
-  const int len = lengths[b];
+  const int len = causal ? min(lengths[b], l + 1) : lengths[b];  // causal: keys <= l
   WarpSoftmax st;
   st.init();
   for (int k0 = 0; k0 < len; k0 += 32) {
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(128) k_cross_attention_step(
 __global__ void __launch_bounds__(256) k_attn_smem(
     int R, int G, int H, int dh, const void *q, int ldq, int q_dtype, int qoff, const void *kv,
     int ld_kv, int kv_dtype, int koff, int voff, int L, const int *row_sent, const int *lengths,
-    float scale, void *ctx, int ldc, int ctx_dtype) {
+    float scale, void *ctx, int ldc, int ctx_dtype, int causal) {
   PDL_ENTRY();
   extern __shared__ float sm[];
   const int g = blockIdx.x, h = blockIdx.y;
@@ -281,10 +282,11 @@ __global__ void __launch_bounds__(256) k_attn_smem(
     __syncwarp();
     WarpSoftmax st;
     st.init();
-    for (int k0 = 0; k0 < len; k0 += 32) {
+    const int leni = causal ? min(len, i + 1) : len;  // causal: query i sees keys <= i
+    for (int k0 = 0; k0 < leni; k0 += 32) {
       const int j = k0 + lane;
       float s = -INFINITY;
-      if (j < len) {
+      if (j < leni) {
         const float *kr = Ks + j * ldk;
         float a = 0.f;
         for (int c = 0; c < dh; ++c) a = fmaf(qs[c], kr[c], a);
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(256) k_attn_smem(
 #pragma unroll
       for (int jj = 0; jj < MAX_DH / 32; ++jj) st.o[jj] *= corr;
       st.m = mnew;
-      const int nk = min(32, len - k0);
+      const int nk = min(32, leni - k0);
       for (int k = 0; k < nk; ++k) {
         const float pk = __shfl_sync(0xffffffffu, p, k);
         const float *vr = Vs + (k0 + k) * ldk;
@@ -502,7 +504,7 @@ template <int DH>
 __global__ void __launch_bounds__(128) k_attn_mma(
     int R, int G, int H, const __nv_bfloat16 *q, int ldq, const __nv_bfloat16 *kv, int ld_kv,
     int koff, int voff, int L, const int *row_sent, const int *lengths, float scale, void *ctx,
-    int ldc, int ctx_dtype) {
+    int ldc, int ctx_dtype, int causal) {
   PDL_ENTRY();
   constexpr int LD = DH + 8;        // padded smem row (bf16)
   constexpr int KC = 64;            // keys per chunk
@@ -558,7 +560,11 @@ __global__ void __launch_bounds__(128) k_attn_mma(
 #pragma unroll
     for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
-    for (int j0 = 0; j0 < len; j0 += KC) {
+    // causal (teacher-forced decoder): query i of the group sees keys <= i
+    const int lim_a = causal ? min(len, rt + gq + 1) : len;
+    const int lim_b = causal ? min(len, rt + gq + 9) : len;
+    const int jend = causal ? min(len, rt + 16) : len;
+    for (int j0 = 0; j0 < jend; j0 += KC) {
       // ---- S = Q K^T for 64 keys (8 n-tiles)
       float sc[KC / 8][4];
 #pragma unroll
@@ -578,9 +584,9 @@ __global__ void __launch_bounds__(128) k_attn_mma(
       for (int nt = 0; nt < KC / 8; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const bool ok = j0 + nt * 8 + tq * 2 + e < len;
-          sc[nt][e] = ok ? sc[nt][e] * scale : -INFINITY;
-          sc[nt][2 + e] = ok ? sc[nt][2 + e] * scale : -INFINITY;
+          const int j = j0 + nt * 8 + tq * 2 + e;
+          sc[nt][e] = j < lim_a ? sc[nt][e] * scale : -INFINITY;
+          sc[nt][2 + e] = j < lim_b ? sc[nt][2 + e] * scale : -INFINITY;
           cm_a = fmaxf(cm_a, sc[nt][e]);
           cm_b = fmaxf(cm_b, sc[nt][2 + e]);
         }
@@ -823,7 +829,7 @@ static bool attn_vec_ok(int dh, int q_dtype, int kv_dtype, const void *q, int ld
 static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, int qoff,
                            const void *kv, int ld_kv, int koff, int voff, int L, const int *row_sent,
                            const int *lengths, float scale, void *ctx, int ldc, int ctx_dtype,
-                           cudaStream_t st) {
+                           cudaStream_t st, int causal = 0) {
   {
     // tensor-core path: one warp per 16 query rows
     const int Lp = (L + 63) / 64 * 64;
@@ -839,13 +845,13 @@ static int launch_attn_vec(int R, int G, int H, int dh, const void *q, int ldq, 
       auto *kb = reinterpret_cast<const __nv_bfloat16 *>(kv);
       if (dh == 64)
         launch_k(k_attn_mma<64>, grid, 32 * nwm, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
-                 row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+                 row_sent, lengths, scale, ctx, ldc, ctx_dtype, causal);
       else if (dh == 128)
         launch_k(k_attn_mma<128>, grid, 32 * nwm, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
-                 row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+                 row_sent, lengths, scale, ctx, ldc, ctx_dtype, causal);
       else
         launch_k(k_attn_mma<32>, grid, 32 * nwm, smem, st, R, G, H, qb, ldq, kb, ld_kv, koff, voff, L,
-                 row_sent, lengths, scale, ctx, ldc, ctx_dtype);
+                 row_sent, lengths, scale, ctx, ldc, ctx_dtype, causal);
       return 0;
     }
   }
@@ -1359,14 +1365,17 @@ extern "C" int skb_attn_plan(int R, int rows_per_group, int S_max, const int *an
   return SKB_OK;
 }
 
-extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qkv, int ld_qkv,
-                                     int qkv_dtype, const int *lengths, void *ctx, int ldc,
-                                     int ctx_dtype, void *stream) {
-  if (B <= 0 || L <= 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "encoder_attention: shape");
-  if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "encoder_attention: head dim %d > %d", dh, MAX_DH);
+// Full self-attention of B sequences of width L over a fused [B*L, 3*H*dh]
+// Q|K|V buffer: key padding by lengths (encoder, model.py:420-429) and, with
+// causal, query l sees keys <= l (teacher-forced decoder, model.py:456-462).
+static int full_self_attention(int B, int L, int H, int dh, const void *qkv, int ld_qkv,
+                               int qkv_dtype, const int *lengths, void *ctx, int ldc, int ctx_dtype,
+                               void *stream, int causal) {
+  if (B <= 0 || L <= 0 || H <= 0 || dh <= 0) return fail(SKB_ERR_SHAPE, "self attention: shape");
+  if (dh > MAX_DH) return fail(SKB_ERR_UNSUPPORTED, "self attention: head dim %d > %d", dh, MAX_DH);
   if (attn_vec_ok(dh, qkv_dtype, qkv_dtype, qkv, ld_qkv, qkv, ld_qkv, H * dh, 2 * H * dh, 0) &&
       launch_attn_vec(B * L, L, H, dh, qkv, ld_qkv, 0, qkv, ld_qkv, H * dh, 2 * H * dh, L, nullptr,
-                      lengths, attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream)) == 0) {
+                      lengths, attn_scale(dh), ctx, ldc, ctx_dtype, as_stream(stream), causal) == 0) {
     SKB_CHECK_LAUNCH("k_attn_mma(encoder)");
     return SKB_OK;
   }
@@ -1379,16 +1388,30 @@ extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qk
       dim3 g2(B, H);
       launch_k(k_attn_smem, g2, 32 * nw, smem, as_stream(stream), 
           B * L, L, H, dh, qkv, ld_qkv, qkv_dtype, 0, qkv, ld_qkv, qkv_dtype, D, 2 * D, L, nullptr,
-          lengths, attn_scale(dh), ctx, ldc, ctx_dtype);
+          lengths, attn_scale(dh), ctx, ldc, ctx_dtype, causal);
       SKB_CHECK_LAUNCH("k_attn_smem(encoder)");
       return SKB_OK;
     }
   }
   dim3 grid(B * H, (L + 7) / 8);
   launch_k(k_encoder_attention, grid, 256, 0, as_stream(stream), B, L, H, dh, qkv, ld_qkv, qkv_dtype,
-                                                           lengths, attn_scale(dh), ctx, ldc, ctx_dtype);
+           lengths, attn_scale(dh), ctx, ldc, ctx_dtype, causal);
   SKB_CHECK_LAUNCH("k_encoder_attention");
   return SKB_OK;
+}
+
+extern "C" int skb_encoder_attention(int B, int L, int H, int dh, const void *qkv, int ld_qkv,
+                                     int qkv_dtype, const int *lengths, void *ctx, int ldc,
+                                     int ctx_dtype, void *stream) {
+  return full_self_attention(B, L, H, dh, qkv, ld_qkv, qkv_dtype, lengths, ctx, ldc, ctx_dtype,
+                             stream, 0);
+}
+
+extern "C" int skb_causal_self_attention(int B, int T, int H, int dh, const void *qkv, int ld_qkv,
+                                         int qkv_dtype, const int *lengths, void *ctx, int ldc,
+                                         int ctx_dtype, void *stream) {
+  return full_self_attention(B, T, H, dh, qkv, ld_qkv, qkv_dtype, lengths, ctx, ldc, ctx_dtype,
+                             stream, 1);
 }
 
 // Tensor-core self-attention launch (k_self_attn_tc); -1 if the shape or
@@ -1560,7 +1583,7 @@ extern "C" int skb_cross_attention_step(int R, int H, int dh, const void *q, int
       launch_k(k_attn_smem, g2, 32 * nw, smem, as_stream(stream), R, G, H, dh, q, ldq, q_dtype, 0, kv,
                                                             ld_kv, kv_dtype, koff, voff, L, row_sent,
                                                             lengths, attn_scale(dh), ctx, ldc,
-                                                            ctx_dtype);
+                                                            ctx_dtype, 0);
       SKB_CHECK_LAUNCH("k_attn_smem(cross)");
       return SKB_OK;
     }

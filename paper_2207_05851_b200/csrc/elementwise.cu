@@ -423,3 +423,39 @@ extern "C" int skb_quantize_rows(int rows, int k, const float *x, int ldx, void 
   SKB_CHECK_LAUNCH("k_quantize_rows");
   return SKB_OK;
 }
+
+// --------------------------------------------------------- SSRU scan
+// The SSRU recurrence over a whole target sequence (model.py:482-493
+// _ssru_scan, cell model.py:268-272) for the teacher-forced pass: g is the
+// fp32 [B*T, 2d] output of the interleaved [W_f; W] GEMM (column 2j = W_f h,
+// 2j+1 = W h), bias the interleaved [2d] bias (b_f at even columns).  Per
+// (sentence, column): c_0 = 0, f = sigmoid(W_f h + b_f), c = f c + (1 - f)
+// W h, x += relu(c) — the arithmetic of the decode step's SSRU epilogue.
+namespace skb {
+__global__ void k_ssru_scan(int B, int T, int d, const float *__restrict__ g, int ldg,
+                            const float *__restrict__ bias, float *__restrict__ x, int ldx) {
+  PDL_ENTRY();
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || j >= d) return;
+  const float bf = bias ? bias[2 * j] : 0.f;
+  float c = 0.f;
+  for (int t = 0; t < T; ++t) {
+    const size_t r = (size_t)b * T + t;
+    const float f = sigmoid_ref(g[r * ldg + 2 * j] + bf);
+    c = f * c + (1.0f - f) * g[r * ldg + 2 * j + 1];
+    float *xp = x + r * ldx + j;
+    *xp = *xp + fmaxf(c, 0.f);
+  }
+}
+}  // namespace skb
+
+extern "C" int skb_ssru_scan(int B, int T, int d, const float *g, int ldg, const float *bias,
+                             float *x, int ldx, void *stream) {
+  if (B <= 0 || T <= 0 || d <= 0 || ldg < 2 * d || ldx < d)
+    return fail(SKB_ERR_SHAPE, "ssru_scan: B=%d T=%d d=%d", B, T, d);
+  dim3 grid((d + 127) / 128, B);
+  launch_k(k_ssru_scan, grid, 128, 0, as_stream(stream), B, T, d, g, ldg, bias, x, ldx);
+  SKB_CHECK_LAUNCH("k_ssru_scan");
+  return SKB_OK;
+}

@@ -902,3 +902,86 @@ class ProtocolState:
             prev = (t - 1) & 1
             for li in range(len(m.dec)):
                 sb.cell[li, prev, :n].copy_(cells[li])
+
+
+# ============================================================ teacher forced
+def teacher_forced(model: Model, src_ids, src_factor_ids, src_lengths, trg_in_ids,
+                   trg_in_factor_ids):
+    """The full teacher-forced pass (model.py:444-493) for all B x T target
+    positions at once: one batched encoder, then per decoder layer GEMMs over
+    B*T rows with the causal self-attention kernel (or the SSRU gate GEMM +
+    recurrence scan), cross-attention of the B*T queries against each
+    sentence's encoder K/V, the feed-forward block, and one output
+    projection.  Returns (surface [B, T, V] fp32, factors [B, T, Vk], enc)."""
+    c = model.config
+    d, H, dh, D = c.d_model, c.heads, c.head_dim, c.decoder_layers
+    dev, cdt = model.device, model.cdt
+    trg = np.asarray(trg_in_ids)
+    if trg.ndim != 2:
+        raise ShapeError(f"trg_in_ids must be [B, T], got shape {trg.shape}")
+    B, T = trg.shape
+    fac_in = [np.asarray(f) for f in trg_in_factor_ids]
+    if len(fac_in) != len(c.target_factor_specs):
+        raise ShapeError(f"model wants {len(c.target_factor_specs)} target factor streams, "
+                         f"got {len(fac_in)}")
+    if T > model.max_steps:
+        raise ShapeError(f"target length {T} exceeds the {model.max_steps} decoder positions")
+    if (trg < 0).any() or (trg >= c.trg_vocab_size).any():
+        raise ShapeError("ids out of range for embedding table")
+    st = ProtocolState.create(model, src_ids, src_factor_ids, src_lengths)
+    n = B * T
+    nf = len(fac_in)
+    with torch.cuda.device(dev):
+        x = torch.empty(n, d, device=dev)
+        ids = torch.from_numpy(trg.reshape(-1).astype(np.int32)).to(dev)
+        fids = torch.from_numpy(np.stack(fac_in).reshape(max(nf, 1), -1).astype(np.int32)
+                                if nf else np.zeros((1, n), np.int32)).to(dev)
+        # target embedding + positions 0..T-1 (+ summed factors), model.py:399-410
+        kern.embed_source(ids, model.E_trg, model.pe_trg, [d] * nf, [0] * nf,
+                          fids if nf else None, model.trg_ftab_ptrs, x, B, T, d)
+        h = torch.empty(n, d, device=dev, dtype=cdt)
+        ctx = torch.empty(n, d, device=dev, dtype=cdt)
+        q = torch.empty(n, d, device=dev, dtype=cdt)
+        f = torch.empty(n, c.ff_dim, device=dev, dtype=cdt)
+        tlen = torch.full((B,), T, dtype=I32, device=dev)
+        row_sent = torch.arange(n, dtype=I32, device=dev) // T
+        int8 = None
+        if model.quantized:
+            from .quant import Int8Scratch
+            int8 = Int8Scratch(n, d, c.ff_dim, dev)
+        if c.decoder_kind == SSRU:
+            g = torch.empty(n, 2 * d, device=dev)
+        else:
+            qkv = torch.empty(n, 3 * d, device=dev, dtype=cdt)
+        for li, Ly in enumerate(model.dec):
+            kern.layernorm(x, *Ly.ln_self, h)
+            if c.decoder_kind == SSRU:
+                kern.gemm(h, Ly.w_ssru, g, N.EPI_STORE)
+                kern.ssru_scan(g, Ly.b_ssru, x, B, T, d)
+            else:
+                kern.gemm(h, Ly.wqkv, qkv, N.EPI_STORE)
+                kern.causal_self_attention(qkv, tlen, ctx, B, T, H, dh)
+                kern.gemm(ctx, Ly.wo, x, N.EPI_RESID)
+            kern.layernorm(x, *Ly.ln_cross, h)
+            kern.gemm(h, Ly.wq_c, q, N.EPI_STORE)
+            kern.cross_attention_step(q, st.ckv, li * 2 * d, li * 2 * d + d, st.L, row_sent,
+                                      st.len_d, ctx, n, H, dh, T)
+            kern.gemm(ctx, Ly.wo_c, x, N.EPI_RESID)
+            if getattr(Ly, "q1", None) is not None:
+                from .quant import ffn_int8
+                ffn_int8(Ly, x, int8, n)
+                continue
+            kern.layernorm(x, *Ly.ln_ffn, h)
+            kern.gemm(h, Ly.w1, f, N.EPI_RELU, Ly.b1)
+            kern.gemm(f, Ly.w2, x, N.EPI_RESID, Ly.b2)
+        kern.layernorm(x, *model.ln_final, h)
+        V = c.trg_vocab_size
+        surface = torch.empty(n, V, device=dev)
+        kern.gemm(h, model.E_trg_c, surface, N.EPI_STORE)
+        facs = []
+        if nf:
+            fac = torch.empty(n, model.w_fac.shape[0], device=dev)
+            kern.gemm(h, model.w_fac, fac, N.EPI_STORE, model.b_fac)
+            off = model.fac_off.cpu().numpy()
+            facs = [fac[:, off[k]:off[k + 1]].reshape(B, T, -1) for k in range(nf)]
+    return surface.view(B, T, V), facs, st

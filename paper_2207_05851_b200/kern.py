@@ -127,6 +127,20 @@ def encoder_attention(qkv, lengths, ctx, B, L, H, dh):
     _count()
 
 
+def causal_self_attention(qkv, lengths, ctx, B, T, H, dh):
+    """Teacher-forced decoder self-attention over [B*T, 3d] (model.py:456-462)."""
+    N.call("skb_causal_self_attention", B, T, H, dh, qkv.data_ptr(), qkv.stride(0), dcode(qkv),
+           lengths.data_ptr(), ctx.data_ptr(), ctx.stride(0), dcode(ctx), stream())
+    _count()
+
+
+def ssru_scan(g, bias, x, B, T, d):
+    """SSRU recurrence along T (model.py:482-493): x += relu(c_t)."""
+    N.call("skb_ssru_scan", B, T, d, g.data_ptr(), g.stride(0), N.ptr(bias), x.data_ptr(),
+           x.stride(0), stream())
+    _count()
+
+
 def self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S_max, group=1, plan=None):
     """plan (from attn_plan) replaces the per-layer ancestor walk."""
     if plan is not None:

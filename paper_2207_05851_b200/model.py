@@ -286,11 +286,23 @@ class Model:
     def forward_sequence(self, src_ids, src_factor_ids, src_lengths, trg_in_ids,
                          trg_in_factor_ids) -> "SequenceOutput":
         """model.py:444-492, teacher forced: target inputs carry BOS at
-        position 0 (and the shift marker in factor streams).  The decoder
-        runs position by position on the device step kernels — the causal
-        self-attention of the full pass is the incremental attention over the
-        cached K/V (the reference's own invariant, test_model.py:270-282) —
-        and the SSRU recurrence is its scan.  surface: raw logits [B, T, V]."""
+        position 0 (and the shift marker in factor streams).  One batched
+        pass over all B x T positions (engine.teacher_forced: causal
+        self-attention kernel, SSRU recurrence scan, B*T-row GEMMs).
+        surface: raw logits [B, T, V]."""
+        from .engine import _HostView, teacher_forced
+        surface, facs, st = teacher_forced(self, src_ids, src_factor_ids, src_lengths,
+                                           trg_in_ids, trg_in_factor_ids)
+        nvs = None
+        if self.config.nvs_enabled:
+            nvs = _HostView(self.nvs_logits_device(st.enc.x, st.enc.lengths, st.enc.B, st.enc.L))
+        return SequenceOutput(_HostView(surface), [_HostView(f) for f in facs], nvs)
+
+    def forward_sequence_stepwise(self, src_ids, src_factor_ids, src_lengths, trg_in_ids,
+                                  trg_in_factor_ids) -> "SequenceOutput":
+        """The same outputs position by position through the incremental
+        decode step (cached K/V, SSRU state) — the reference's own invariant
+        between the two paths (test_model.py:270-282)."""
         from .engine import _HostView
         trg = np.asarray(trg_in_ids)
         if trg.ndim != 2:

@@ -94,3 +94,35 @@ def test_forward_sequence_matches_reference(name, precision):
     worst = float(np.abs(O.log_softmax(got) - O.log_softmax(ref)).max())
     assert worst <= TOL[precision], worst
     assert len(out.factors) == ntf
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("name", ["toy", "ssru", "tiny", "factored", "srcfac"])
+def test_batched_teacher_forced_pass(name, precision):
+    """forward_sequence runs all B x T positions in one pass (causal
+    self-attention kernel / SSRU scan, B*T-row GEMMs): a ragged batch of 3
+    sentences vs the oracle's full-sequence restatement of model.py:444-492,
+    and vs the stepwise incremental path (the reference invariant
+    test_model.py:270-282)."""
+    m = product_model(name, precision)
+    om = oracle_model(name)
+    c = m.config
+    nsf, ntf = len(c.source_factor_specs), len(c.target_factor_specs)
+    rng = np.random.default_rng(17)
+    B, L, T = 3, 6, 7
+    lens = np.array([6, 3, 5])
+    src = rng.integers(4, c.src_vocab_size, size=(B, L)).astype(np.int64)
+    src_f = [rng.integers(4, s.vocab_size, size=(B, L)).astype(np.int64) for s in c.source_factor_specs]
+    trg = rng.integers(4, c.trg_vocab_size, size=(B, T)).astype(np.int64)
+    trg[:, 0] = 2  # BOS
+    trg_f = [rng.integers(5, s.vocab_size, size=(B, T)).astype(np.int64) for s in c.target_factor_specs]
+    for f in trg_f:
+        f[:, 0] = 4  # shift marker
+    got = m.forward_sequence(src, src_f, lens, trg, trg_f).surface.data
+    want = om.forward_sequence(src, src_f, lens, trg, trg_f)
+    assert got.shape == (B, T, c.trg_vocab_size)
+    worst = float(np.abs(O.log_softmax(got) - O.log_softmax(np.asarray(want, np.float32))).max())
+    assert worst <= TOL[precision], worst
+    step = m.forward_sequence_stepwise(src, src_f, lens, trg, trg_f).surface.data
+    worst = float(np.abs(O.log_softmax(got) - O.log_softmax(step)).max())
+    assert worst <= TOL[precision], worst
