@@ -255,25 +255,11 @@ def gemm_roofline(model, R, L, peak, U=None):
     for A, W, o, kind, b in calls:
         flops += 2 * R * W.shape[0] * W.shape[1]
 
-    # the decode step's output projection runs in candidate mode (bf16):
-    # per-tile top-K records instead of fp32 logits for non-forced rows
-    from paper_2207_05851_b200 import engine as _eng
-    cand = force = None
-    if _eng.LOGITS_CAND and cdt == torch.bfloat16:
-        cand = torch.zeros(R, ((U + 127) // 128) * 12, device=dev)
-        nb = (R + 4) // 5
-        force = (torch.zeros(1, dtype=torch.int32, device=dev),
-                 torch.zeros(nb, dtype=torch.int32, device=dev),
-                 torch.full((nb,), 70, dtype=torch.int32, device=dev))
-
     def run(cs):
         for A, W, o, kind, b in cs:
-            lg = kind == N.EPI_LOGITS
-            kern.gemm(A, W, o, kind, b, lse_part=part if lg else None,
+            kern.gemm(A, W, o, kind, b, lse_part=part if kind == N.EPI_LOGITS else None,
                       c_state=cell if kind == N.EPI_SSRU else None,
-                      src_row=rows if kind == N.EPI_SSRU else None,
-                      cand=cand if lg else None, cand_k=5, force=force if lg else None,
-                      rows_per_group=5 if lg else 1)
+                      src_row=rows if kind == N.EPI_SSRU else None)
 
     for _ in range(3):
         run(calls)

@@ -109,23 +109,6 @@ typedef struct skb_epilogue {
   /* (0 or 1 = this call has the GPU to itself): tiles are sized for a      */
   /* 1/streams share of the SMs.  Never changes the numbers.                */
   int streams;
-  /* SKB_EPI_LOGITS candidate mode (cand != NULL, bf16 tcgen05 path):        */
-  /* instead of storing the fp32 logits, write for every row m and 128-      */
-  /* column tile j the record cand[(m * cand_ld + j) * 12 ...]: the tile's   */
-  /* top cand_k (<= 8) active columns in (value desc, column asc) order as   */
-  /* values[8] (-inf past the end), column offsets in the tile as 8 bytes    */
-  /* (0xff past the end), then the largest unlisted active value ("next").   */
-  /* The beam step proves from "next" that no unlisted column reaches its    */
-  /* top K (and flags the sentence otherwise).  Rows whose sentence is      */
-  /* forced at this step (t = *force_step < force_prefix_len[b] or          */
-  /* t == force_max_len[b] - 1, b = m / rows_per_group) still get their full */
-  /* logits in out.  The (max, sum exp) partials are written as always.     */
-  float *cand;
-  int cand_ld;
-  int cand_k;
-  const int *force_step;
-  const int *force_prefix_len;
-  const int *force_max_len;
 } skb_epilogue;
 
 /* Library identity / diagnostics */
@@ -357,14 +340,6 @@ typedef struct skb_beam_state {
   int *best_parent;       /* [B] beam index of the parent row at step steps-1 */
   int *best_fac;          /* [B, n_factors] factor entry of the EOS step */
   int *n_done;            /* [1] sentences finished (for host polling)      */
-  /* candidate mode (see skb_epilogue.cand): per row and 128-column tile the */
-  /* listed columns; with prune, non-forced steps read these instead of the */
-  /* logits.  inexact[B] is set for a sentence whose step could not be      */
-  /* proven exact from the lists (the caller reruns it with full logits).   */
-  const float *cand;
-  int cand_ld;
-  int cand_k;
-  int *inexact;
 } skb_beam_state;
 
 /*

@@ -35,9 +35,7 @@ class Epilogue(C.Structure):
                 ("splitk_counters_n", i32), ("ln_gain", vp), ("ln_bias", vp),
                 ("ln_eps", C.c_float), ("ln_out", vp), ("ln_ldo", i32), ("ln_counter", vp),
                 ("ln_in", vp), ("ln_in_ld", i32), ("ln_in_gain", vp), ("ln_in_bias", vp),
-                ("ln_in_eps", C.c_float), ("streams", i32), ("cand", vp), ("cand_ld", i32),
-                ("cand_k", i32), ("force_step", vp), ("force_prefix_len", vp),
-                ("force_max_len", vp)]
+                ("ln_in_eps", C.c_float), ("streams", i32)]
 
 
 class BeamState(C.Structure):
@@ -52,8 +50,7 @@ class BeamState(C.Structure):
                 ("cand_score", vp), ("cand_lp", vp),
                 ("cand_col", vp), ("cand_cnt", vp), ("row_argmax", vp), ("fac_choice", vp),
                 ("counter", vp), ("best_norm", vp), ("best_logprob", vp), ("best_steps", vp),
-                ("best_forced", vp), ("best_parent", vp), ("best_fac", vp), ("n_done", vp),
-                ("cand", vp), ("cand_ld", i32), ("cand_k", i32), ("inexact", vp)]
+                ("best_forced", vp), ("best_parent", vp), ("best_fac", vp), ("n_done", vp)]
 
 
 # (name, argtypes) — must match include/skiff_b200.h

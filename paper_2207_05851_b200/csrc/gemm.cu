@@ -60,25 +60,7 @@ struct EpiArgs {
   // weights [N]; out = (f32(acc) * a_scale[m]) * w_scale[n] (+bias ...)
   const float *a_scale;
   const float *w_scale;
-  // LOGITS candidate mode (cand != nullptr): per row and 128-column tile the
-  // top cand_k active columns + the next value instead of the fp32 logits,
-  // which are still stored for rows whose sentence is forced at this step
-  float *cand;
-  int cand_ld;
-  int cand_k;
-  const int *f_step;
-  const int *f_plen;
-  const int *f_mlen;
 };
-
-// Row m's sentence is forced at this step (target prefix or the final EOS,
-// search.py:296-297, 351-356): the beam step reads its logits directly.
-__device__ __forceinline__ bool row_forced(const EpiArgs &e, int m) {
-  if (!e.f_step) return false;
-  const int b = m / e.rows_per_group;
-  const int t = *e.f_step;
-  return t < e.f_plen[b] || t == e.f_mlen[b] - 1;
-}
 
 // Partial log-softmax statistics of `cnt` consecutive logits of row m
 // starting at column n (a 32-column group): (max, sum exp(x - max)) over the
@@ -1131,144 +1113,6 @@ __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int
   }
 }
 
-// LOGITS candidate mode: per tile row (128 logits of one activation row),
-// the top cand_k active columns in the order (value desc, column asc) —
-// the order the beam step breaks ties in (search.py:363) — and the largest
-// value not listed ("next"), so the beam step can prove that no unlisted
-// column reaches its top K.  Record [12 floats]: values[8], column offsets
-// (8 bytes), next, unused.  Warp-uniform selection rounds on order-
-// preserving integer images (redux.sync), one tile row per warp iteration.
-__device__ __forceinline__ unsigned ord_f32(float v) {
-  const unsigned u = __float_as_uint(v + 0.0f);
-  return (u >> 31) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float unord_f32(unsigned o) {
-  return __uint_as_float((o >> 31) ? (o & 0x7fffffffu) : ~o);
-}
-
-template <int E>
-__device__ __forceinline__ void logits_cand_t(const EpiArgs &e, uint32_t stg, int M, int N, int m0,
-                                              int n0, int rows, int warp_e, int lane) {
-  constexpr int U = 4;  // tile rows per iteration: independent selection chains (ILP)
-  const int g = lane >> 3, sub = lane & 7;
-  const int n = n0 + g * 32;
-  unsigned tail = 0xffffffffu;
-  if (n >= N) tail = 0u;
-  else if (N - n < 32) tail = (1u << (N - n)) - 1u;
-#pragma unroll 1
-  for (int ml0 = warp_e; ml0 < rows && m0 + ml0 < M; ml0 += 4 * U) {
-    // each lane's 4 values of each row, sorted (image desc, column asc):
-    // a selection round pops the warp-best head
-    unsigned o[U][4];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ml = ml0 + 4 * u, m = m0 + ml;
-      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-      unsigned b4 = 0u;
-      if (ml < rows && m < M) {
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w)
-                     : "r"(stg + (uint32_t)(ml * 128 + lane * 4) * 4u));
-        unsigned bits = tail;
-        if (e.mask && tail) bits &= e.mask[(size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5)];
-        b4 = (bits >> (sub * 4)) & 0xfu;
-      }
-      // image << 2 | (3 - q): one key orders (value desc, column asc) among a
-      // lane's 4 values; 0 = masked (images of finite values are >= 2^23)
-      const unsigned k0 = (b4 & 1u) ? ord_f32(f.x) : 0u, k1 = (b4 & 2u) ? ord_f32(f.y) : 0u;
-      const unsigned k2 = (b4 & 4u) ? ord_f32(f.z) : 0u, k3 = (b4 & 8u) ? ord_f32(f.w) : 0u;
-      o[u][0] = k0; o[u][1] = k1; o[u][2] = k2; o[u][3] = k3;
-    }
-    float vals[U][E];
-    unsigned cols[U][2];
-    float next[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      cols[u][0] = cols[u][1] = 0xffffffffu;
-      next[u] = -INFINITY;
-    }
-#pragma unroll
-    for (int j = 0; j <= E; ++j) {
-      unsigned lb[U], lq[U], best[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {  // lane-local first max
-        lb[u] = o[u][0];
-        lq[u] = 0;
-#pragma unroll
-        for (int q = 1; q < 4; ++q)
-          if (o[u][q] > lb[u]) { lb[u] = o[u][q]; lq[u] = q; }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) best[u] = __reduce_max_sync(0xffffffffu, lb[u]);
-      unsigned bc[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        bc[u] = __reduce_min_sync(0xffffffffu, (lb[u] == best[u] && best[u] != 0u)
-                                                   ? (unsigned)(lane * 4) + lq[u] : 0xffffffffu);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float v = best[u] == 0u ? -INFINITY : unord_f32(best[u]);
-        if (j == E) {
-          next[u] = v;
-        } else {
-          vals[u][j] = v;
-          const unsigned cb = best[u] == 0u ? 0xffu : bc[u];
-          cols[u][j >> 2] = (cols[u][j >> 2] & ~(0xffu << (8 * (j & 3)))) | (cb << (8 * (j & 3)));
-          if (best[u] != 0u && (unsigned)(lane * 4) + lq[u] == bc[u]) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (q == (int)lq[u]) o[u][q] = 0u;  // taken
-          }
-        }
-      }
-    }
-    if (lane < U) {  // lane u writes row u's record
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u != lane) continue;
-        const int ml = ml0 + 4 * u, m = m0 + ml;
-        if (ml >= rows || m >= M) continue;
-        float4 *rec = reinterpret_cast<float4 *>(e.cand + ((size_t)m * e.cand_ld + (n0 >> 7)) * 12);
-        float w[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) w[j] = j < E ? vals[u][j < E ? j : 0] : -INFINITY;
-        rec[0] = make_float4(w[0], w[1], w[2], w[3]);
-        rec[1] = make_float4(w[4], w[5], w[6], w[7]);
-        rec[2] = make_float4(__uint_as_float(cols[u][0]), __uint_as_float(cols[u][1]), next[u], 0.f);
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void logits_cand(const EpiArgs &e, uint32_t stg, int M, int N, int m0,
-                                            int n0, int rows, int warp_e, int lane) {
-  if (n0 >= N) return;  // a CTA-pair tile's second half can lie past N
-  switch (e.cand_k) {  // compile-time list length: registers only
-    case 1: logits_cand_t<1>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    case 2: logits_cand_t<2>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    case 3: logits_cand_t<3>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    case 4: logits_cand_t<4>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    case 5: logits_cand_t<5>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    case 6: logits_cand_t<6>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    case 7: logits_cand_t<7>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-    default: logits_cand_t<8>(e, stg, M, N, m0, n0, rows, warp_e, lane); break;
-  }
-}
-
-// Candidate mode: does any row of [m0, m0 + rows) need its full logits?
-// Each of the 128 epilogue threads checks its rows and votes through a
-// per-warp shared-memory flag (every warp rewrites its own flag each time;
-// the caller's barrier orders the writes before the reads).
-__device__ __forceinline__ bool any_forced_rows(const EpiArgs &e, int M, int m0, int rows, int tid,
-                                                volatile uint32_t *flags) {
-  bool f = false;
-  for (int rl = tid; rl < rows && m0 + rl < M; rl += 128) f |= row_forced(e, m0 + rl);
-  const unsigned any = __ballot_sync(0xffffffffu, f);
-  if ((tid & 31) == 0) flags[tid >> 5] = any ? 1u : 0u;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  return (flags[0] | flags[1] | flags[2] | flags[3]) != 0u;
-}
-
 //   warp 0 : TMA producer (one lane)   warp 1 : MMA issuer (one lane)
 //   warps 2..5 : epilogue, TMEM lane quarter = warp % 4
 // grid (weight tiles x activation tiles, CS), cluster (1, CS): the CS CTAs
@@ -1490,21 +1334,13 @@ __global__ void __launch_bounds__(192, 1)
         // before the CTA exits.  (Statistics taken from the accumulator
         // registers instead — warp reductions over the 32 lanes of a group —
         // measured 1.7x slower than this shared-memory pass.)
-        bool store = true;
-        if constexpr (KIND == SKB_EPI_LOGITS)
-          if (ep.cand) store = any_forced_rows(ep, M, m0, Na, row, tmem_slot + 4);
-        if (store) {
-          flush_tile<KIND>(&tmO, stg, n0, m0, warp == 2 && lane == 0, [] {}, lnout,
-                           KIND == SKB_EPI_LOGITS);
-        } else {
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // staged tile complete
-        }
+        flush_tile<KIND>(&tmO, stg, n0, m0, warp == 2 && lane == 0, [] {}, lnout,
+                         KIND == SKB_EPI_LOGITS);
         if constexpr (KIND == SKB_EPI_LOGITS) {
           if (warp == 3 && lane == 0) SW_STAMP(11);
           if (dbg != 3) logits_stats(ep, stg, M, N, m0, n0, Na, warp - 2, lane);
-          if (ep.cand) logits_cand(ep, stg, M, N, m0, n0, Na, warp - 2, lane);
           if (warp == 3 && lane == 0) SW_STAMP(12);
-          if (store && warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
       }
     } else {
@@ -2156,17 +1992,9 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t sb = stg0 + (uint32_t)((chunk & 1) * STG_BYTES);
         sw::stage16<KIND>(sb, bf16, 0, row, bn, v);
         sw::stage16<KIND>(sb, bf16, 16, row, bn, v + 16);
-        bool store = true;
+        sw::flush_tile<KIND>(&tmO, sb, n0, m0 + c, leader, [] {}, false, true);
         if constexpr (KIND == SKB_EPI_LOGITS)
-          if (ep.cand) store = sw::any_forced_rows(ep, M, m0 + c, CHUNK, row, tmem_slot + 1);
-        if (store)
-          sw::flush_tile<KIND>(&tmO, sb, n0, m0 + c, leader, [] {}, false, true);
-        else
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // staged chunk complete
-        if constexpr (KIND == SKB_EPI_LOGITS) {
           sw::logits_stats(ep, sb, M, N, m0 + c, n0, CHUNK, warp - 2, lane);
-          if (ep.cand) sw::logits_cand(ep, sb, M, N, m0 + c, n0, CHUNK, warp - 2, lane);
-        }
       }
       if (local == 0 && leader) PC_STAMP(6);
     }
@@ -2425,12 +2253,6 @@ static EpiArgs to_args(const skb_epilogue *e) {
   a.late_trigger = 0;
   a.a_scale = nullptr;
   a.w_scale = nullptr;
-  a.cand = e->kind == SKB_EPI_LOGITS ? e->cand : nullptr;
-  a.cand_ld = e->cand_ld;
-  a.cand_k = e->cand_k;
-  a.f_step = e->force_step;
-  a.f_plen = e->force_prefix_len;
-  a.f_mlen = e->force_max_len;
   return a;
 }
 
@@ -2446,17 +2268,11 @@ static int check_args(int in_dtype, int M, int N, int K, const void *A, const vo
   if (epi->kind == SKB_EPI_LOGITS && (!epi->lse_part || epi->lse_ld < (N + 31) / 32 ||
                                       epi->out_dtype != SKB_F32))
     return fail(SKB_ERR_CONFIG, "gemm: LOGITS needs fp32 out and a partials buffer");
-  if (epi->kind == SKB_EPI_LOGITS && epi->cand &&
-      (epi->cand_k < 1 || epi->cand_k > 8 || epi->cand_ld < (N + 127) / 128 ||
-       (epi->force_step && (!epi->force_prefix_len || !epi->force_max_len))))
-    return fail(SKB_ERR_CONFIG, "gemm: candidate mode needs 1 <= cand_k <= 8, cand_ld >= N/128 "
-                                "and complete force tables");
   return SKB_OK;
 }
 
 static int gemm_simt(int in_dtype, int M, int N, int K, const void *A, int lda, const void *W,
                      int ldw, const EpiArgs &ep, cudaStream_t st) {
-  if (ep.cand) return fail(SKB_ERR_UNSUPPORTED, "gemm: LOGITS candidate mode needs the bf16 tcgen05 path");
   dim3 grid((N + 63) / 64, (M + 63) / 64);
   if (in_dtype == SKB_F32)
     launch_k(k_gemm_simt<float>, grid, 256, 0, st, M, N, K, (const float *)A, lda, (const float *)W, ldw, ep);
@@ -2666,7 +2482,6 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
     }
     return sw::launch(M, N, K, A, lda, W, ldw, ep, st, na, cs, conc);
   }
-  if (ep.cand) return fail(SKB_ERR_UNSUPPORTED, "gemm: LOGITS candidate mode needs the swap-AB kernel");
   if (epi->ln_in) {
     rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
     if (rc) return rc;

@@ -159,7 +159,6 @@ struct BeamSmem {
   float rm[MAXK][SUB];      // row max / sum of exp partials
   float rs[MAXK][SUB];
   float rgv[MAXK][SUB * MAXK];  // top group maxima
-  float cnx[MAXK][SUB];     // candidate mode: largest unlisted value seen
 };
 
 #ifndef SKB_BEAM_SUB5
@@ -342,46 +341,7 @@ __global__ void __launch_bounds__(MAXK * 32 * SUB)
         if (key > tk[MAXK - 1]) list_insert<MAXK>(tk, tl, tc, key, lp, c);
       }
     };
-    const bool cand_mode = use_part && st.prune && st.cand != nullptr && do_topk && !need_argmax;
-    float cnx = -INFINITY;  // candidate mode: largest unlisted value of the visited tiles
-    if (cand_mode) {
-      // The output GEMM stored per 128-column tile its top cand_k columns
-      // (value desc, column asc) and the largest unlisted value.  Visit the
-      // listed columns of every tile holding a candidate group (same exact
-      // threshold as below); the unlisted values are bounded by `next`,
-      // checked against the row's K-th key once the row list is known.
-      const float thr = T == -INFINITY ? -INFINITY
-                                       : T - (4e-6f * (fabsf(T) + fabsf(mx) + fabsf(lse) + 1.0f) +
-                                              (float)(1e-15 * (fabs(s_r) + 1.0)));
-      const int NT = (U + 127) >> 7;
-      const int E = st.cand_k;
-      const float *crow = st.cand + (size_t)r * st.cand_ld * 12;
-      for (int t0 = s * 32; t0 < NT; t0 += SW) {
-        const int tt = t0 + lane;
-        bool c = false;
-        if (tt < NT) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int g = tt * 4 + q;
-            c |= g < G && part[g].x >= thr;
-          }
-        }
-        unsigned m = __ballot_sync(0xffffffffu, c);
-        while (m) {
-          const int tile = t0 + __ffs(m) - 1;
-          m &= m - 1;
-          const float *rec = crow + (size_t)tile * 12;
-          if (lane < E) {
-            const float x = __ldcs(rec + lane);
-            const unsigned cw = __float_as_uint(__ldcs(rec + 8 + (lane >> 2)));
-            const int off = (int)((cw >> (8 * (lane & 3))) & 0xffu);
-            if (off != 0xff) visit((tile << 7) + off, x);
-          }
-          if (lane == 0) cnx = fmaxf(cnx, __ldcs(rec + 10));
-        }
-      }
-      if (lane == 0) sm.cnx[i][s] = cnx;
-    } else if (use_part && st.prune && (do_topk || need_argmax)) {
+    if (use_part && st.prune && (do_topk || need_argmax)) {
       const float thr_top = do_topk ? (T == -INFINITY ? -INFINITY
                                        : T - (4e-6f * (fabsf(T) + fabsf(mx) + fabsf(lse) + 1.0f) +
                                               (float)(1e-15 * (fabs(s_r) + 1.0))))
@@ -523,22 +483,7 @@ __global__ void __launch_bounds__(MAXK * 32 * SUB)
           }
           ++cnt;
         }
-        if (lane == 0) {
-          sm.cnt[i] = cnt;
-          if (cand_mode) {
-            // an unlisted column could reach this row's top K (a tie with the
-            // K-th key after rounding, or fewer listed than K): the result of
-            // this step is not proven exact — flag the sentence for a rerun
-            // with full logits (engine.BeamBatch)
-            float nx = sm.cnx[i][0];
-#pragma unroll
-            for (int q = 1; q < SUB; ++q) nx = fmaxf(nx, sm.cnx[i][q]);
-            if (nx != -INFINITY) {
-              const double kn = s_r + (double)((nx - mx) - lse);
-              if (cnt < kk || kn >= sm.key[i][kk - 1]) atomicOr(st.inexact + b, 1);
-            }
-          }
-        }
+        if (lane == 0) sm.cnt[i] = cnt;
       }
       TP(9);
       // factor choices of this row (search.py:261-272): prefix override at

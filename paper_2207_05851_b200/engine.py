@@ -66,9 +66,6 @@ class StepBuffers:
         G = (U + 31) // 32
         self.lse_part = torch.zeros(R, 2 * (G + (G & 1)), device=dev)  # rows 16-byte aligned
         self.mask = None          # [B, words] active-column bits (restricted vocab)
-        self.cand = None          # LOGITS candidate records (DecodeWorkspace, bf16)
-        self.cand_k = 0
-        self.force = None         # (step, prefix_len, max_len) device tables
         self.group = 1            # rows per sentence group (beam size)
         self.fac = torch.zeros(R, int(model.fac_off[-1].item()) if nf else 1, device=dev)
         if c.decoder_kind == SSRU:
@@ -160,7 +157,7 @@ def step_forward(model: Model, sb: StepBuffers) -> None:
         resid(sb.f, Ly.w2, Ly.b2, 3 * li + 2, nxt)
     h_ready = fuse and D > 0
     on_h(sb.E_out, sb.logits, N.EPI_LOGITS, None, model.ln_final, h_ready, lse_part=sb.lse_part,
-         mask=sb.mask, rows_per_group=sb.group, cand=sb.cand, cand_k=sb.cand_k, force=sb.force)
+         mask=sb.mask, rows_per_group=sb.group)
     if nf:
         on_h(model.w_fac, sb.fac, N.EPI_STORE, model.b_fac, model.ln_final, h_ready)
 
@@ -244,7 +241,7 @@ class DecodeWorkspace:
     CHUNK = 8
 
     def __init__(self, model: Model, B: int, L: int, S_max: int, K: int, P: int, U: int,
-                 alpha: float, restricted: bool, cand: bool = False):
+                 alpha: float, restricted: bool):
         c = model.config
         dev = model.device
         nf, nsf = len(c.target_factor_specs), len(c.source_factor_specs)
@@ -273,8 +270,7 @@ class DecodeWorkspace:
             off += n
         # ---- decode state: int32 / float64 arenas reset from init images
         st_sizes = dict(n_alive=B, done=B, counter=B, best_steps=B, best_forced=B, best_parent=B,
-                        best_fac=B * nf1, n_done=1, step=1, tok=R, ftok=nf1 * R, parent=R,
-                        inexact=B)
+                        best_fac=B * nf1, n_done=1, step=1, tok=R, ftok=nf1 * R, parent=R)
         self.st = {}
         tot = sum(st_sizes.values())
         self.st_i32 = torch.zeros(tot, dtype=I32, device=dev)
@@ -302,13 +298,6 @@ class DecodeWorkspace:
                               self.row_sent)
         sb = self.sb
         sb.step, sb.tok, sb.parent = self.st["step"], self.st["tok"], self.st["parent"]
-        # LOGITS candidate mode: the output GEMM keeps only each 128-column
-        # tile's top-K records for non-forced rows instead of the fp32 logits
-        self.cand = cand
-        if cand:
-            sb.cand = torch.zeros(R, ((U + 127) // 128) * 12, device=dev)
-            sb.cand_k = K
-            sb.force = (self.st["step"], self.inp["prefix_len"], self.inp["max_len"])
         sb.ftok = self.st["ftok"].view(nf1, R)
         sb.group = K
         sb.mask = self.inp["mask"].view(B, -1) if restricted else None
@@ -330,7 +319,7 @@ class DecodeWorkspace:
         self.fac_choice = z(R * nf1)
         self.tokens_out = z(B * S_max).view(B, S_max)
         self.factors_out = z(B * nf1 * S_max).view(B, nf1, S_max)
-        self.out_host = torch.zeros(B * S_max + B * nf1 * S_max + 3 * B, dtype=I32,
+        self.out_host = torch.zeros(B * S_max + B * nf1 * S_max + 2 * B, dtype=I32,
                                     pin_memory=True)
         self.lp_host = torch.zeros(B, dtype=torch.float64, pin_memory=True)
         self.out_ready = None
@@ -358,9 +347,7 @@ class DecodeWorkspace:
             self.cand_cnt.data_ptr(), self.row_argmax.data_ptr(), self.fac_choice.data_ptr(),
             st["counter"].data_ptr(), st["best_norm"].data_ptr(), st["best_logprob"].data_ptr(),
             st["best_steps"].data_ptr(), st["best_forced"].data_ptr(),
-            st["best_parent"].data_ptr(), st["best_fac"].data_ptr(), st["n_done"].data_ptr(),
-            N.ptr(sb.cand), ((self.U + 127) // 128) if self.cand else 0, sb.cand_k,
-            st["inexact"].data_ptr())
+            st["best_parent"].data_ptr(), st["best_fac"].data_ptr(), st["n_done"].data_ptr())
 
     # ---------------------------------------------------------------- work
     def encode(self):
@@ -450,9 +437,7 @@ class DecodeWorkspace:
         h[B * S:B * S + B * nf1 * S].copy_(self.factors_out.view(-1), non_blocking=True)
         h[B * S + B * nf1 * S:B * S + B * nf1 * S + B].copy_(self.st["best_steps"],
                                                               non_blocking=True)
-        h[B * S + B * nf1 * S + B:B * S + B * nf1 * S + 2 * B].copy_(self.st["best_forced"],
-                                                                     non_blocking=True)
-        h[B * S + B * nf1 * S + 2 * B:].copy_(self.st["inexact"], non_blocking=True)
+        h[B * S + B * nf1 * S + B:].copy_(self.st["best_forced"], non_blocking=True)
         self.lp_host.copy_(self.st["best_logprob"], non_blocking=True)
         self.out_ready = torch.cuda.Event()
         self.out_ready.record()
@@ -470,9 +455,8 @@ class DecodeWorkspace:
         toks = arr[:B * S].reshape(B, S)
         facs = arr[B * S:B * S + B * nf1 * S].reshape(B, nf1, S)
         steps = arr[B * S + B * nf1 * S:B * S + B * nf1 * S + B]
-        forced = arr[B * S + B * nf1 * S + B:B * S + B * nf1 * S + 2 * B]
-        inexact = arr[B * S + B * nf1 * S + 2 * B:]
-        return toks, facs, steps, forced, lp.numpy(), inexact
+        forced = arr[B * S + B * nf1 * S + B:]
+        return toks, facs, steps, forced, lp.numpy()
 
 
 def _round_up(x: int, m: int) -> int:
@@ -522,8 +506,7 @@ class BeamBatch:
     finalize, one D2H copy of the results."""
 
     def __init__(self, model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
-                 nvs_threshold: float | None = None, use_graph: bool = True, slot: int = 0,
-                 cand: bool | None = None):
+                 nvs_threshold: float | None = None, use_graph: bool = True, slot: int = 0):
         if beam < 1:
             raise ConfigError(f"beam size must be at least 1, got {beam}")
         if beam > 32:
@@ -532,15 +515,6 @@ class BeamBatch:
         self.use_graph = use_graph
         self.nvs_threshold = nvs_threshold
         self.slot = slot  # workspace slot: consecutive batches alternate (pipelining)
-        # LOGITS candidate mode (bf16 tensor-core path, beam <= 8): the default
-        # unless SKB_LOGITS_CAND=0; a batch whose step the beam kernel could
-        # not prove exact from the candidate lists reruns those sentences
-        # with full logits (collect)
-        if cand is None:
-            cand = LOGITS_CAND
-        # (the output GEMM must take the swap-AB path: TMA-aligned rows)
-        self.cand = bool(cand and beam <= 8 and model.cdt == torch.bfloat16
-                         and model.config.d_model % 8 == 0)
         c = model.config
         nf, nsf = len(c.target_factor_specs), len(c.source_factor_specs)
         self.nf = nf
@@ -586,9 +560,8 @@ class BeamBatch:
         else:
             U = V
         Lw = self.L_ws
-        self.cand = self.cand and U % 4 == 0
-        key = (B, Lw, K, P, U, self.alpha, restricted, self.slot, kern.concurrency, self.cand)
-        ws = _workspace(model, key, B, Lw, self.S_max, K, P, U, self.alpha, restricted, self.cand)
+        key = (B, Lw, K, P, U, self.alpha, restricted, self.slot, kern.concurrency)
+        ws = _workspace(model, key, B, Lw, self.S_max, K, P, U, self.alpha, restricted)
         self.ws = ws
         # this batch's inputs: own pinned staging + own device copy (several
         # batches of one shape can be staged before any of them runs)
@@ -710,10 +683,9 @@ class BeamBatch:
         return self.finish()
 
     def collect(self) -> list[ChunkResult]:
-        toks, facs, steps, forced, lp, inexact = self.ws.collect()
+        toks, facs, steps, forced, lp = self.ws.collect()
         nf = self.nf
         out = []
-        self.reruns = 0
         for b in range(self.B):
             s = int(steps[b])
             if s <= 0:
@@ -721,17 +693,6 @@ class BeamBatch:
             out.append(ChunkResult(toks[b, :s - 1].tolist(),
                                    [facs[b, k, :s].tolist() for k in range(nf)],
                                    float(lp[b]), s, bool(forced[b])))
-        redo = [b for b in range(self.B) if inexact[b]]
-        if redo:
-            # candidate lists could not prove a step exact (an unlisted column
-            # tied the K-th key): rerun those sentences with full logits — rows
-            # are independent, so they get exactly the numbers they would have
-            # had in this batch
-            again = BeamBatch(self.model, [self.jobs[b] for b in redo], self.K, self.alpha,
-                              self.nvs_threshold, self.use_graph, slot=self.slot, cand=False)
-            for b, r in zip(redo, again.run()):
-                out[b] = r
-            self.reruns = len(redo)
         return out
 
 
@@ -787,7 +748,6 @@ def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_
     return results
 
 
-LOGITS_CAND = os.environ.get("SKB_LOGITS_CAND", "0") == "1"
 DECODE_STREAMS = int(os.environ.get("SKB_STREAMS", "3"))  # concurrent decode batches per device (serving mode; 3 measured best on B200)
 _STREAMS: dict = {}  # device index -> decode streams
 

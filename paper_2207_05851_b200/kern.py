@@ -45,8 +45,7 @@ def dcode(t: torch.Tensor) -> int:
 
 def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_row=None,
          step=None, state_stride=0, lse_part=None, mask=None, rows_per_group=1, simt=False,
-         ln=None, ln_out=None, ln_counter=None, eps=1e-5, ln_in=None, cand=None, cand_k=0,
-         force=None):
+         ln=None, ln_out=None, ln_counter=None, eps=1e-5, ln_in=None):
     """out (or residual x) <- epilogue(A[M,K] . W[N,K]^T).  For RESID, ln =
     (gain, bias) with ln_out (bf16) and ln_counter also writes
     ln_out = LayerNorm(x) of the updated rows (fused on the swap-AB kernel,
@@ -61,10 +60,6 @@ def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_ro
                      lse_part.shape[1] // 2 if lse_part is not None else 0, N.ptr(mask),
                      mask.shape[1] if mask is not None else 0, rows_per_group)
     epi.streams = concurrency
-    if cand is not None:  # LOGITS candidate mode (see skb_epilogue.cand)
-        epi.cand, epi.cand_ld, epi.cand_k = cand.data_ptr(), cand.shape[1] // 12, cand_k
-        if force is not None:
-            epi.force_step, epi.force_prefix_len, epi.force_max_len = (t.data_ptr() for t in force)
     if ln is not None:
         epi.ln_gain, epi.ln_bias = ln[0].data_ptr(), ln[1].data_ptr()
         epi.ln_eps = eps

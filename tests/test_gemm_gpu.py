@@ -3,8 +3,6 @@ of the same op (kernels.py:167-195, 479-484), all epilogues."""
 
 import ctypes as C
 
-import numpy as np
-
 import pytest
 import torch
 
@@ -443,86 +441,3 @@ def test_pair_kernel_bitwise_equal_sw(gemm_path, kind, M, Nn, K):
         got = run(mode)
         for a, b in zip(want, got):
             assert torch.equal(a, b), (mode, (a.float() - b.float()).abs().max().item())
-
-
-@pytest.mark.parametrize("M,Nn,K,masked,E", [(77, 1000, 256, False, 5), (640, 32000, 1024, False, 5),
-                                            (45, 3000, 128, True, 3), (12, 800, 64, False, 1),
-                                            (1280, 32000, 1024, False, 8)])
-def test_logits_candidate_mode(gemm_path, M, Nn, K, masked, E):
-    """SKB_EPI_LOGITS candidate mode: per row and 128-column tile the top-E
-    active columns (value desc, column asc) and the next value, bitwise from
-    the same accumulators as the full logits; partials unchanged; full
-    logits still written for the rows of forced sentences only."""
-    if gemm_path == "tc":
-        pytest.skip("candidate mode runs on the swap-AB / CTA-pair kernels")
-    g = torch.Generator(device="cuda").manual_seed(M + Nn)
-    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
-    W = torch.randn(Nn, K, device="cuda", generator=g).bfloat16()
-    G = (Nn + 31) // 32
-    words = (Nn + 31) // 32
-    rpg = 5
-    nb = (M + rpg - 1) // rpg
-    mask = None
-    if masked:
-        act = torch.rand(nb, Nn, device="cuda", generator=g) < 0.3
-        bits = torch.zeros(nb, words * 32, dtype=torch.int64, device="cuda")
-        bits[:, :Nn] = act.long()
-        wts = (1 << torch.arange(32, device="cuda", dtype=torch.int64))
-        mask = (bits.view(-1, words, 32) * wts).sum(-1)
-        mask = torch.where(mask >= 2 ** 31, mask - 2 ** 32, mask).to(torch.int32).contiguous()
-
-    def run(cand):
-        out = torch.full((M, Nn), float("nan"), device="cuda")
-        part = torch.zeros(M, 2 * G, device="cuda")
-        epi = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None,
-                         0, part.data_ptr(), G, N.ptr(mask), words if masked else 0, rpg)
-        keep = None
-        if cand:
-            NT = (Nn + 127) // 128
-            c = torch.zeros(M, NT * 12, device="cuda")
-            step = torch.tensor([3], dtype=torch.int32, device="cuda")
-            plen = torch.zeros(nb, dtype=torch.int32, device="cuda")
-            mlen = torch.full((nb,), 50, dtype=torch.int32, device="cuda")
-            plen[1] = 5          # sentence 1: prefix-forced at t = 3
-            mlen[nb - 1] = 4     # last sentence: final forced EOS at t = 3
-            epi.cand, epi.cand_ld, epi.cand_k = c.data_ptr(), NT, E
-            epi.force_step, epi.force_prefix_len, epi.force_max_len = (
-                step.data_ptr(), plen.data_ptr(), mlen.data_ptr())
-            keep = (c, step, plen, mlen)
-        _run("skb_gemm", N.BF16, A, W, epi)
-        torch.cuda.synchronize()
-        return out, part, keep
-
-    full, part_f, _ = run(False)
-    out, part_c, (cand, _, _, _) = run(True)
-    assert torch.equal(part_f, part_c)
-    forced_rows = [m for m in range(M) if m // rpg in (1, nb - 1)]
-    assert torch.equal(out[forced_rows], full[forced_rows])
-    # a store unit (tile / 32-row chunk) without a forced row writes no logits
-    stored = ~torch.isnan(out).all(1)
-    assert torch.equal(out[stored], full[stored])
-    if M >= 640:
-        assert (~stored).sum().item() >= M // 4
-    x = full.cpu().numpy()
-    cnp = cand.cpu().numpy().reshape(M, -1, 12)
-    act = None
-    if masked:
-        act = np.repeat(np.unpackbits(mask.cpu().numpy().astype("<u4").view(np.uint8), bitorder="little")
-                        .reshape(nb, -1)[:, :Nn].astype(bool), rpg, 0)[:M]
-    for m in range(0, M, max(1, M // 23)):
-        for t in range(cnp.shape[1]):
-            lo, hi = 128 * t, min(Nn, 128 * t + 128)
-            cols = np.arange(lo, hi)
-            if act is not None:
-                cols = cols[act[m, lo:hi]]
-            vals = x[m, cols]
-            order = np.lexsort((cols, -vals))  # value desc, column asc
-            rec = cnp[m, t]
-            offs = rec[8:10].view(np.uint8)
-            for j in range(E):
-                if j < order.size:
-                    assert rec[j] == vals[order[j]] and offs[j] == cols[order[j]] - lo, (m, t, j)
-                else:
-                    assert rec[j] == -np.inf and offs[j] == 255
-            nxt = vals[order[E]] if order.size > E else -np.inf
-            assert rec[10] == nxt, (m, t)

@@ -105,10 +105,7 @@ def forced_engine_run(model, tr, sents, copies):
             np.testing.assert_array_equal(a, s["active"])  # same restriction as the reference
     jobs = [ChunkJob([int(x) for x in sents[b % n]["src"]], active_ids=actives[b % n])
             for b in range(B)]
-    # full fp32 logits (candidate mode keeps only per-tile records of the
-    # non-forced rows; its decisions are checked against this path in
-    # test_search_gpu.py::test_logits_candidate_mode_equals_full_logits)
-    bb = BeamBatch(model, jobs, K, tr["alpha"], use_graph=False, cand=False)
+    bb = BeamBatch(model, jobs, K, tr["alpha"], use_graph=False)
     ws = bb.ws
     ws.bind_state(bb.eos_col)
     torch.cuda.current_stream().wait_event(bb.in_ready)

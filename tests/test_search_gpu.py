@@ -178,50 +178,3 @@ def test_translate_from_reference_written_model_dir(name):
         assert r.text == g["text"] and r.factors == g["factors"] and r.chunks == g["chunks"]
         if g["error"] is None:
             assert abs(r.score - g["score"]) < 1e-4
-
-
-@pytest.mark.parametrize("beam", [1, 5])
-def test_logits_candidate_mode_equals_full_logits(beam):
-    """bf16 decode with the output GEMM's candidate records (no fp32 logits
-    for non-forced rows) gives bit-identical hypotheses and scores to the
-    full-logits path (tiny model, 16 sentences, beam 1 and 5, prefixes)."""
-    from paper_2207_05851_b200.engine import BeamBatch
-    from paper_2207_05851_b200.search import SentenceInput, _chunk_job
-    case = next(c for c in SEARCH_CASES if c["name"] == "tiny_greedy_16x32")
-    m = product_model("tiny", "bf16")
-    v = product_vocabs("tiny")
-    inputs = [SentenceInput(**i) for i in case["inputs"]]
-    inputs[3] = SentenceInput(tokens=inputs[3].tokens, target_prefix=["w5", "w7", "w9"])
-    jobs = [_chunk_job(m, inp, v, None)[0] for inp in inputs]
-    a = BeamBatch(m, jobs, beam, 1.0, cand=True)
-    got = a.run()
-    want = BeamBatch(m, jobs, beam, 1.0, cand=False).run()
-    assert a.cand and a.reruns == 0
-    for g, w in zip(got, want):
-        assert g.tokens == w.tokens and g.logprob == w.logprob and g.steps == w.steps
-
-
-def test_logits_candidate_mode_reruns_unprovable_steps():
-    """A tile whose unlisted value ties its listed K-th value (36 identical
-    target embedding rows) cannot be proven exact from the candidate
-    records: the sentence is flagged and rerun with full logits, and the
-    results equal the full-logits path."""
-    from paper_2207_05851_b200.engine import BeamBatch
-    from paper_2207_05851_b200.model import Model
-    from paper_2207_05851_b200.search import SentenceInput, _chunk_job
-    from fixture_models import oracle_model, product_config
-    p = dict(oracle_model("tiny").p)
-    E = p["embed.trg.surface"].copy()
-    E[4:40] = E[4] * 3.0    # identical logits in tile 0, large for one sign of h.E[4]
-    E[40:76] = E[4] * -3.0  # ... and for the other
-    p["embed.trg.surface"] = E
-    m = Model(product_config("tiny"), params=p, precision="bf16")
-    v = product_vocabs("tiny")
-    case = next(c for c in SEARCH_CASES if c["name"] == "tiny_greedy_16x32")
-    jobs = [_chunk_job(m, SentenceInput(**i), v, None)[0] for i in case["inputs"][:6]]
-    a = BeamBatch(m, jobs, 5, 1.0, cand=True)
-    got = a.run()
-    want = BeamBatch(m, jobs, 5, 1.0, cand=False).run()
-    assert a.reruns > 0
-    for g, w in zip(got, want):
-        assert g.tokens == w.tokens and g.logprob == w.logprob

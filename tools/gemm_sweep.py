@@ -63,15 +63,7 @@ for name, (Nn, K) in SHAPES.items():
         out = torch.zeros(M, Nn, device=dev)
         part = torch.zeros(M, 2 * ((Nn + 31) // 32), device=dev)
         epi = N.Epilogue(N.EPI_LOGITS, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None,
-                         0, part.data_ptr(), part.shape[1] // 2, None, 0, 5)
-        if os.environ.get("CAND"):  # candidate records instead of fp32 logits
-            cand = torch.zeros(M, ((Nn + 127) // 128) * 12, device=dev)
-            fstep = torch.zeros(1, dtype=torch.int32, device=dev)
-            fpl = torch.zeros(M // 5 + 1, dtype=torch.int32, device=dev)
-            fml = torch.full((M // 5 + 1,), 70, dtype=torch.int32, device=dev)
-            epi.cand, epi.cand_ld, epi.cand_k = cand.data_ptr(), (Nn + 127) // 128, 5
-            epi.force_step, epi.force_prefix_len, epi.force_max_len = (
-                fstep.data_ptr(), fpl.data_ptr(), fml.data_ptr())
+                         0, part.data_ptr(), part.shape[1] // 2, None, 0, 1)
     else:
         out = torch.zeros(M, Nn, device=dev, dtype=torch.bfloat16)
         epi = N.Epilogue(N.EPI_STORE, None, out.data_ptr(), Nn, N.BF16, None, None, None, 0, None,
