@@ -148,8 +148,9 @@ int skb_gemm_force_sw(int mode, int na, int cs);
 
 /* Select the persistent CTA-pair GEMM (tcgen05.mma.cta_group::2, 256 weight
  * rows x na activation rows per tile, two TMEM accumulators): mode 0 =
- * automatic (M >= 1024 and N >= 8192, i.e. the output projection of large
- * batches; shapes without a cluster K-split), 1 = never,
+ * automatic (M >= 1024 and N >= 8192 outside the LOGITS epilogue, i.e. the
+ * cross-attention K/V projection of a batch; shapes without a cluster
+ * K-split), 1 = never,
  * 2 = always where applicable; na in {32..256} step 32, pairs = CTA pairs per
  * launch; 0 = choose automatically.  Bitwise equal to the swap-AB kernel. */
 int skb_gemm_force_pc(int mode, int na, int pairs);

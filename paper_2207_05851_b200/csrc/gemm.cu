@@ -2454,7 +2454,11 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   {
     const int cs_sw = epi->kind == SKB_EPI_LOGITS ? 1 : sw::pick_cs(N, K);
     const bool pc_ok = cs_sw == 1 && logits_tma && sw::g_mode == 0;
-    if (pc_ok && (pc::g_mode == 2 || (pc::g_mode == 0 && M >= pc::g_min_m && N >= 8192))) {
+    // automatic: wide plain GEMMs of large M (the cross-attention K/V
+    // projection of a batch, N = 2 d D); the LOGITS epilogue measured slower
+    // on the pair kernel (126.6 vs 116.1 us at M = 1280, profiles/r2_05_*)
+    const bool pc_auto = M >= pc::g_min_m && N >= 8192 && epi->kind != SKB_EPI_LOGITS;
+    if (pc_ok && (pc::g_mode == 2 || (pc::g_mode == 0 && pc_auto))) {
       if (epi->ln_in) {
         rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
         if (rc) return rc;
