@@ -132,8 +132,10 @@ MODELS = {
                            "lexical shortlist top-200", 200),
     "big_20_2": (BIG_20_2, "transformer-big 20-2, self-attention decoder (d1024 H16 ff4096 V32000)",
                  None),
+    "big_ssru_nosl": (BIG_SSRU, "transformer-big 20-2 hybrid, SSRU decoder (d1024 H16 ff4096 V32000)",
+                      None),
 }
-DEFAULT_BATCH = {"big": 128, "base": 64, "big_ssru": 128, "big_20_2": 128}
+DEFAULT_BATCH = {"big": 128, "base": 64, "big_ssru": 128, "big_20_2": 128, "big_ssru_nosl": 128}
 
 
 def synthetic_shortlist_rows(V: int, k: int = 200, seed: int = 7) -> dict:
@@ -155,7 +157,7 @@ def synthetic_shortlist_rows(V: int, k: int = 200, seed: int = 7) -> dict:
     return rows
 
 
-def build_model(name="big", precision="bf16"):
+def build_model(name="big", precision="bf16", gemm_split="throughput"):
     from paper_2207_05851_b200.checkpoint import SPECIALS, Vocabulary
     from paper_2207_05851_b200.config import ModelConfig, init_params
     from paper_2207_05851_b200.model import Model
@@ -163,7 +165,7 @@ def build_model(name="big", precision="bf16"):
     from paper_2207_05851_b200.shortlist import Shortlist
     spec, _, topk = MODELS[name]
     cfg = ModelConfig(**spec)
-    model = Model(cfg, params=init_params(cfg, 13), precision=precision)
+    model = Model(cfg, params=init_params(cfg, 13), precision=precision, gemm_split=gemm_split)
     words = SPECIALS + [f"w{i}" for i in range(cfg.trg_vocab_size - 4)]
     v = Vocabulary(words)
     vocabs = SimpleNamespace(src_vocab=v, trg_vocab=v, src_factor_vocabs=[], trg_factor_vocabs=[])
@@ -582,6 +584,21 @@ def workload_name(name, K, alpha, B, L):
     return f"{desc} {search}, batch {B} sentences/GPU, src len {L}, {2 * L + 10}-step cap"
 
 
+def latency_model_batch1(name, L=30, which=(("greedy", 1), ("beam5", 5))):
+    """batch1_latency on Model(gemm_split="latency") of config `name`."""
+    import gc
+    import torch
+    from paper_2207_05851_b200 import engine
+    m, v, rs = build_model(name, gemm_split="latency")
+    out = batch1_latency(m, v, L, m.config.trg_vocab_size, restriction=rs, which=which)
+    out["gemm_split"] = "latency"
+    del m, v, rs
+    engine.clear_workspaces()
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
 def secondary_configs(args, peaks):
     """The other BASELINE.json configs, measured in the same run (rank 0,
     N=1): base 6-6 beam 5 batch 64; big 20-2 SSRU + top-200 shortlist greedy
@@ -623,18 +640,14 @@ def secondary_configs(args, peaks):
     m, v, rs = build_model("big_ssru")
     one("big_ssru_sl200_beam5_b128", "big_ssru", 128, 5, args.streams, 6, m, v, rs)
     one("big_ssru_sl200_greedy_b128", "big_ssru", 128, 1, args.streams, 6, m, v, rs)
-    lat = {"big_ssru_sl200": batch1_latency(m, v, L, m.config.trg_vocab_size, restriction=rs),
-           "big_ssru": batch1_latency(m, v, L, m.config.trg_vocab_size, which=(("greedy", 1),))}
     del m, v, rs
     engine.clear_workspaces()
     gc.collect()
     torch.cuda.empty_cache()
-    m, v, rs = build_model("big_20_2")
-    lat["big_20_2"] = batch1_latency(m, v, L, m.config.trg_vocab_size, which=(("greedy", 1),))
-    del m, v, rs
-    engine.clear_workspaces()
-    gc.collect()
-    torch.cuda.empty_cache()
+    # batch-1 latency by architecture, latency-configured models
+    lat = {"big_ssru_sl200": latency_model_batch1("big_ssru", L),
+           "big_ssru": latency_model_batch1("big_ssru_nosl", L, which=(("greedy", 1),)),
+           "big_20_2": latency_model_batch1("big_20_2", L, which=(("greedy", 1),))}
     out["batch1_latency_by_architecture"] = lat
     return out
 
@@ -686,7 +699,13 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    lat = None if args.no_e2e else batch1_latency(model, vocabs, L, V, restriction=restriction)
+    lat = None
+    if not args.no_e2e:
+        # batch-1 latency on the latency-configured model (same weights, every
+        # projection split into short K-partials: Model(gemm_split="latency"));
+        # the serving model's own batch-1 numbers beside it
+        lat = latency_model_batch1(args.config)
+        lat["throughput_model"] = batch1_latency(model, vocabs, L, V, restriction=restriction)
     roof = gemm_roofline(model, B * K, L, peak_tf, U=U)
     roof["peak_source"] = peak_src
     breakdown = step_breakdown(bb)

@@ -109,6 +109,14 @@ typedef struct skb_epilogue {
   /* (0 or 1 = this call has the GPU to itself): tiles are sized for a      */
   /* 1/streams share of the SMs.  Never changes the numbers.                */
   int streams;
+  /* K-split of the bf16 GEMM: 0 = the library's choice from (N, K) alone;  */
+  /* 1, 2, 4, 8 or 16 = exactly that many K-partials, each one K-ordered    */
+  /* tensor-core accumulation over a contiguous K range,                    */
+  /* summed in partial order.  It fixes the fp32 summation order, so the    */
+  /* caller must pass the same value for a weight matrix at every M to keep */
+  /* a row's result independent of its batch (latency models: 8 / 16;      */
+  /* DESIGN.md §4).  Ignored by LOGITS (always 1) and the int8 GEMM.        */
+  int k_split;
 } skb_epilogue;
 
 /* Library identity / diagnostics */
@@ -260,6 +268,10 @@ int skb_self_attention_step(int R, int H, int dh, const void *qkv, int ld_qkv, i
 size_t skb_attn_plan_bytes(int R, int rows_per_group, int S_max);
 int skb_attn_plan(int R, int rows_per_group, int S_max, const int *anc, const int *step,
                   void *plan, void *stream);
+/* Test override (calling host thread only) of the tensor-core attention's  */
+/* heads per CTA: 2, 4 or 8; 0 = automatic (4, or 2 for small grids).      */
+/* Never changes the numbers.                                               */
+int skb_attn_force_heads(int hg);
 /* skb_self_attention_step over a step plan instead of the ancestor table   */
 /* (bitwise equal); bf16, d_h = 64, rows_per_group <= 16, else             */
 /* SKB_ERR_UNSUPPORTED.                                                     */

@@ -35,7 +35,7 @@ class Epilogue(C.Structure):
                 ("splitk_counters_n", i32), ("ln_gain", vp), ("ln_bias", vp),
                 ("ln_eps", C.c_float), ("ln_out", vp), ("ln_ldo", i32), ("ln_counter", vp),
                 ("ln_in", vp), ("ln_in_ld", i32), ("ln_in_gain", vp), ("ln_in_bias", vp),
-                ("ln_in_eps", C.c_float), ("streams", i32)]
+                ("ln_in_eps", C.c_float), ("streams", i32), ("k_split", i32)]
 
 
 class BeamState(C.Structure):
@@ -63,6 +63,7 @@ SIGNATURES = {
     "skb_gemm_simt": [i32, i32, i32, i32, vp, i32, vp, i32, C.POINTER(Epilogue), vp],
     "skb_gemm_force": [i32, i32, i32],
     "skb_gemm_force_sw": [i32, i32, i32],
+    "skb_attn_force_heads": [i32],
     "skb_gemm_force_pc": [i32, i32, i32],
     "skb_quantize_rows": [i32, i32, vp, i32, vp, i32, vp, vp],
     "skb_causal_self_attention": [i32, i32, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp],

@@ -1414,6 +1414,8 @@ extern "C" int skb_causal_self_attention(int B, int T, int H, int dh, const void
                              stream, 1);
 }
 
+static thread_local int g_attn_hg = 0;  // test override of the heads per CTA (0 = automatic)
+
 // Tensor-core self-attention launch (k_self_attn_tc); -1 if the shape or
 // dtypes do not fit it.  plan != nullptr selects the planned variant.
 static int launch_self_tc(int R, int H, int dh, const void *qkv, int ld_qkv, int qkv_dtype, void *kc,
@@ -1428,9 +1430,12 @@ static int launch_self_tc(int R, int H, int dh, const void *qkv, int ld_qkv, int
     if (tc_cap > 64) tc_cap = 64;  // one pass = at most 8 mma n-tiles
     if (tc_cap < 16) tc_cap = 16;
     e = getenv("SKB_ATTN_HG");
-    tc_hg = e ? atoi(e) : 4;
+    tc_hg = e ? atoi(e) : 0;
   }
-  int hg = tc_hg;
+  // heads per CTA (one warp each; a row's numbers do not depend on it):
+  // 4, or 2 when the grid would be small (batch-1 decoding: 8 instead of 4
+  // CTAs for 16 heads, half the entries staged per CTA on the critical path)
+  int hg = g_attn_hg > 0 ? g_attn_hg : tc_hg > 0 ? tc_hg : (((R + G2 - 1) / G2) * (H / 4) < 64 ? 2 : 4);
   while (hg > 1 && H % hg) hg >>= 1;
   if (!(tc_mode && G2 >= 1 && G2 <= 16 && qkv_dtype == SKB_BF16 && ctx_dtype == SKB_BF16 && dh == 64 &&
         ldc % 2 == 0 && ld_qkv % 8 == 0 && (hg == 2 || hg == 4 || hg == 8) &&
@@ -1472,6 +1477,12 @@ static int launch_self_tc(int R, int H, int dh, const void *qkv, int ld_qkv, int
   }
   SKB_CHECK_LAUNCH("k_self_attn_tc");
   return 0;
+}
+
+extern "C" int skb_attn_force_heads(int hg) {
+  if (!(hg == 0 || hg == 2 || hg == 4 || hg == 8)) return fail(SKB_ERR_CONFIG, "attn_force_heads: %d", hg);
+  g_attn_hg = hg;
+  return SKB_OK;
 }
 
 extern "C" int skb_self_attention_step_planned(int R, int H, int dh, const void *qkv, int ld_qkv,

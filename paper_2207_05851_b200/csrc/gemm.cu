@@ -824,6 +824,9 @@ __device__ int g_dbg;
 #endif
 
 constexpr int W_BYTES = 128 * tc::BK * 2;  // 16 KB weight k-block
+constexpr int PUSH_ROWS = 8;               // split-K slices up to this many rows: st.async push
+
+
 constexpr int SMEM_MAX = 232448;          // 227 KB opt-in
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
@@ -844,6 +847,54 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
+}
+
+// the small-slice reduction (st.async from registers) for Na/CS rows per CTA
+__host__ __device__ constexpr bool push_small(int Na, int CS) {
+  return CS > 1 && Na / CS <= PUSH_ROWS && ((Na / CS) & (Na / CS - 1)) == 0;
+}
+
+// Rows c..c+15 of output column `row` (v) belong to owners c/CPR ..; send
+// each owner its CPR rows (one vector st.async, tx bytes on the owner's
+// rbar) or keep them (plain st.shared) — slot [rank][row][0..CPR).
+template <int CPR>
+__device__ __forceinline__ void push_slices(const float *v, int c, int rank, uint32_t rbase,
+                                            uint32_t rbar, int row) {
+#pragma unroll
+  for (int q = 0; q < 16 / CPR; ++q) {
+    const int p = c / CPR + q;
+    const uint32_t a = rbase + (uint32_t)((rank * 128 + row) * CPR) * 4u;
+    const float *w = v + q * CPR;
+#pragma unroll
+    for (int h = 0; h < (CPR + 3) / 4; ++h) {
+      const uint32_t ah = a + 16u * h;
+      if (p == rank) {
+        if (CPR == 1)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(ah), "f"(w[0]) : "memory");
+        else if (CPR == 2)
+          asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(ah), "f"(w[0]), "f"(w[1]) : "memory");
+        else
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(ah), "f"(w[4 * h]), "f"(w[4 * h + 1]),
+                       "f"(w[4 * h + 2]), "f"(w[4 * h + 3])
+                       : "memory");
+      } else {
+        const uint32_t ra = mapa(ah, (uint32_t)p), rm = mapa(rbar, (uint32_t)p);
+        if (CPR == 1)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+                       "r"(__float_as_uint(w[0])), "r"(rm)
+                       : "memory");
+        else if (CPR == 2)
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1,%2}, [%3];" ::"r"(ra),
+                       "r"(__float_as_uint(w[0])), "r"(__float_as_uint(w[1])), "r"(rm)
+                       : "memory");
+        else
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(ra),
+                       "r"(__float_as_uint(w[4 * h])), "r"(__float_as_uint(w[4 * h + 1])),
+                       "r"(__float_as_uint(w[4 * h + 2])), "r"(__float_as_uint(w[4 * h + 3])), "r"(rm)
+                       : "memory");
+      }
+    }
+  }
 }
 
 // Epilogue of one element (m, n).  Lanes of a warp hold consecutive n for
@@ -1004,7 +1055,7 @@ __device__ __forceinline__ void ln_row(const EpiArgs &e, int m, int d, int lane)
 // have placed there.  Same arithmetic as ln_row / k_layernorm_reg (bitwise).
 __device__ __forceinline__ void ln_row_panel(const EpiArgs &e, int m, int rl, int d, int Na,
                                              uint8_t *panel, int lane, const float4 (&g)[8],
-                                             const float4 (&bb)[8]) {
+                                             const float4 (&bb)[8], int kb0, int kb1) {
   const int nv = d >> 7;
   const float4 *xr = reinterpret_cast<const float4 *>(e.lnx + (size_t)m * e.lnx_ld);
   float4 v[8];
@@ -1033,9 +1084,11 @@ __device__ __forceinline__ void ln_row_panel(const EpiArgs &e, int m, int rl, in
       uint2 w;
       w.x = *reinterpret_cast<uint32_t *>(&p0);
       w.y = *reinterpret_cast<uint32_t *>(&p1);
-      const int c = 4 * c4, cc = c & 63;
-      *reinterpret_cast<uint2 *>(panel + (size_t)(c >> 6) * Na * 128 + rl * 128 +
-                                 ((((cc >> 3) ^ (rl & 7))) << 4) + (cc & 7) * 2) = w;
+      // statistics over the whole row; only this CTA's k-blocks are stored
+      const int c = 4 * c4, cc = c & 63, kb = c >> 6;
+      if (kb >= kb0 && kb < kb1)
+        *reinterpret_cast<uint2 *>(panel + (size_t)(kb - kb0) * Na * 128 + rl * 128 +
+                                   ((((cc >> 3) ^ (rl & 7))) << 4) + (cc & 7) * 2) = w;
     }
 }
 
@@ -1130,12 +1183,19 @@ __global__ void __launch_bounds__(192, 1)
   // normalised activation rows sit in a resident panel [nk][Na][64] (SW128)
   // (a separate instantiation: its registers would lower co-residency of
   // the plain kernel)
-  constexpr bool lnx = LNX && CS == 1 && KIND != SKB_EPI_RESID && KIND != SKB_EPI_SSRU;
+  constexpr bool lnx = LNX && KIND != SKB_EPI_RESID && KIND != SKB_EPI_SSRU;
   constexpr bool lnout = LNX && KIND == SKB_EPI_RESID;  // fused LayerNorm of the updated rows
   const int SB = lnx ? W_BYTES : W_BYTES + Na * 128;
   uint8_t *panel = smem + stages * SB;
-  const int panel_bytes = lnx ? ((K + BK - 1) / BK) * Na * 128 : 0;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + stages * SB + panel_bytes);
+  // (with a K split the panel holds this CTA's k-blocks only)
+  const int panel_bytes = lnx ? (((K + BK - 1) / BK + CS - 1) / CS) * Na * 128 : 0;
+  // small-slice K split (<= PUSH_ROWS rows per CTA): peers push their partial
+  // slices straight from registers into this CTA's receive area (st.async),
+  // which therefore lives outside the ring (a peer may finish first)
+  const bool apush = push_small(Na, CS);
+  float *arecv = reinterpret_cast<float *>(smem + stages * SB + panel_bytes);  // [CS][128][cpr]
+  const int arecv_bytes = apush ? Na * 512 : 0;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + stages * SB + panel_bytes + arecv_bytes);
   uint64_t *empty = full + stages;
   uint64_t *tfull = empty + stages;
   uint64_t *rbar = tfull + 1;  // split-K: peers' partial slices landed
@@ -1180,6 +1240,16 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (apush) {
+    // the (CS-1) peer slices this CTA will receive; then announce to the
+    // cluster that this CTA's barriers exist (waited for only right before
+    // the first st.async, long after — off the critical path)
+    if (threadIdx.x == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rbar)),
+                   "r"((uint32_t)((CS - 1) * Na * 512 / CS))
+                   : "memory");
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1232,7 +1302,7 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t *st = smem + s * SB;
         const uint64_t da = umma_desc_sw128(st);
-        const uint64_t db = umma_desc_sw128(lnx ? panel + (size_t)(kb0 + it) * Na * 128 : st + W_BYTES);
+        const uint64_t db = umma_desc_sw128(lnx ? panel + (size_t)it * Na * 128 : st + W_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k) {
           if constexpr (I8)
@@ -1266,14 +1336,14 @@ __global__ void __launch_bounds__(192, 1)
       for (int rl = warp - 2; rl < Na; rl += 4)
         if (m0 + rl >= M)
 #pragma unroll 1
-          for (int c = lane; c < K / 8; c += 32)
-            *reinterpret_cast<uint4 *>(panel + (size_t)(c >> 3) * Na * 128 + rl * 128 + (c & 7) * 16) =
+          for (int c = kb0 * 8 + lane; c < kb1 * 8; c += 32)
+            *reinterpret_cast<uint4 *>(panel + (size_t)((c >> 3) - kb0) * Na * 128 + rl * 128 + (c & 7) * 16) =
                 make_uint4(0u, 0u, 0u, 0u);
       pdl_wait();
       // normalise this tile's activation rows into the panel
 #pragma unroll 1
       for (int rl = warp - 2; rl < Na && m0 + rl < M; rl += 4)
-        ln_row_panel(ep, m0 + rl, rl, K, Na, panel, lane, lg, lb);
+        ln_row_panel(ep, m0 + rl, rl, K, Na, panel, lane, lg, lb, kb0, kb1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(xready);
       if (warp == 2 && lane == 0) SW_STAMP(13);
@@ -1343,6 +1413,56 @@ __global__ void __launch_bounds__(192, 1)
           if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
       }
+    } else if (apush) {
+      // small slices: every CTA owns rows [rank*cpr, (rank+1)*cpr) of the
+      // tile.  Each thread (output column `row`) sends every other owner its
+      // rows of the partial straight from registers with vector st.async into
+      // the owner's receive area arecv[src][row][cpr] (the tx bytes complete
+      // on the owner's rbar; nothing of the sender's shared memory is read,
+      // so the sender may exit at once) and keeps its own rows there too.  No
+      // cluster barrier on the critical path: the only one (barriers
+      // initialised) was entered at kernel start.  The owner sums in rank
+      // order (the fp32 order of the push path below) and stores from
+      // registers.
+      const int cpr = Na / CS;
+      const uint32_t rbase = smem_u32(arecv), rb = smem_u32(rbar);
+      asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // peers' rbar initialised
+#pragma unroll 1
+      for (int c = 0; c < Na; c += 16) {
+        float v[16];
+        tmem_ld16(tb + (uint32_t)c, v);
+        if (cpr == 1)
+          push_slices<1>(v, c, rank, rbase, rb, row);
+        else if (cpr == 2)
+          push_slices<2>(v, c, rank, rbase, rb, row);
+        else if (cpr == 4)
+          push_slices<4>(v, c, rank, rbase, rb, row);
+        else
+          push_slices<8>(v, c, rank, rbase, rb, row);
+      }
+      mbar_wait(rbar, 0);
+      if (warp == 2 && lane == 0) SW_STAMP(9);
+      const float bn = (ep.bias && nok) ? __ldg(ep.bias + n) : 0.f;
+      const int c0 = rank * cpr;
+#pragma unroll 1
+      for (int j = 0; j < cpr; ++j) {
+        const int m = m0 + c0 + j;
+        float acc = 0.f;
+#pragma unroll
+        for (int src = 0; src < CS; ++src) {
+          float x;
+          asm volatile("ld.shared.f32 %0, [%1];"
+                       : "=f"(x)
+                       : "r"(rbase + (uint32_t)((src * 128 + row) * cpr + j) * 4u)
+                       : "memory");
+          acc = src == 0 ? x : acc + x;
+        }
+        if (KIND == SKB_EPI_SSRU)
+          epi_ssru(ep, cprev, cnext, m, n, acc, bn, nok && m < M);
+        else if (nok && m < M)
+          epi_one<KIND>(ep, m, n, acc, bn);
+      }
+      if (warp == 2 && lane == 0) SW_STAMP(4);
     } else {
       // park the fp32 partial in my shared memory: part[m][128] (row-major
       // in m, so the slice each peer finishes is one contiguous block)
@@ -1365,7 +1485,9 @@ __global__ void __launch_bounds__(192, 1)
   }
   __syncwarp();
   if (warp == 2 && lane == 0) SW_STAMP(1);
-  if (CS > 1) {
+  if (CS > 1 && apush && warp < 2)
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // pairs the early arrive
+  if (CS > 1 && !apush) {
     // split-K reduction, push model: every CTA bulk-copies slice p of its
     // partial into CTA p's receive slot [my rank] (async copy engine over
     // the cluster network), then CTA p sums its slice in rank order.
@@ -1498,6 +1620,8 @@ static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMa
                     const CUtensorMap &mo, int Na, int stages, int stg_off, int tma_out,
                     size_t smem, EpiArgs ep, cudaStream_t st) {
   ensure_smem_fn(k_gemm_sw<KIND, CS, LNX, I8>, SMEM_MAX);
+  if (CS > 8)  // 16-CTA clusters are opt-in (non-portable) on B200
+    cudaFuncSetAttribute(k_gemm_sw<KIND, CS, LNX, I8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int n_wt = (N + 127) / 128, n_at = (M + Na - 1) / Na;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_wt * n_at, CS);
@@ -1531,15 +1655,28 @@ static int launch_k2(int M, int N, int K, const CUtensorMap &mw, const CUtensorM
                      const CUtensorMap &mo, int Na, int CS, int stages, int stg_off, int tma_out,
                      size_t smem, EpiArgs ep, cudaStream_t st) {
   if constexpr (KIND == SKB_EPI_STORE || KIND == SKB_EPI_RELU)
-    if (ep.lnx) return launch_t<KIND, 1, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+    if (ep.lnx) {
+      if (CS == 8)
+        return launch_t<KIND, 8, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+      if (CS == 4)
+        return launch_t<KIND, 4, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+      return launch_t<KIND, 1, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+    }
   if constexpr (KIND == SKB_EPI_RESID)
     if (ep.ln_out) {
+      if (CS == 8)
+        return launch_t<KIND, 8, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
       if (CS == 4)
         return launch_t<KIND, 4, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
       if (CS == 2)
         return launch_t<KIND, 2, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
       return launch_t<KIND, 1, true>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
     }
+  if constexpr (KIND != SKB_EPI_LOGITS)
+    if (CS == 16)
+      return launch_t<KIND, 16>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
+  if (CS == 8)
+    return launch_t<KIND, 8>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
   if (CS == 4)
     return launch_t<KIND, 4>(M, N, K, mw, mx, mo, Na, stages, stg_off, tma_out, smem, ep, st);
   if (CS == 2)
@@ -1571,8 +1708,8 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
     cudaMemcpyToSymbol(g_dbg, &d, sizeof(int));
   }
 #endif
-  if (Na < 16 || Na > 256 || Na % 16 || !(CS == 1 || CS == 2 || CS == 4) ||
-      (CS > 1 && Na % (4 * CS)))
+  if (Na < 16 || Na > 256 || Na % 16 || !(CS == 1 || CS == 2 || CS == 4 || CS == 8 || CS == 16) ||
+      (CS > 1 && Na % CS) || (CS == 16 && !push_small(Na, CS)))
     return fail(SKB_ERR_CONFIG, "gemm_sw: bad tile Na=%d CS=%d", Na, CS);
   if (i8 && (CS != 1 || ep.lnx || ep.ln_out || ep.kind == SKB_EPI_SSRU || ep.kind == SKB_EPI_LOGITS))
     return fail(SKB_ERR_CONFIG, "gemm_sw: the int8 path has no K split, LayerNorm, SSRU or LOGITS epilogue");
@@ -1582,13 +1719,15 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   rc = tc::make_map(&mx, X, M, K, ldx, Na, i8);
   if (rc) return rc;
   const bool lnx = ep.lnx != nullptr;
-  if (lnx && (CS != 1 || K % 128 || K > 1024 || ep.kind == SKB_EPI_RESID || ep.kind == SKB_EPI_SSRU))
-    return fail(SKB_ERR_CONFIG, "gemm_sw: prologue LayerNorm needs CS=1, K %% 128 == 0 <= 1024");
+  if (lnx && (K % 128 || K > 1024 || ep.kind == SKB_EPI_RESID || ep.kind == SKB_EPI_SSRU))
+    return fail(SKB_ERR_CONFIG, "gemm_sw: prologue LayerNorm needs K %% 128 == 0 <= 1024");
   const int SB = lnx ? W_BYTES : W_BYTES + Na * 128;
   const int kbe = i8 ? 2 * tc::BK : tc::BK;
   const int nk = (K + kbe - 1) / kbe;
   const int nkc = (nk + CS - 1) / CS;
-  const int panel_bytes = lnx ? nk * Na * 128 : 0;
+  const int panel_bytes = lnx ? nkc * Na * 128 : 0;  // this CTA's k-blocks
+  const int arecv_bytes = push_small(Na, CS) ? Na * 512 : 0;  // st.async receive area
+  const int fixed = panel_bytes + arecv_bytes + 1024 + 512;
   // TMA-store epilogue: the output tile is staged in the (drained) ring
   const bool f32o = ep.kind == SKB_EPI_RESID || ep.out_dtype == SKB_F32;
   const int es = f32o ? 4 : 2;
@@ -1608,13 +1747,13 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
     budget = e ? atoi(e) : 113 * 1024;
     if (budget > SMEM_MAX) budget = SMEM_MAX;
   }
-  int stages = (budget - 1024 - 512 - panel_bytes) / SB;
+  int stages = (budget - fixed) / SB;
   if (stages < 2) stages = 2;
   if (stages > nkc) stages = nkc;
   if (stages * SB < need) stages = (need + SB - 1) / SB;
-  if (stages < 1 || stages * SB + panel_bytes + 1024 + 512 > SMEM_MAX)
+  if (stages < 1 || stages * SB + fixed > SMEM_MAX)
     return fail(SKB_ERR_UNSUPPORTED, "gemm_sw: Na=%d CS=%d does not fit", Na, CS);
-  const size_t smem = (size_t)stages * SB + panel_bytes + 1024 + 512;
+  const size_t smem = (size_t)stages * SB + fixed;
   CUtensorMap mo;
   if (tma_out) {
     rc = make_map_out(&mo, ep.out, M, N, ep.ldo, f32o, rows_box);
@@ -1688,7 +1827,8 @@ static int pick_na(int M, int N, int CS, int conc) {
   double best_c = 1e30;
   for (int na = 16; na <= na_max; na += 16) {
     if (na < na_floor && na + 16 <= na_max && (long)n_wt * ((M + na - 1) / na) > 1) continue;
-    if (CS > 1 && na % (4 * CS)) continue;
+    if (CS > 1 && na % CS) continue;
+    if (CS >= 8 && !push_small(na, CS)) continue;  // wide clusters: power-of-two slices only
     const double ctas = (double)n_wt * ((M + na - 1) / na) * CS;
     const double waves = ctas <= slots ? 1.0 : ctas / slots;
     const double c = waves * (128.0 + na + 160.0);
@@ -2414,6 +2554,9 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
                      int ldw, const skb_epilogue *epi, void *stream, bool &fused_ln) {
   int rc = check_args(in_dtype, M, N, K, A, W, epi);
   if (rc) return rc;
+  if (!(epi->k_split == 0 || epi->k_split == 1 || epi->k_split == 2 || epi->k_split == 4 ||
+        epi->k_split == 8 || epi->k_split == 16))
+    return fail(SKB_ERR_CONFIG, "gemm: k_split %d not in {0, 1, 2, 4, 8, 16}", epi->k_split);
   if (M == 0) return SKB_OK;
   EpiArgs ep = to_args(epi);
   cudaStream_t st = as_stream(stream);
@@ -2451,8 +2594,12 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
   // (and its prologue LayerNorm) has the shorter critical path.
   pc::init_mode();
   const int conc = epi->streams > 0 ? epi->streams : 1;  // decode streams sharing the GPU
+  // K split: the caller's (a function of the weight matrix, see
+  // skb_epilogue.k_split) or the library's (N, K) rule
+  int ksplit = epi->kind == SKB_EPI_LOGITS ? 1 : (epi->k_split > 0 ? epi->k_split : sw::pick_cs(N, K));
+  while (ksplit > 1 && (K + tc::BK - 1) / tc::BK < ksplit) ksplit >>= 1;  // >= 1 k-block per partial
   {
-    const int cs_sw = epi->kind == SKB_EPI_LOGITS ? 1 : sw::pick_cs(N, K);
+    const int cs_sw = ksplit;
     const bool pc_ok = cs_sw == 1 && logits_tma && sw::g_mode == 0;
     // automatic: wide plain GEMMs of large M (the cross-attention K/V
     // projection of a batch, N = 2 d D); the LOGITS epilogue measured slower
@@ -2468,13 +2615,16 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
     }
   }
   if (sw::g_mode != 1 && logits_tma && (sw::g_mode == 2 || sw_pref)) {
-    const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : sw::pick_cs(N, K));
+    const int cs = epi->kind == SKB_EPI_LOGITS ? 1 : (sw::g_cs > 0 ? sw::g_cs : ksplit);
     const int na = sw::g_na > 0 ? sw::g_na : sw::pick_na(M, N, cs, conc);
-    fused_ln = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr;
+    // (instantiated: prologue LayerNorm for cs 1/4/8, fused LayerNorm-out for cs <= 8)
+    fused_ln = epi->kind == SKB_EPI_RESID && epi->ln_out != nullptr && cs <= 8;
+    if (!fused_ln) ep.ln_out = nullptr;
     if (epi->ln_in) {
       // input LayerNorm in the prologue while each CTA's share is small;
       // else one LayerNorm launch writes A first (identical bits)
-      if (cs == 1 && M <= sw::lnx_max_rows() && (long)na * K * 2 <= 64 * 1024 && K % 128 == 0 &&
+      const long panel = (long)na * ((K / tc::BK + cs - 1) / cs) * 128;  // this CTA's k-blocks
+      if ((cs == 1 || cs == 4 || cs == 8) && M <= sw::lnx_max_rows() && panel <= 64 * 1024 && K % 128 == 0 &&
           K <= 1024 && epi->kind != SKB_EPI_RESID &&
           epi->kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(epi->ln_in) & 15) == 0 &&
           epi->ln_in_ld % 4 == 0) {

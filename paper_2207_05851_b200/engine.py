@@ -417,12 +417,18 @@ class DecodeWorkspace:
                 steps += 1
             if poll and steps < S_run:
                 # early exit for finished batches, checked one chunk late so the
-                # host never stalls the GPU pipeline
+                # host never stalls the GPU pipeline; the counter is copied on a
+                # side stream, so the decode stream runs the next graph at once
+                # (a copy on the decode stream would sit between the graphs)
                 if ev is not None and ev.query() and int(done_host[0]) >= self.B:
                     break
-                done_host.copy_(self.st["n_done"], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record()
+                main = torch.cuda.current_stream()
+                side = _poll_stream(main)
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    done_host.copy_(self.st["n_done"], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record()
         return steps
 
     def enqueue_collect(self) -> None:
@@ -457,6 +463,17 @@ class DecodeWorkspace:
         steps = arr[B * S + B * nf1 * S:B * S + B * nf1 * S + B]
         forced = arr[B * S + B * nf1 * S + B:]
         return toks, facs, steps, forced, lp.numpy()
+
+
+_POLL_STREAMS: dict = {}
+
+
+def _poll_stream(main: torch.cuda.Stream) -> torch.cuda.Stream:
+    """Side stream (one per decode stream) for the early-exit counter copies."""
+    key = (main.device, main.cuda_stream)
+    if key not in _POLL_STREAMS:
+        _POLL_STREAMS[key] = torch.cuda.Stream(device=main.device)
+    return _POLL_STREAMS[key]
 
 
 def _round_up(x: int, m: int) -> int:

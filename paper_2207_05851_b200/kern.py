@@ -7,6 +7,7 @@ stream and counts them in `launches` (the bench reports it as gpu_launches).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -43,6 +44,24 @@ def dcode(t: torch.Tensor) -> int:
     raise TypeError(f"unsupported dtype {t.dtype}")
 
 
+LATENCY_KB = int(os.environ.get("SKB_LATENCY_KB", "2"))  # k-blocks (64 K) per partial
+
+
+def latency_k_split(K: int, kb: int = 0) -> int:
+    """K-partials of a latency-model projection: the smallest split in
+    {1, 2, 4, 8} whose partial spans <= kb 64-wide k-blocks (default 2: a
+    128-row weight slice of <= 32 KB per CTA, fetched while the previous
+    kernel runs, and 8 serial MMAs).  A function of K only (K = 1024 -> 8,
+    K = 4096 -> 8 on the big model: 16-CTA clusters measured slower,
+    8.8 vs 6.4 us on the batch-1 critical path)."""
+    kb = kb or LATENCY_KB
+    nk = (K + 63) // 64
+    s = 1
+    while s < 8 and (nk + s - 1) // s > kb:
+        s *= 2
+    return s
+
+
 def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_row=None,
          step=None, state_stride=0, lse_part=None, mask=None, rows_per_group=1, simt=False,
          ln=None, ln_out=None, ln_counter=None, eps=1e-5, ln_in=None):
@@ -60,6 +79,7 @@ def gemm(A, W, out, kind=N.EPI_STORE, bias=None, *, M=None, c_state=None, src_ro
                      lse_part.shape[1] // 2 if lse_part is not None else 0, N.ptr(mask),
                      mask.shape[1] if mask is not None else 0, rows_per_group)
     epi.streams = concurrency
+    epi.k_split = getattr(W, "_skb_k_split", 0)  # the model's K-split policy (Model.gemm_split)
     if ln is not None:
         epi.ln_gain, epi.ln_bias = ln[0].data_ptr(), ln[1].data_ptr()
         epi.ln_eps = eps

@@ -62,10 +62,20 @@ class Model:
     """Encoder/decoder weights on one GPU plus the reference model protocol."""
 
     def __init__(self, config: ModelConfig, params: dict | None = None, seed: int = 13,
-                 precision: str = "bf16", device: str = "cuda"):
+                 precision: str = "bf16", device: str = "cuda", gemm_split: str = "throughput"):
+        """gemm_split (bf16 only) fixes how the tensor-core GEMMs split K, i.e.
+        the fp32 summation order of every projection — a property of the model,
+        the same at every batch size, so a sentence's result never depends on
+        its batch either way.  "throughput": the library's rule (K = 4096 split
+        in 4, else whole-K tiles; best at serving batches of hundreds of rows).
+        "latency": every decoder/encoder projection split into partials of
+        <= 256 K (kern.latency_k_split), so each CTA's weight slice is fetched
+        while the previous kernel still runs (best for batch-1 decoding)."""
         config.validate()
         if precision not in ("bf16", "fp32"):
             raise ConfigError(f"precision must be bf16 or fp32, got {precision!r}")
+        if gemm_split not in ("throughput", "latency"):
+            raise ConfigError(f"gemm_split must be throughput or latency, got {gemm_split!r}")
         if params is None:
             params = init_params(config, seed)
         params = {n: (v.data if hasattr(v, "data") and not isinstance(v, np.ndarray) else v)
@@ -80,8 +90,15 @@ class Model:
             N.call("skb_set_device", self.device.index)
         self.cdt = torch.bfloat16 if precision == "bf16" else torch.float32
         self.quantized: dict = {}
+        self.gemm_split = gemm_split
         self._upload(params)
         self.params = params
+        if gemm_split == "latency" and precision == "bf16":
+            for L in self.enc + self.dec:
+                for name in ("wqkv", "wo", "wq_c", "wo_c", "w1", "w2", "w_ssru"):
+                    w = getattr(L, name, None)
+                    if w is not None:
+                        w._skb_k_split = kern.latency_k_split(w.shape[1])
 
     # ------------------------------------------------------------ weights
     def _f32(self, a):

@@ -131,3 +131,35 @@ def test_cross_attention_matches_reference(G, L):
         sc = torch.einsum("hd,lhd->hl", q[r].float().view(H, dh), K[b, :n]) / math.sqrt(dh)
         ref[r] = torch.einsum("hl,lhd->hd", torch.softmax(sc, -1), V[b, :n])
     assert (ctx.float() - ref.view(R, D)).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("B,G,t", [(1, 5, 35), (1, 1, 69), (7, 5, 20), (128, 5, 40)])
+def test_self_attention_heads_per_cta_bitwise(B, G, t):
+    """Heads per CTA (one warp per head; 2 automatically for batch-1 grids,
+    else 4) only changes which CTA computes a head, never its numbers."""
+    from paper_2207_05851_b200 import _native as N
+    dh, H, S = 64, 16, 80
+    g = torch.Generator(device="cuda").manual_seed(B + t)
+    R, D = B * G, H * dh
+    qkv = torch.randn(R, 3 * D, device="cuda", generator=g).bfloat16()
+    kc0 = torch.randn(R, S, H, dh, device="cuda", generator=g).bfloat16()
+    vc0 = torch.randn(R, S, H, dh, device="cuda", generator=g).bfloat16()
+    anc = torch.zeros(2, R, S, dtype=torch.int32, device="cuda")
+    grp = torch.arange(R, device="cuda") // G
+    anc[t & 1] = (grp[:, None] * G + torch.randint(0, G, (R, S), device="cuda", generator=g)).int()
+    step = torch.tensor([t], dtype=torch.int32, device="cuda")
+    plan = torch.zeros(kern.attn_plan_bytes(R, G, S), dtype=torch.uint8, device="cuda")
+    kern.attn_plan(anc, step, plan, R, S, G)
+    outs = []
+    try:
+        for hg in (0, 2, 4, 8):
+            N.call("skb_attn_force_heads", hg)
+            kc, vc = kc0.clone(), vc0.clone()
+            ctx = torch.zeros(R, D, device="cuda", dtype=torch.bfloat16)
+            kern.self_attention_step(qkv, kc, vc, anc, step, ctx, R, H, dh, S, group=G, plan=plan)
+            torch.cuda.synchronize()
+            outs.append(ctx)
+    finally:
+        N.call("skb_attn_force_heads", 0)
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)

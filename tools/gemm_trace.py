@@ -46,6 +46,7 @@ for name, (Nn, K) in shapes.items():
         gin, bin_ = torch.ones(K, device="cuda"), torch.zeros(K, device="cuda")
         epi.ln_in, epi.ln_in_ld, epi.ln_in_gain, epi.ln_in_bias, epi.ln_in_eps = (
             xin.data_ptr(), K, gin.data_ptr(), bin_.data_ptr(), 1e-5)
+    epi.k_split = int(os.environ.get("KSPLIT", "0"))
     for na, cs in cfgs:
         N.call("skb_gemm_force_sw", 2, na, cs)
         buf = (C.c_ulonglong * (1024 * 16))()

@@ -90,11 +90,13 @@ int main() {
   cudaMalloc(&clk, 4096 * 8);
   cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   const int iters = 2000;
-  for (int per_sm = 1; per_sm <= 2; ++per_sm)
+  for (int active : {nsm, 40, 8})
+  for (int per_sm = 1; per_sm <= 4; ++per_sm)
     for (int stages : {2, 4, 6, 8, 12}) {
-      if (per_sm == 2 && stages > 6) continue;
+      if (stages * per_sm > 13) continue;
+      if (active != nsm && per_sm > 2) continue;
       const int smem = stages * 16384 + 2048;
-      const int grid = nsm * per_sm;
+      const int grid = active * per_sm;
       k_ingest<<<grid, 64, smem>>>(tm, rows, 50, stages, clk);
       cudaEvent_t a, b;
       cudaEventCreate(&a);
@@ -106,9 +108,9 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       const double bytes = (double)grid * iters * 16384;
-      printf("ctas/SM %d stages %2d: %.1f GB/s total, %.1f GB/s per SM, %.1f B/clk/SM @1.965GHz  (%s)\n",
-             per_sm, stages, bytes / ms / 1e6, bytes / ms / 1e6 / nsm, bytes / ms / 1e6 / nsm / 1.965,
-             cudaGetErrorString(cudaGetLastError()));
+      printf("SMs %3d ctas/SM %d stages %2d: %.1f GB/s total, %.1f GB/s per SM, %.1f B/clk/SM @1.965GHz  (%s)\n",
+             active, per_sm, stages, bytes / ms / 1e6, bytes / ms / 1e6 / active,
+             bytes / ms / 1e6 / active / 1.965, cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
 }
