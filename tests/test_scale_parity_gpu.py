@@ -36,7 +36,7 @@ from oracle.fixture_configs import (BASE_RECORDS, SCALE_CONFIGS, SCALE_TRACES,
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp32": 1e-4, "bf16": 2e-2}
+TOL = {"fp32": 1e-4, "bf16": 2e-2, "bf16-lat": 2e-2}
 TRACES = {t["name"]: t for t in SCALE_TRACES}
 
 
@@ -51,7 +51,8 @@ _MODELS = {}
 
 
 def scale_model(cfg_name, precision):
-    """One device model alive at a time (the big configs are 1-1.4 GB each)."""
+    """One device model alive at a time (the big configs are 1-1.4 GB each).
+    precision "bf16-lat": the bf16 model with Model(gemm_split="latency")."""
     import torch
     from paper_2207_05851_b200 import engine
     from paper_2207_05851_b200.config import ModelConfig
@@ -61,8 +62,10 @@ def scale_model(cfg_name, precision):
         _MODELS.clear()
         engine._WS_CACHE.clear()
         torch.cuda.empty_cache()
+        split = "latency" if precision.endswith("-lat") else "throughput"
         _MODELS[key] = Model(ModelConfig(**SCALE_CONFIGS[cfg_name]["config"]),
-                             params=_params(cfg_name), precision=precision)
+                             params=_params(cfg_name), precision=precision.split("-")[0],
+                             gemm_split=split)
     return _MODELS[key]
 
 
@@ -172,7 +175,7 @@ def forced_engine_run(model, tr, sents, copies):
     return worst
 
 
-CASES = [(name, prec, copies) for name in TRACES for prec in ("bf16", "fp32")
+CASES = [(name, prec, copies) for name in TRACES for prec in ("bf16", "fp32", "bf16-lat")
          for copies in (1, 64)
          if not (prec == "fp32" and copies == 64 and TRACES[name]["config"] == "big_ssru")]
 

@@ -139,18 +139,21 @@ def test_concurrent_stream_batches_identical(precision):
     assert [(r.text, r.score) for r in out[1]] == [(r.text, r.score) for r in out[3]]
 
 
-def test_batch_invariance_at_scale():
+@pytest.mark.parametrize("gemm_split", ["throughput", "latency"])
+def test_batch_invariance_at_scale(gemm_split):
     """test_search.py:400-405 at the benchmark model's size (bf16): a batch
     whose encoder sees > 2560 rows (B*L) and whose decoder runs several
     streams of R = 640 rows, against the same sentences one at a time
     (R = beam, prologue-LayerNorm GEMMs).  Every GEMM, the split-K FFN2 and
-    the log-softmax partials must take the same reduction order."""
+    the log-softmax partials must take the same reduction order — for the
+    serving model and for the latency model (every projection K-split, the
+    small-slice st.async reduction at R = 5, the bulk-copy one at R = 640)."""
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
     import bench
     from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
-    model, vocabs, _ = bench.build_model("big")
+    model, vocabs, _ = bench.build_model("big", gemm_split=gemm_split)
     rng = np.random.default_rng(7)
     sents = [[f"w{i}" for i in rng.integers(0, 31996, size=int(n))] for n in rng.integers(1, 121, size=160)]
     st = SearchSettings(beam=5, length_alpha=1.0)
