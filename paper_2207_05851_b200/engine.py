@@ -238,7 +238,7 @@ class DecodeWorkspace:
     by every BeamBatch of the same shape: a new batch costs one pinned H2D
     copy of its inputs, two D2D state resets and graph replays."""
 
-    CHUNK = 8
+    CHUNK = int(os.environ.get("SKB_GRAPH_CHUNK", "8"))  # decode steps per captured graph
 
     def __init__(self, model: Model, B: int, L: int, S_max: int, K: int, P: int, U: int,
                  alpha: float, restricted: bool):
