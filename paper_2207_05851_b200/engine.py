@@ -34,6 +34,7 @@ from . import _native as N
 from .config import SSRU
 from .errors import ConfigError, ShapeError
 from .model import BOS_ID, EOS_ID, PAD_ID, SHIFT_ID, UNK_ID, Model, validate_active_ids
+from .shortlist import sorted_union
 
 I32 = torch.int32
 
@@ -567,7 +568,7 @@ class BeamBatch:
         V = c.trg_vocab_size
         if restricted:
             actives = [a if a is not None else np.arange(V, dtype=np.int64) for a in actives]
-            U_ids = np.unique(np.concatenate(actives)).astype(np.int64)
+            U_ids = sorted_union(*actives)
             U_real = int(U_ids.size)
             # union width bucketed to 1024 columns (a batch-1 shortlist run
             # has a different union per sentence; coarse buckets let calls
@@ -612,22 +613,25 @@ class BeamBatch:
             ct[:U_real] = U_ids.astype(np.int32)
             ct[U_real:] = U_ids[-1]
             mask = h["mask"].numpy().view(np.uint32).reshape(B, -1)
-            mask[:] = 0
+            nbits = mask.shape[1] * 32
             for b, a in enumerate(actives):
-                cols = np.searchsorted(U_ids, a)
-                np.bitwise_or.at(mask[b], cols >> 5, (np.uint32(1) << (cols & 31).astype(np.uint32)))
-            col_of = {int(t): i for i, t in enumerate(U_ids)}
+                # bit c of row b set for every active column c (little-endian
+                # words: column c is bit c & 31 of word c >> 5)
+                bits = np.zeros(nbits, dtype=bool)
+                bits[np.searchsorted(U_ids, a)] = True
+                mask[b] = np.packbits(bits, bitorder="little").view(np.uint32)
+
+            def col_of(tok):
+                i = int(np.searchsorted(U_ids, tok))
+                if i >= U_real or int(U_ids[i]) != tok:
+                    raise ConfigError(f"token id {tok} missing from the restricted vocabulary")
+                return i
         for b, j in enumerate(jobs):
             for t, tok in enumerate(j.prefix_ids):
-                if restricted:
-                    if tok not in col_of:
-                        raise ConfigError(f"token id {tok} missing from the restricted vocabulary")
-                    pcol[b, t] = col_of[tok]
-                else:
-                    pcol[b, t] = tok
+                pcol[b, t] = col_of(tok) if restricted else tok
             for k, stream in enumerate(j.prefix_factor_ids[:nf]):
                 pfac[b, k, :len(stream)] = stream
-        eos_col = col_of[EOS_ID] if restricted else EOS_ID
+        eos_col = col_of(EOS_ID) if restricted else EOS_ID
         self.eos_col = eos_col
         self.h2d_bytes = self.in_host.numel() * 4
         self.in_dev = self.in_host.to(model.device, non_blocking=True)

@@ -28,6 +28,7 @@ from . import kern
 from . import _native as N
 from .config import SSRU, ModelConfig, check_params, init_params
 from .errors import ConfigError, ShapeError
+from .shortlist import sorted_union
 
 PAD_ID, UNK_ID, BOS_ID, EOS_ID, SHIFT_ID = 0, 1, 2, 3, 4
 
@@ -46,7 +47,7 @@ def positional_encoding(length: int, dim: int, offset: int = 0) -> np.ndarray:
 
 def validate_active_ids(config: ModelConfig, active_ids) -> np.ndarray:
     """model.py:333-340."""
-    ids = np.unique(np.asarray(active_ids, dtype=np.int64))
+    ids = sorted_union(active_ids)
     if ids.size == 0:
         raise ConfigError("restricted output vocabulary is empty")
     if ids[0] < 0 or ids[-1] >= config.trg_vocab_size:

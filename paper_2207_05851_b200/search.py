@@ -31,6 +31,7 @@ from . import _native as N
 from .checkpoint import Vocabulary
 from .engine import ChunkJob, ChunkResult, decode_jobs
 from .errors import ConfigError, InputError
+from .shortlist import sorted_union
 from .model import (BOS_ID, EOS_ID, PAD_ID, SHIFT_ID, UNK_ID, Model, validate_active_ids)
 
 logger = logging.getLogger(__name__)
@@ -89,7 +90,7 @@ class ShortlistRestriction:
         self.shortlist = shortlist
 
     def resolve(self, model, state, src_ids, lengths, extra_ids) -> np.ndarray:
-        return np.union1d(self.shortlist.lookup(src_ids), extra_ids)
+        return sorted_union(self.shortlist.lookup(src_ids), extra_ids)
 
 
 class NvsRestriction:

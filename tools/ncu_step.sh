@@ -7,7 +7,7 @@ set -e
 STEP=${STEP:-35}
 OUT=${OUT:-gpurun_out}
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/step_list.csv \
-    python tools/profile_run.py > /dev/null 2>&1
+    python tools/profile_run.py $PR_ARGS > /dev/null 2>&1
 read SKIP COUNT < <(python - "$OUT/step_list.csv" "$STEP" <<'PY'
 import csv, sys
 rows = list(csv.reader(open(sys.argv[1])))
@@ -20,8 +20,8 @@ print(starts[s], starts[s + 1] - starts[s])
 PY
 )
 echo "step $STEP: skip $SKIP count $COUNT"
-ncu --set full --clock-control none -s $SKIP -c $COUNT -o /tmp/step_full \
-    python tools/profile_run.py > $OUT/ncu_step.log 2>&1
+ncu --set full --clock-control none -f -s $SKIP -c $COUNT -o /tmp/step_full \
+    python tools/profile_run.py $PR_ARGS > $OUT/ncu_step.log 2>&1
 ncu -i /tmp/step_full.ncu-rep --page raw --csv --metrics \
 gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_uma.avg.pct_of_peak_sustained_active,lts__t_bytes.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_active,launch__grid_size,launch__registers_per_thread \
     > $OUT/step_full_raw.csv

@@ -18,8 +18,9 @@ ap.add_argument("--batch", type=int, default=128)
 ap.add_argument("--beam", type=int, default=5)
 ap.add_argument("--src-len", type=int, default=30)
 ap.add_argument("--graph", action="store_true")
+ap.add_argument("--gemm-split", default="throughput", choices=["throughput", "latency"])
 a = ap.parse_args()
-model, vocabs, _ = bench.build_model("big")
+model, vocabs, _ = bench.build_model("big", gemm_split=a.gemm_split)
 sents = bench.synth_sentences(a.batch, a.src_len, 32000, seed=13)
 bb = bench.make_batch(model, vocabs, sents, a.beam, 1.0)
 bb.use_graph = a.graph
