@@ -719,10 +719,12 @@ class BeamBatch:
 
 def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
                 nvs_threshold: float | None = None, max_rows: int = 2560,
-                use_graph: bool = True) -> list[ChunkResult]:
+                use_graph: bool = True, on_done=None) -> list[ChunkResult]:
     """Decode chunks in length-sorted device batches of <= max_rows rows.
     Results are independent of batch composition (row-wise kernels with a
-    fixed reduction order), so sorting never changes outputs."""
+    fixed reduction order), so sorting never changes outputs.  on_done(i, r)
+    is called for every chunk as soon as its batch is read back, while the
+    later batches still decode (host post-processing overlaps the GPU)."""
     if not jobs:
         return []
     order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i].src_ids))
@@ -731,11 +733,19 @@ def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
     # stream n % S); on each stream batch n+S is prepared and launched before
     # batch n is read back, so a stream alternates two workspaces.
     with torch.cuda.device(model.device):
-        return _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_graph)
+        return _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_graph,
+                            on_done)
 
 
-def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_graph):
+def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_graph, on_done=None):
     results: list[ChunkResult | None] = [None] * len(jobs)
+
+    def take(idx, bb):
+        for i, r in zip(idx, bb.finish()):
+            results[i] = r
+            if on_done is not None:
+                on_done(i, r)
+
     n_batches = (len(order) + per_batch - 1) // per_batch
     S = max(1, min(DECODE_STREAMS, n_batches))
     kern.set_concurrency(S)
@@ -758,12 +768,9 @@ def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_
             bb.start()
         pending.append((idx, bb))
         if len(pending) > S:
-            pi, pb = pending.pop(0)
-            for i, r in zip(pi, pb.finish()):
-                results[i] = r
+            take(*pending.pop(0))
     for pi, pb in pending:
-        for i, r in zip(pi, pb.finish()):
-            results[i] = r
+        take(pi, pb)
     for st in streams[1:]:
         main.wait_stream(st)
     return results

@@ -210,19 +210,22 @@ def _check_prefix_budget(prefix_ids, max_len) -> None:
 
 
 def _chunk_job(model, chunk: SentenceInput, vocabs, restriction) -> tuple[ChunkJob, float | None]:
-    """Host half of _start_state (search.py:235-242): ids, prefix, active ids."""
-    src_ids, src_f, lengths = encode_chunk(chunk, vocabs)
+    """Host half of _start_state (search.py:235-242): ids, prefix, active ids
+    (encode_chunk's ids as plain lists: no numpy round trip per sentence)."""
+    ids = vocabs.src_vocab.encode(chunk.source_prefix + chunk.tokens)
+    plen = len(chunk.source_prefix)
+    fids = [[PAD_ID] * plen + v.encode(s) for s, v in zip(chunk.source_factors, vocabs.src_factor_vocabs)]
     pre, pre_f = encode_target_prefix(chunk, vocabs)
-    _check_prefix_budget(pre, _max_output_len(int(lengths[0])))
-    job = ChunkJob([int(x) for x in src_ids[0]], [[int(x) for x in f[0]] for f in src_f],
-                   pre, pre_f)
+    _check_prefix_budget(pre, _max_output_len(len(ids)))
+    job = ChunkJob(ids, fids, pre, pre_f)
     nvs = None
     if isinstance(restriction, NvsRestriction):
         nvs = restriction.threshold
     elif restriction is not None:
         extra = np.array([PAD_ID, UNK_ID, EOS_ID] + list(pre), dtype=np.int64)
-        ids = restriction.resolve(model, None, src_ids[0], lengths, extra)
-        job.active_ids = validate_active_ids(model.config, ids)
+        ids_a = np.asarray(ids, dtype=np.int64)
+        a = restriction.resolve(model, None, ids_a, np.array([ids_a.size], dtype=np.int64), extra)
+        job.active_ids = validate_active_ids(model.config, a)
     return job, nvs
 
 
@@ -296,11 +299,17 @@ def translate(model, vocabs, inputs, settings: SearchSettings | None = None,
         except InputError as e:
             logger.warning("input skipped: %s", e)
             plans.append(str(e))
+    texts: dict = {}  # chunk index -> (surface tokens, factor tokens), built while the GPU decodes
+
+    def detok(i, r):
+        texts[i] = (vocabs.trg_vocab.decode(r.tokens),
+                    [vocabs.trg_factor_vocabs[q].decode(r.factors[q][1:]) for q in range(nf)])
+
     if jobs:
         K = _decide(settings)
         if isinstance(model, Model):
             results = [_hyp(r) for r in decode_jobs(model, jobs, K, settings.length_alpha,
-                                                    nvs_thr, max_rows)]
+                                                    nvs_thr, max_rows, on_done=detok)]
         else:
             results = [ProtocolSearch.from_job(model, j, K, settings.restriction,
                                                settings.length_alpha).run() for j in jobs]
@@ -315,8 +324,11 @@ def translate(model, vocabs, inputs, settings: SearchSettings | None = None,
         lp, steps, forced = 0.0, 0, False
         for k, ch in enumerate(chunks):
             h = results[first + k]
-            toks = vocabs.trg_vocab.decode(h.tokens)
-            aligned = [vocabs.trg_factor_vocabs[q].decode(h.factors[q][1:]) for q in range(nf)]
+            if first + k in texts:
+                toks, aligned = texts[first + k]
+            else:
+                toks = vocabs.trg_vocab.decode(h.tokens)
+                aligned = [vocabs.trg_factor_vocabs[q].decode(h.factors[q][1:]) for q in range(nf)]
             if inp.strip_prefix and ch.target_prefix:
                 drop = min(len(ch.target_prefix), len(toks))
                 toks = toks[drop:]

@@ -30,3 +30,4 @@ for s in sents[2:]:
 pr.disable()
 print(f"{name} beam {beam}: {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms per call")
 pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+pstats.Stats(pr).sort_stats("cumtime").print_stats(25)

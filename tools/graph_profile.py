@@ -18,10 +18,10 @@ import bench  # noqa: E402
 import os
 B = int(os.environ.get("BATCH", "128"))
 K = int(os.environ.get("BEAM", "5"))
-model, vocabs, _ = bench.build_model(os.environ.get("CONFIG", "big"),
+model, vocabs, rs = bench.build_model(os.environ.get("CONFIG", "big"),
                                      gemm_split=os.environ.get("GEMM_SPLIT", "throughput"))
 sents = bench.synth_sentences(B, 30, 32000, seed=13)
-bb = bench.make_batch(model, vocabs, sents, K, 1.0)
+bb = bench.make_batch(model, vocabs, sents, K, 1.0, restriction=rs)
 for _ in range(2):
     bb.run()
 torch.cuda.synchronize()
