@@ -164,3 +164,20 @@ def test_reads_model_dirs_written_by_the_reference(name):
         assert Vocabulary.load(d / f"vocab.src.factor{i}.json").tokens == v.tokens
     for i, v in enumerate(ov["trg_f"]):
         assert Vocabulary.load(d / f"vocab.trg.factor{i}.json").tokens == v.tokens
+
+
+def test_sorted_union_equals_numpy_unique():
+    """The shortlist / restriction union (bitmap) is np.unique of the
+    concatenation: sorted, unique, int64, for any mix of inputs."""
+    import numpy as np
+    from paper_2207_05851_b200.shortlist import sorted_union
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        parts = [rng.integers(0, int(rng.integers(1, 40000)), size=int(rng.integers(0, 300)))
+                 for _ in range(int(rng.integers(1, 6)))]
+        want = np.unique(np.concatenate(parts)).astype(np.int64)
+        got = sorted_union(*parts)
+        assert got.dtype == np.int64 and np.array_equal(got, want)
+    assert sorted_union(np.array([-3, 2, 2])).tolist() == [-3, 2]  # fallback path
+    assert sorted_union(np.zeros(0, dtype=np.int64)).size == 0
+    assert sorted_union([7, 1], np.array([1, 4])).tolist() == [1, 4, 7]
