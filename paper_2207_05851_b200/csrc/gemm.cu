@@ -1237,6 +1237,7 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncwarp();  // reconverge the warp (lane-divergent roles) before bar.sync
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
@@ -1248,7 +1249,8 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(rbar)),
                    "r"((uint32_t)((CS - 1) * Na * 512 / CS))
                    : "memory");
-    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   }
 
   if (warp == 0) {
@@ -1426,7 +1428,8 @@ __global__ void __launch_bounds__(192, 1)
       // registers.
       const int cpr = Na / CS;
       const uint32_t rbase = smem_u32(arecv), rb = smem_u32(rbar);
-      asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // peers' rbar initialised
+      __syncwarp();
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' rbar initialised
 #pragma unroll 1
       for (int c = 0; c < Na; c += 16) {
         float v[16];
@@ -1486,7 +1489,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncwarp();
   if (warp == 2 && lane == 0) SW_STAMP(1);
   if (CS > 1 && apush && warp < 2)
-    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // pairs the early arrive
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // pairs the early arrive
   if (CS > 1 && !apush) {
     // split-K reduction, push model: every CTA bulk-copies slice p of its
     // partial into CTA p's receive slot [my rank] (async copy engine over
@@ -1567,6 +1570,7 @@ __global__ void __launch_bounds__(192, 1)
     if (ln_last)
       for (int rl = warp - 2; rl < Na && m0 + rl < M; rl += 4) ln_row(ep, m0 + rl, N, lane);
   }
+  __syncwarp();  // reconverge the warp (lane-divergent roles) before bar.sync
   __syncthreads();
 #ifdef SKB_GEMM_TRACE
   if (threadIdx.x == 0) {
