@@ -397,6 +397,7 @@ class DecodeWorkspace:
         else:
             self.graph_enc.replay()
             kern.launches += self.launches_enc
+            _mark("encoder graph launched")
         steps = 0
         if self.graph_1 is None:
             self.one_step()                    # step 0 eagerly, then capture
@@ -409,6 +410,8 @@ class DecodeWorkspace:
         ev = None
         while steps < S_run:
             if self.graph_n is not None and S_run - steps >= self.CHUNK:
+                if steps == 0:
+                    _mark("first decode graph: launch")
                 self.graph_n.replay()
                 kern.launches += self.launches_chunk
                 steps += self.CHUNK
@@ -477,6 +480,16 @@ def _poll_stream(main: torch.cuda.Stream) -> torch.cuda.Stream:
     return _POLL_STREAMS[key]
 
 
+HOST_TRACE = os.environ.get("SKB_HOST_TRACE", "0") == "1"
+HOST_MARKS: list = []  # (label, perf_counter) when SKB_HOST_TRACE=1 (tools/host_timeline.py)
+
+
+def _mark(label: str) -> None:
+    if HOST_TRACE:
+        import time
+        HOST_MARKS.append((label, time.perf_counter()))
+
+
 def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -525,6 +538,7 @@ class BeamBatch:
 
     def __init__(self, model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
                  nvs_threshold: float | None = None, use_graph: bool = True, slot: int = 0):
+        _mark("BeamBatch")
         if beam < 1:
             raise ConfigError(f"beam size must be at least 1, got {beam}")
         if beam > 32:
@@ -634,6 +648,7 @@ class BeamBatch:
         eos_col = col_of(EOS_ID) if restricted else EOS_ID
         self.eos_col = eos_col
         self.h2d_bytes = self.in_host.numel() * 4
+        _mark("inputs packed")
         self.in_dev = self.in_host.to(model.device, non_blocking=True)
         # start() may run on another stream: it waits for this copy
         self.in_ready = torch.cuda.Event()
@@ -685,6 +700,7 @@ class BeamBatch:
                                   if nsf else None, len_d, self.B, self.L)
             self._prepare(nvs_active_sets(m, enc, len_d, self.B, self.L, self.nvs_threshold,
                                           self.jobs))
+        _mark("start")
         ws = self.ws
         if ws.state is None or ws.eos_col != self.eos_col:
             ws.bind_state(self.eos_col)
@@ -692,8 +708,11 @@ class BeamBatch:
         torch.cuda.current_stream().wait_event(self.in_ready)
         ws.in_dev.copy_(self.in_dev, non_blocking=True)   # device-resident inputs
         ws.reset()
+        _mark("inputs copied, state reset")
         self.steps_run = ws.run(self.S_run, self.use_graph)
+        _mark("decode graphs launched")
         ws.enqueue_collect()
+        _mark("collect enqueued")
 
     def finish(self) -> list[ChunkResult]:
         """Wait for this batch's results (launched by start())."""

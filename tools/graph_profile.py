@@ -53,3 +53,14 @@ print(f"{'kernel':60s} {'n':>6s} {'crit ms':>8s} {'crit us':>8s} {'incl us':>8s}
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
     print(f"{k:60s} {cnt[k]:6d} {v / 1e3:8.3f} {v / cnt[k]:8.2f} {incl[k] / cnt[k]:8.2f} "
           f"{100 * v / wall:5.1f}%")
+if os.environ.get("GAPS"):
+    # idle gaps on the device timeline (next kernel start - max end so far) > 2 us
+    prev_end = evs[0][1]
+    gaps = []
+    for s0, e0, name in evs[1:]:
+        if s0 - prev_end > 2.0:
+            gaps.append((round(s0 - prev_end, 1), name))
+        prev_end = max(prev_end, e0)
+    print(f"idle gaps > 2 us: {len(gaps)}, total {sum(g for g, _ in gaps) / 1e3:.3f} ms")
+    for g, n in gaps[:40]:
+        print(f"   {g:8.1f} us before {n}")
