@@ -283,7 +283,7 @@ def gemm_roofline(model, R, L, peak, U=None):
     out_flops = 2 * R * U * d
     achieved = flops / (ms / 1e3) / 1e12
     return_kernel = ("tcgen05 GEMMs: k_gemm_sw (swap-AB, 128 weight rows x Na activation rows per "
-                     "CTA; FFN2 split over a 4-CTA cluster), all GEMMs of one decode step, R=%d" % R)
+                     "CTA; FFN2 split over a 2-CTA cluster), all GEMMs of one decode step, R=%d" % R)
     return {"kernel": return_kernel,
             "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": _gemm_traffic(),

@@ -1792,11 +1792,20 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
 
 // Cluster split CS from (N, K) only (numerics must not depend on M).
 // Measured on B200 at M = 640 (tools/gemm_sweep.py): the bulk-copy
-// reduction costs ~3-4 us, so only long-K shapes (FFN2, K = 4096) gain.
+// reduction costs ~3-4 us, so only long-K shapes (FFN2, K = 4096) split.
 static int pick_cs(int N, int K) {
   const int nk = (K + tc::BK - 1) / tc::BK;
   const int n_wt = (N + 127) / 128;
-  if (nk >= 48 && n_wt <= 16) return 4;
+  // Long-K shapes (FFN2, K = 4096) split in 2: measured on B200 (bench, 3
+  // decode streams, profiles/r2_55_exp.txt, r2_56_exp.txt): split 4 -> 5070,
+  // 2 -> 5400, 1 -> 5476 sentences/s, single stream 3131 / 3121 / 2914.
+  // SKB_CS_LONGK overrides.
+  static int long_k = -1;
+  if (long_k < 0) {
+    const char *e = getenv("SKB_CS_LONGK");
+    long_k = e ? atoi(e) : 2;
+  }
+  if (nk >= 48 && n_wt <= 16) return long_k;
   // SKB_CS_SMALLN=2|4 also splits the narrow K = 1024 shapes (wo, wo_c):
   // still a function of (N, K) only, a latency / throughput trade-off —
   // measured on B200: 4 gives batch-1 greedy 21.4 ms (from 23.5) but costs

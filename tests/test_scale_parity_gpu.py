@@ -17,7 +17,7 @@ and 1e-4 in fp32.
 Two batch shapes per trace: the traced sentences alone (R = K per
 sentence: the small-M path, LayerNorm in the GEMM prologue) and replicated
 to the bench batch of 128 sentences (R = 640: the bench's own GEMM tiles,
-4-CTA split-K clusters, the separate LayerNorm launch).
+cluster split-K FFN2, the separate LayerNorm launch).
 
 Whole-sequence fp32 parity: the product's own beam_search / greedy_search
 (fp32 mode) must reproduce the reference's final hypotheses (north star:
