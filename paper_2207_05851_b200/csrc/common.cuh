@@ -99,11 +99,24 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-// Logistic split on sign so exp never overflows (kernels.py:253-260).
+// Logistic split on sign so exp never overflows (kernels.py:253-260):
+// 1 / (1 + exp(-x)) for x >= 0, exp(x) / (1 + exp(x)) otherwise, written
+// branch-free (exp(-|x|) is the exponential of either side, the sign picks
+// the numerator) with the SFU exponential and division (relative error
+// ~1e-6, far inside the 1e-4 fp32 parity bound; every kernel that needs a
+// sigmoid calls this one, so all paths agree bit for bit).  The accurate
+// expf + IEEE division cost ~6 us of a 7 us SSRU epilogue at M = 640
+// (profiles/r2_67/68_trace_ssru.txt).
 __device__ __forceinline__ float sigmoid_ref(float x) {
-  if (x >= 0.f) return 1.0f / (1.0f + expf(-x));
-  float e = expf(x);
-  return e / (1.0f + e);
+  const float e = __expf(-fabsf(x));
+  return __fdividef(x >= 0.f ? 1.0f : e, 1.0f + e);
+}
+
+// SSRU cell (model.py:268-272): c = f * c_prev + (1 - f) * W h with
+// f = sigmoid(W_f h + b_f); one definition for every epilogue path.
+__device__ __forceinline__ float ssru_cell(float v, float bn, float w, float cp) {
+  const float f = sigmoid_ref(v + bn);
+  return f * cp + (1.0f - f) * w;
 }
 
 }  // namespace skb

@@ -442,8 +442,7 @@ __global__ void k_ssru_scan(int B, int T, int d, const float *__restrict__ g, in
   float c = 0.f;
   for (int t = 0; t < T; ++t) {
     const size_t r = (size_t)b * T + t;
-    const float f = sigmoid_ref(g[r * ldg + 2 * j] + bf);
-    c = f * c + (1.0f - f) * g[r * ldg + 2 * j + 1];
+    c = ssru_cell(g[r * ldg + 2 * j], bf, g[r * ldg + 2 * j + 1], c);
     float *xp = x + r * ldx + j;
     *xp = *xp + fmaxf(c, 0.f);
   }

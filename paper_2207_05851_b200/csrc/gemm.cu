@@ -102,10 +102,8 @@ __device__ __forceinline__ void epilogue_run(const EpiArgs &e, int m, int n, int
       const int nn = n + q;
       if (nn >= N) break;
       const int j = nn >> 1;
-      float fpre = v[q] + (e.bias ? e.bias[nn] : 0.f);
-      float f = sigmoid_ref(fpre);
       float cp = cprev ? cprev[(size_t)srow * e.ld_state + j] : 0.f;
-      float c = f * cp + (1.0f - f) * v[q + 1];
+      float c = ssru_cell(v[q], e.bias ? e.bias[nn] : 0.f, v[q + 1], cp);
       cnext[(size_t)m * e.ld_state + j] = c;
       float *xp = x + (size_t)m * e.ldo + j;
       *xp = *xp + fmaxf(c, 0.f);
@@ -918,33 +916,86 @@ __device__ __forceinline__ void epi_one(const EpiArgs &e, int m, int n, float v,
     reinterpret_cast<__nv_bfloat16 *>(e.out)[o] = __float2bfloat16_rn(t);
 }
 
-// SSRU cell (model.py:268-272) on the lane pair (2j, 2j+1) = (W_f h, W h);
-// called by all 32 lanes (the partner value comes by shuffle).
+// SSRU cell on the lane pair (2j, 2j+1) = (W_f h, W h); called by all 32
+// lanes (the partner value comes by shuffle).
 __device__ __forceinline__ void epi_ssru(const EpiArgs &e, const float *cprev, float *cnext,
                                          int m, int n, float v, float bn, bool ok) {
   const float w = __shfl_xor_sync(0xffffffffu, v, 1);
   if (!ok || (n & 1)) return;
   const int j = n >> 1;
   const int srow = e.src_row ? e.src_row[m] : m;
-  const float f = sigmoid_ref(v + bn);
   const float cp = cprev ? cprev[(size_t)srow * e.ld_state + j] : 0.f;
-  const float c = f * cp + (1.0f - f) * w;
+  const float c = ssru_cell(v, bn, w, cp);
   cnext[(size_t)m * e.ld_state + j] = c;
   float *xp = reinterpret_cast<float *>(e.out) + (size_t)m * e.ldo + j;
   *xp = *xp + fmaxf(c, 0.f);
 }
 
-// 16 consecutive activation rows m0..m0+15 of output column n.
-template <int KIND>
-__device__ __forceinline__ void epi16(const EpiArgs &e, const float *cprev, float *cnext, int M,
-                                      int m0, int n, bool nok, float bn, const float *v) {
+// 16 consecutive activation rows m0..m0+15 of output column n.  SSRU: all
+// loads of the 16 rows (parent-row indices, then the parents' cells and the
+// residual rows) are issued before any store — one row at a time, every
+// row's loads waited behind the previous row's stores (they may alias as far
+// as the compiler knows), which made the SSRU GEMM ~10x its mainloop at
+// M = 640 (profiles/r2_60_graph_ssru128.txt).
+// SSRU epilogue in two halves so loads can run ahead of the stores (and of
+// the accumulator): the parents' cells and the residual rows of rows
+// m0..m0+15 (they never alias this call's stores: c_next is the other half
+// of the step double buffer, x rows are the call's own)...
+__device__ __forceinline__ void ssru_load16(const EpiArgs &e, const float *cprev, int M, int m0, int n,
+                                            bool nok, float (&cp)[16], float (&xo)[16]) {
+  const int j = n >> 1;
+  const bool even = (n & 1) == 0;
+  const float *x = reinterpret_cast<const float *>(e.out);
+  int srow[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int m = m0 + i;
-    if (KIND == SKB_EPI_SSRU)
-      epi_ssru(e, cprev, cnext, m, n, v[i], bn, nok && m < M);
-    else if (nok && m < M)
-      epi_one<KIND>(e, m, n, v[i], bn);
+    srow[i] = (nok && even && m < M && e.src_row) ? __ldg(e.src_row + m) : m;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int m = m0 + i;
+    const bool ok = nok && even && m < M;
+    cp[i] = (ok && cprev) ? __ldcg(cprev + (size_t)srow[i] * e.ld_state + j) : 0.f;
+    xo[i] = ok ? __ldcg(x + (size_t)m * e.ldo + j) : 0.f;
+  }
+}
+
+// ...then the cells and the residual update (all 32 lanes: the W h partner
+// value comes by shuffle).
+__device__ __forceinline__ void ssru_store16(const EpiArgs &e, float *cnext, int M, int m0, int n, bool nok,
+                                             float bn, const float *v, const float (&cp)[16],
+                                             const float (&xo)[16]) {
+  const int j = n >> 1;
+  const bool even = (n & 1) == 0;
+  float *x = reinterpret_cast<float *>(e.out);
+  float w[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[i] = __shfl_xor_sync(0xffffffffu, v[i], 1);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int m = m0 + i;
+    if (nok && even && m < M) {
+      const float c = ssru_cell(v[i], bn, w[i], cp[i]);
+      cnext[(size_t)m * e.ld_state + j] = c;
+      x[(size_t)m * e.ldo + j] = xo[i] + fmaxf(c, 0.f);
+    }
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void epi16(const EpiArgs &e, const float *cprev, float *cnext, int M,
+                                      int m0, int n, bool nok, float bn, const float *v) {
+  if constexpr (KIND == SKB_EPI_SSRU) {
+    float cp[16], xo[16];
+    ssru_load16(e, cprev, M, m0, n, nok, cp, xo);
+    ssru_store16(e, cnext, M, m0, n, nok, bn, v, cp, xo);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int m = m0 + i;
+      if (nok && m < M) epi_one<KIND>(e, m, n, v[i], bn);
+    }
   }
 }
 
@@ -1361,6 +1412,10 @@ __global__ void __launch_bounds__(192, 1)
         cprev = t == 0 ? nullptr : ep.c_next + ((t + 1) & 1) * ep.state_stride;
       }
     }
+    // SSRU, whole-K tiles: the first 16 rows' parent cells and residual rows
+    // are read while the MMAs run (software-pipelined below)
+    float scp[16], sxo[16];
+    if constexpr (KIND == SKB_EPI_SSRU && CS == 1) ssru_load16(ep, cprev, M, m0, n, nok, scp, sxo);
     mbar_wait(tfull, 0);
     if (ep.late_trigger == 1 && warp == 2 && lane == 0) pdl_trigger();  // (2: only at exit)
     if (warp == 2 && lane == 0) SW_STAMP(5);
@@ -1384,6 +1439,35 @@ __global__ void __launch_bounds__(192, 1)
         else
           for (int i = 0; i < 16; ++i) v[i] = (float)i;
         if (dbg == 1) continue;
+        if constexpr (KIND == SKB_EPI_SSRU) {
+          // next chunk's loads before this chunk's stores
+          const bool more = c + 16 < Na && m0 + c + 16 < M;
+          float ncp[16], nxo[16];
+          if (more) {
+            if (dbg == 7) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) ncp[i] = nxo[i] = 0.f;
+            } else {
+              ssru_load16(ep, cprev, M, m0 + c + 16, n, nok, ncp, nxo);
+            }
+          }
+          if (dbg == 6) {  // trace experiments: cells computed, nothing stored
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc += ssru_cell(v[i], bn, __shfl_xor_sync(0xffffffffu, v[i], 1), scp[i]) + sxo[i];
+            if (acc == 12345.f) cnext[0] = acc;
+          } else {
+            ssru_store16(ep, cnext, M, m0 + c, n, nok, bn, v, scp, sxo);
+          }
+          if (more) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              scp[i] = ncp[i];
+              sxo[i] = nxo[i];
+            }
+          }
+          continue;
+        }
         if constexpr (I8) {
           // quant.py:124-128: (float32(acc) * a_scale) * w_scale, each
           // product rounded on its own (no FMA), the bias added after

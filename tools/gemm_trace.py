@@ -14,7 +14,7 @@ from paper_2207_05851_b200 import _native as N  # noqa: E402
 import os
 M = int(os.environ.get("M", "640"))
 shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024),
-          "out_proj": (32000, 1024)}
+          "out_proj": (32000, 1024), "ssru": (2048, 1024)}
 import os
 if os.environ.get("SHAPES"):
     shapes = {k: shapes[k] for k in os.environ["SHAPES"].split(",")}
@@ -32,6 +32,13 @@ for name, (Nn, K) in shapes.items():
         epi = N.Epilogue(N.EPI_RESID, None, out.data_ptr(), Nn, N.F32, None, None, None, 0, None,
                          0, None, 0, None, 0, 1, None, 0, None, 0, gain.data_ptr(), lb.data_ptr(),
                          1e-5, hln.data_ptr(), Nn, ctr.data_ptr())
+    elif os.environ.get("SSRU"):  # SSRU cell epilogue, decode-loop double buffer at step 5
+        out = torch.zeros(M, Nn // 2, device="cuda")
+        cell = torch.zeros(2, M, Nn // 2, device="cuda")
+        rows = torch.arange(M, dtype=torch.int32, device="cuda")
+        stp = torch.tensor([5], dtype=torch.int32, device="cuda")
+        epi = N.Epilogue(N.EPI_SSRU, None, out.data_ptr(), Nn // 2, N.F32, None, cell.data_ptr(),
+                         rows.data_ptr(), Nn // 2, stp.data_ptr(), M * (Nn // 2))
     elif os.environ.get("LOGITS"):
         out = torch.zeros(M, Nn, device="cuda")
         part = torch.zeros(M, 2 * ((Nn + 31) // 32), device="cuda")
