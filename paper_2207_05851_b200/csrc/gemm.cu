@@ -1150,7 +1150,8 @@ __device__ __forceinline__ void ln_row_panel(const EpiArgs &e, int m, int rl, in
 // one whole 512-byte tile row per instruction (conflict-free); the group
 // reductions are fixed shuffle trees (deterministic, M-independent).
 __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int M, int N, int m0,
-                                             int n0, int rows, int warp_e, int lane) {
+                                             int n0, int rows, int warp_e, int lane,
+                                             uint32_t smask = 0) {
   constexpr int U = 4;  // independent tile rows per iteration (shuffle-latency ILP)
   const int g = lane >> 3, sub = lane & 7;  // group within the tile row, lane within group
   const int n = n0 + g * 32;
@@ -1172,7 +1173,15 @@ __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int
                      : "=f"(f[u].x), "=f"(f[u].y), "=f"(f[u].z), "=f"(f[u].w)
                      : "r"(stg + (uint32_t)(ml * 128 + lane * 4) * 4u));
         unsigned bits = tail;
-        if (e.mask && tail) bits &= e.mask[(size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5)];
+        if (e.mask && tail) {
+          if (smask) {  // staged ahead of the accumulator (logits_mask_stage)
+            unsigned w;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(smask + (uint32_t)(ml * 4 + g) * 4u));
+            bits &= w;
+          } else {
+            bits &= e.mask[(size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5)];
+          }
+        }
         b4[u] = (bits >> (sub * 4)) & 0xfu;
       }
     }
@@ -1217,6 +1226,22 @@ __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int
   }
 }
 
+// Restricted vocabulary: the tile's column-mask words [rows][4 groups] into
+// shared memory while the MMAs run (they were written before the decode
+// loop), so the statistics pass reads them from shared memory instead of
+// one dependent L2 load per row batch.
+__device__ __forceinline__ void logits_mask_stage(const EpiArgs &e, uint32_t smask, int M, int N, int m0,
+                                                  int n0, int rows, int tid) {
+#pragma unroll 1
+  for (int i = tid; i < rows * 4; i += 128) {
+    const int ml = i >> 2, g = i & 3, m = m0 + ml, n = n0 + 32 * g;
+    const unsigned w = (m < M && n < N)
+                           ? __ldg(e.mask + (size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5))
+                           : 0u;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smask + (uint32_t)i * 4u), "r"(w) : "memory");
+  }
+}
+
 //   warp 0 : TMA producer (one lane)   warp 1 : MMA issuer (one lane)
 //   warps 2..5 : epilogue, TMEM lane quarter = warp % 4
 // grid (weight tiles x activation tiles, CS), cluster (1, CS): the CS CTAs
@@ -1246,7 +1271,11 @@ __global__ void __launch_bounds__(192, 1)
   const bool apush = push_small(Na, CS);
   float *arecv = reinterpret_cast<float *>(smem + stages * SB + panel_bytes);  // [CS][128][cpr]
   const int arecv_bytes = apush ? Na * 512 : 0;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + stages * SB + panel_bytes + arecv_bytes);
+  // LOGITS over a restricted vocabulary: the tile's mask words [Na][4]
+  const int smask_bytes = (KIND == SKB_EPI_LOGITS && ep.mask) ? Na * 16 : 0;
+  const uint32_t smask = smask_bytes ? smem_u32(smem + stages * SB + panel_bytes + arecv_bytes) : 0u;
+  uint64_t *full =
+      reinterpret_cast<uint64_t *>(smem + stages * SB + panel_bytes + arecv_bytes + smask_bytes);
   uint64_t *empty = full + stages;
   uint64_t *tfull = empty + stages;
   uint64_t *rbar = tfull + 1;  // split-K: peers' partial slices landed
@@ -1416,6 +1445,8 @@ __global__ void __launch_bounds__(192, 1)
     // are read while the MMAs run (software-pipelined below)
     float scp[16], sxo[16];
     if constexpr (KIND == SKB_EPI_SSRU && CS == 1) ssru_load16(ep, cprev, M, m0, n, nok, scp, sxo);
+    if constexpr (KIND == SKB_EPI_LOGITS)
+      if (smask) logits_mask_stage(ep, smask, M, N, m0, n0, Na, threadIdx.x - 64);
     mbar_wait(tfull, 0);
     if (ep.late_trigger == 1 && warp == 2 && lane == 0) pdl_trigger();  // (2: only at exit)
     if (warp == 2 && lane == 0) SW_STAMP(5);
@@ -1494,7 +1525,7 @@ __global__ void __launch_bounds__(192, 1)
                          KIND == SKB_EPI_LOGITS);
         if constexpr (KIND == SKB_EPI_LOGITS) {
           if (warp == 3 && lane == 0) SW_STAMP(11);
-          if (dbg != 3) logits_stats(ep, stg, M, N, m0, n0, Na, warp - 2, lane);
+          if (dbg != 3) logits_stats(ep, stg, M, N, m0, n0, Na, warp - 2, lane, smask);
           if (warp == 3 && lane == 0) SW_STAMP(12);
           if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
@@ -1815,7 +1846,8 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   const int nkc = (nk + CS - 1) / CS;
   const int panel_bytes = lnx ? nkc * Na * 128 : 0;  // this CTA's k-blocks
   const int arecv_bytes = push_small(Na, CS) ? Na * 512 : 0;  // st.async receive area
-  const int fixed = panel_bytes + arecv_bytes + 1024 + 512;
+  const int smask_bytes = (ep.kind == SKB_EPI_LOGITS && ep.mask) ? Na * 16 : 0;  // staged mask words
+  const int fixed = panel_bytes + arecv_bytes + smask_bytes + 1024 + 512;
   // TMA-store epilogue: the output tile is staged in the (drained) ring
   const bool f32o = ep.kind == SKB_EPI_RESID || ep.out_dtype == SKB_F32;
   const int es = f32o ? 4 : 2;
