@@ -64,7 +64,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON rules)")
-    ap.add_argument("--streams", type=int, default=int(os.environ.get("SKB_STREAMS", "3")),
+    ap.add_argument("--gemm-split", default="throughput", choices=["throughput", "latency"],
+                    help="GEMM K-split policy of the measured model (Model(gemm_split=...))")
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("SKB_STREAMS", "5")),
                     help="independent batches decoded concurrently on separate CUDA streams")
     return ap.parse_args()
 
@@ -636,10 +638,11 @@ def secondary_configs(args, peaks):
             gc.collect()
             torch.cuda.empty_cache()
 
-    one("base_beam5_b64", "base", 64, 5, args.streams, 6)
+    nb = max(6, 2 * args.streams)  # batches per secondary config: the stream pipeline fills
+    one("base_beam5_b64", "base", 64, 5, args.streams, nb)
     m, v, rs = build_model("big_ssru")
-    one("big_ssru_sl200_beam5_b128", "big_ssru", 128, 5, args.streams, 6, m, v, rs)
-    one("big_ssru_sl200_greedy_b128", "big_ssru", 128, 1, args.streams, 6, m, v, rs)
+    one("big_ssru_sl200_beam5_b128", "big_ssru", 128, 5, args.streams, nb, m, v, rs)
+    one("big_ssru_sl200_greedy_b128", "big_ssru", 128, 1, args.streams, nb, m, v, rs)
     del m, v, rs
     engine.clear_workspaces()
     gc.collect()
@@ -670,7 +673,7 @@ def run_ours(args):
     hbm = peaks.get("hbm_gbs", 6466.1)
 
     name = args.config
-    model, vocabs, restriction = build_model(name)
+    model, vocabs, restriction = build_model(name, gemm_split=args.gemm_split)
     V = model.config.trg_vocab_size
     B = args.batch or DEFAULT_BATCH[name]
     K, L = args.beam, args.src_len

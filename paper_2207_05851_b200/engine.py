@@ -495,9 +495,10 @@ def _round_up(x: int, m: int) -> int:
 
 
 # Workspaces per model (dropped with the model), least recently used first,
-# bounded by device bytes (SKB_WS_BYTES, default 24 GB of the 180 GB).
+# bounded by device bytes (SKB_WS_BYTES, default 64 GB of the 180 GB: 5 decode
+# streams x 2 slots of the big model plus the latency workspaces stay cached).
 _WS_CACHE: "weakref.WeakKeyDictionary[Model, OrderedDict]" = weakref.WeakKeyDictionary()
-_WS_BYTES = int(float(os.environ.get("SKB_WS_BYTES", 24e9)))
+_WS_BYTES = int(float(os.environ.get("SKB_WS_BYTES", 64e9)))
 
 
 def _ws_bytes(ws) -> int:
@@ -795,7 +796,7 @@ def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_
     return results
 
 
-DECODE_STREAMS = int(os.environ.get("SKB_STREAMS", "3"))  # concurrent decode batches per device (serving mode; 3 measured best on B200)
+DECODE_STREAMS = int(os.environ.get("SKB_STREAMS", "5"))  # concurrent decode batches per device (serving mode; 5 measured best on B200, profiles/r2_75-77)
 _STREAMS: dict = {}  # device index -> decode streams
 
 
