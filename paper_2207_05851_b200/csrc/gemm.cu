@@ -1145,84 +1145,74 @@ __device__ __forceinline__ void ln_row_panel(const EpiArgs &e, int m, int rl, in
 
 // LOGITS epilogue (model.py:577-581, kernels.py:287-295): partial
 // log-softmax statistics (max, sum exp(x - max)) of every 32-column group of
-// the staged fp32 logit tile, over the row's active columns.  Eight lanes
-// share a group (4 values each, one 16-byte shared load), so a warp reads
-// one whole 512-byte tile row per instruction (conflict-free); the group
-// reductions are fixed shuffle trees (deterministic, M-independent).
+// the staged fp32 logit tile, over the row's active columns.  Two lanes share
+// a group (16 values each: four 16-byte shared loads, their order rotated by
+// lane so a warp's 32 loads hit distinct bank quads), a warp covers 4 rows x
+// 4 groups per step, and each reduction is ONE xor-shuffle with the partner
+// half — the earlier 8-lanes-per-group layout spent 6 dependent shuffle
+// levels per row (5.7 us of a 67 us output projection at M = 640,
+// profiles/r2_91_stats.txt).  Fixed per-lane order: deterministic and
+// independent of M.
 __device__ __forceinline__ void logits_stats(const EpiArgs &e, uint32_t stg, int M, int N, int m0,
                                              int n0, int rows, int warp_e, int lane,
                                              uint32_t smask = 0) {
-  constexpr int U = 4;  // independent tile rows per iteration (shuffle-latency ILP)
-  const int g = lane >> 3, sub = lane & 7;  // group within the tile row, lane within group
+  constexpr float L2E = 1.4426950408889634f;
+  const int rr = lane >> 3, g = (lane >> 1) & 3, h = lane & 1;  // row in the step, group, half
   const int n = n0 + g * 32;
   unsigned tail = 0xffffffffu;
   if (n >= N) tail = 0u;
   else if (N - n < 32) tail = (1u << (N - n)) - 1u;
 #pragma unroll 1
-  for (int ml0 = warp_e; ml0 < rows && m0 + ml0 < M; ml0 += 4 * U) {
-    float4 f[U];
-    unsigned b4[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ml = ml0 + 4 * u;
-      const int m = m0 + ml;
-      b4[u] = 0u;
-      f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ml < rows && m < M) {
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(f[u].x), "=f"(f[u].y), "=f"(f[u].z), "=f"(f[u].w)
-                     : "r"(stg + (uint32_t)(ml * 128 + lane * 4) * 4u));
-        unsigned bits = tail;
-        if (e.mask && tail) {
-          if (smask) {  // staged ahead of the accumulator (logits_mask_stage)
-            unsigned w;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(smask + (uint32_t)(ml * 4 + g) * 4u));
-            bits &= w;
-          } else {
-            bits &= e.mask[(size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5)];
-          }
+  for (int mb = 4 * warp_e; mb < rows && m0 + mb < M; mb += 16) {
+    const int ml = mb + rr, m = m0 + ml;
+    const bool ok = ml < rows && m < M;
+    float v[16];
+    unsigned bits = 0u;
+    if (ok) {
+      unsigned w = tail;
+      if (e.mask && tail) {
+        if (smask) {  // staged ahead of the accumulator (logits_mask_stage)
+          unsigned mw;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mw) : "r"(smask + (uint32_t)(ml * 4 + g) * 4u));
+          w &= mw;
+        } else {
+          w &= e.mask[(size_t)(m / e.rows_per_group) * e.mask_words + (n >> 5)];
         }
-        b4[u] = (bits >> (sub * 4)) & 0xfu;
       }
-    }
-    // branch-free: masked columns become -inf; ex2.approx (SFU) on x - max,
-    // whose log-sum-exp differs from expf's by < 1e-6 relative
-    float mx[U], sm[U], x[U][4];
+      bits = (w >> (16 * h)) & 0xffffu;
+      const uint32_t base = stg + (uint32_t)(ml * 128 + g * 32 + h * 16) * 4u;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      x[u][0] = (b4[u] & 1u) ? f[u].x : -INFINITY;
-      x[u][1] = (b4[u] & 2u) ? f[u].y : -INFINITY;
-      x[u][2] = (b4[u] & 4u) ? f[u].z : -INFINITY;
-      x[u][3] = (b4[u] & 8u) ? f[u].w : -INFINITY;
-      mx[u] = fmaxf(fmaxf(x[u][0], x[u][1]), fmaxf(x[u][2], x[u][3]));
-    }
+      for (int k = 0; k < 4; ++k) {
+        const int kk = (k + lane) & 3;  // chunk kk of the half in slot k
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v[4 * k]), "=f"(v[4 * k + 1]), "=f"(v[4 * k + 2]), "=f"(v[4 * k + 3])
+                     : "r"(base + (uint32_t)kk * 16u));
+        const unsigned b = (bits >> (4 * kk)) & 0xfu;
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1)
-#pragma unroll
-      for (int u = 0; u < U; ++u) mx[u] = fmaxf(mx[u], __shfl_xor_sync(0xffffffffu, mx[u], o));
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float ml2 = mx[u] == -INFINITY ? 0.f : mx[u] * 1.4426950408889634f;
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float e2;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(fmaf(x[u][q], 1.4426950408889634f, -ml2)));
-        acc += e2;  // ex2(-inf) = +0 for masked columns
+        for (int q = 0; q < 4; ++q)
+          if (!((b >> q) & 1u)) v[4 * k + q] = -INFINITY;  // masked / past N
       }
-      sm[u] = acc;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = -INFINITY;
     }
+    float mx = v[0];
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1)
+    for (int q = 1; q < 16; ++q) mx = fmaxf(mx, v[q]);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    // ex2.approx (SFU) on x - max, whose log-sum-exp differs from expf's by
+    // < 1e-6 relative; ex2(-inf) = +0 for masked columns
+    const float ml2 = mx == -INFINITY ? 0.f : mx * L2E;
+    float acc = 0.f;
 #pragma unroll
-      for (int u = 0; u < U; ++u) sm[u] += __shfl_xor_sync(0xffffffffu, sm[u], o);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ml = ml0 + 4 * u, m = m0 + ml;
-      if (sub == 0 && n < N && ml < rows && m < M)
-        reinterpret_cast<float2 *>(e.lse_part)[(size_t)m * e.lse_ld + (n >> 5)] =
-            make_float2(mx[u], sm[u]);
+    for (int q = 0; q < 16; ++q) {
+      float e2;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(fmaf(v[q], L2E, -ml2)));
+      acc += e2;
     }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (h == 0 && ok && n < N)
+      reinterpret_cast<float2 *>(e.lse_part)[(size_t)m * e.lse_ld + (n >> 5)] = make_float2(mx, acc);
   }
 }
 
