@@ -942,7 +942,7 @@ __device__ __forceinline__ void epi_ssru(const EpiArgs &e, const float *cprev, f
 // m0..m0+15 (they never alias this call's stores: c_next is the other half
 // of the step double buffer, x rows are the call's own)...
 __device__ __forceinline__ void ssru_load16(const EpiArgs &e, const float *cprev, int M, int m0, int n,
-                                            bool nok, float (&cp)[16], float (&xo)[16]) {
+                                            bool nok, float (&cp)[16], float (&xo)[16], bool want_x = true) {
   const int j = n >> 1;
   const bool even = (n & 1) == 0;
   const float *x = reinterpret_cast<const float *>(e.out);
@@ -957,7 +957,7 @@ __device__ __forceinline__ void ssru_load16(const EpiArgs &e, const float *cprev
     const int m = m0 + i;
     const bool ok = nok && even && m < M;
     cp[i] = (ok && cprev) ? __ldcg(cprev + (size_t)srow[i] * e.ld_state + j) : 0.f;
-    xo[i] = ok ? __ldcg(x + (size_t)m * e.ldo + j) : 0.f;
+    xo[i] = (ok && want_x) ? __ldcg(x + (size_t)m * e.ldo + j) : 0.f;
   }
 }
 
@@ -980,6 +980,25 @@ __device__ __forceinline__ void ssru_store16(const EpiArgs &e, float *cnext, int
       cnext[(size_t)m * e.ld_state + j] = c;
       x[(size_t)m * e.ldo + j] = xo[i] + fmaxf(c, 0.f);
     }
+  }
+}
+
+// Staged variant (TMA-store epilogue): the cells and relu(cells) of rows
+// mloc..mloc+15 into two [Na][64] fp32 shared tiles (local column row / 2);
+// one TMA store writes c_next and one TMA reduce-add applies x += relu(c).
+__device__ __forceinline__ void ssru_stage16(uint32_t stgc, uint32_t stgx, int mloc, int row, bool nok,
+                                             int n, float bn, const float *v, const float (&cp)[16]) {
+  float w[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[i] = __shfl_xor_sync(0xffffffffu, v[i], 1);
+  if (!nok || (n & 1)) return;
+  const uint32_t col = (uint32_t)(row >> 1) * 4u;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float c = ssru_cell(v[i], bn, w[i], cp[i]);
+    const uint32_t o = (uint32_t)(mloc + i) * 256u + col;
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(stgc + o), "f"(c) : "memory");
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(stgx + o), "f"(fmaxf(c, 0.f)) : "memory");
   }
 }
 
@@ -1239,8 +1258,8 @@ __device__ __forceinline__ void logits_mask_stage(const EpiArgs &e, uint32_t sma
 template <int KIND, int CS, bool LNX = false, bool I8 = false>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_sw(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-              const __grid_constant__ CUtensorMap tmO, int M, int N, int K, int Na, int stages,
-              int stg_off, int tma_out, EpiArgs ep) {
+              const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M,
+              int N, int K, int Na, int stages, int stg_off, int tma_out, EpiArgs ep) {
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -1434,7 +1453,7 @@ __global__ void __launch_bounds__(192, 1)
     // SSRU, whole-K tiles: the first 16 rows' parent cells and residual rows
     // are read while the MMAs run (software-pipelined below)
     float scp[16], sxo[16];
-    if constexpr (KIND == SKB_EPI_SSRU && CS == 1) ssru_load16(ep, cprev, M, m0, n, nok, scp, sxo);
+    if constexpr (KIND == SKB_EPI_SSRU && CS == 1) ssru_load16(ep, cprev, M, m0, n, nok, scp, sxo, tma_out != 2);
     if constexpr (KIND == SKB_EPI_LOGITS)
       if (smask) logits_mask_stage(ep, smask, M, N, m0, n0, Na, threadIdx.x - 64);
     mbar_wait(tfull, 0);
@@ -1469,7 +1488,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) ncp[i] = nxo[i] = 0.f;
             } else {
-              ssru_load16(ep, cprev, M, m0 + c + 16, n, nok, ncp, nxo);
+              ssru_load16(ep, cprev, M, m0 + c + 16, n, nok, ncp, nxo, tma_out != 2);
             }
           }
           if (dbg == 6) {  // trace experiments: cells computed, nothing stored
@@ -1477,6 +1496,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc += ssru_cell(v[i], bn, __shfl_xor_sync(0xffffffffu, v[i], 1), scp[i]) + sxo[i];
             if (acc == 12345.f) cnext[0] = acc;
+          } else if (tma_out == 2) {  // staged: TMA store / reduce-add after the last chunk
+            const uint32_t stgc = smem_u32(smem) + (uint32_t)stg_off;
+            ssru_stage16(stgc, stgc + (uint32_t)Na * 256u, c, row, nok, n, bn, v, scp);
           } else {
             ssru_store16(ep, cnext, M, m0 + c, n, nok, bn, v, scp, sxo);
           }
@@ -1503,6 +1525,29 @@ __global__ void __launch_bounds__(192, 1)
           stage16<KIND>(stg, bf16, c, row, bn, v);
         else
           epi16<KIND>(ep, cprev, cnext, M, m0 + c, n, nok, bn, v);
+      }
+      if constexpr (KIND == SKB_EPI_SSRU) {
+        if (tma_out == 2 && dbg != 1) {
+          // c_next [halves][M][d] (3D map: the step's half) and x += relu(c)
+          const uint32_t stgc = smem_u32(smem) + (uint32_t)stg_off;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (warp == 2 && lane == 0) {
+            const int half = ep.step ? (*ep.step & 1) : 0;
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmO2)),
+                "r"(n0 >> 1), "r"(m0), "r"(half), "r"(stgc)
+                : "memory");
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmO)),
+                "r"(n0 >> 1), "r"(m0), "r"(0), "r"(stgc + (uint32_t)Na * 256u)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+        }
       }
       if (KIND != SKB_EPI_SSRU && tma_out && dbg != 1) {
         // LOGITS: the store engine and the group statistics both only read
@@ -1693,6 +1738,31 @@ __global__ void __launch_bounds__(192, 1)
 
 // Output tensor map for the TMA-store epilogue: [rows M][cols N] of fp32 or
 // bf16 at pitch ld, box = 128 columns x box_rows rows, no swizzle.
+// Output tensor maps of a swap-AB launch: a = the output (or x), b = the
+// SSRU cell buffer (unused by the other epilogues).
+struct OutMaps {
+  CUtensorMap a, b;
+};
+
+// fp32 [halves][rows][cols] (row pitch ld, half pitch half_stride elements),
+// box 64 columns x box_rows rows x 1: the SSRU epilogue's TMA store of the
+// cells into the step's half of the double buffer and its TMA reduce-add of
+// relu(c) into x (halves = 1), rows past `rows` clipped within each half.
+static int make_map_ssru(CUtensorMap *out, const void *ptr, int rows, int cols, int ld, int halves,
+                         long long half_stride, int box_rows) {
+  tc::EncodeTiledFn fn = tc::encode_fn();
+  if (!fn) return fail(SKB_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)halves};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)(halves > 1 ? half_stride : (long long)ld * rows) * 4};
+  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SKB_ERR_LAUNCH, "cuTensorMapEncodeTiled(ssru) failed (%d)", (int)r);
+  return SKB_OK;
+}
+
 static int make_map_out(CUtensorMap *out, const void *ptr, int rows, int cols, int ld, bool f32,
                         int box_rows) {
   static std::mutex mu;
@@ -1726,7 +1796,7 @@ static int make_map_out(CUtensorMap *out, const void *ptr, int rows, int cols, i
 
 template <int KIND, int CS, bool LNX = false, bool I8 = false>
 static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
-                    const CUtensorMap &mo, int Na, int stages, int stg_off, int tma_out,
+                    const OutMaps &mo, int Na, int stages, int stg_off, int tma_out,
                     size_t smem, EpiArgs ep, cudaStream_t st) {
   ensure_smem_fn(k_gemm_sw<KIND, CS, LNX, I8>, SMEM_MAX);
   if (CS > 8)  // 16-CTA clusters are opt-in (non-portable) on B200
@@ -1753,15 +1823,15 @@ static int launch_t(int M, int N, int K, const CUtensorMap &mw, const CUtensorMa
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS, LNX, I8>, mw, mx, mo, M, N, K, Na, stages, stg_off,
-                     tma_out, ep);
+  cudaLaunchKernelEx(&cfg, k_gemm_sw<KIND, CS, LNX, I8>, mw, mx, mo.a, mo.b, M, N, K, Na, stages,
+                     stg_off, tma_out, ep);
   SKB_CHECK_LAUNCH("k_gemm_sw");
   return SKB_OK;
 }
 
 template <int KIND>
 static int launch_k2(int M, int N, int K, const CUtensorMap &mw, const CUtensorMap &mx,
-                     const CUtensorMap &mo, int Na, int CS, int stages, int stg_off, int tma_out,
+                     const OutMaps &mo, int Na, int CS, int stages, int stg_off, int tma_out,
                      size_t smem, EpiArgs ep, cudaStream_t st) {
   if constexpr (KIND == SKB_EPI_STORE || KIND == SKB_EPI_RELU)
     if (ep.lnx) {
@@ -1841,12 +1911,22 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   // TMA-store epilogue: the output tile is staged in the (drained) ring
   const bool f32o = ep.kind == SKB_EPI_RESID || ep.out_dtype == SKB_F32;
   const int es = f32o ? 4 : 2;
-  const int tma_out = ep.kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
-                      ((long)ep.ldo * es) % 16 == 0;
+  // SSRU with whole-K tiles (mode 2): cells and relu(cells) staged, written
+  // by a TMA store into the step's half of the cell buffer and a TMA
+  // reduce-add into x (c_next rows = M; ld and pitches 16-byte aligned)
+  const bool ssru_tma = ep.kind == SKB_EPI_SSRU && CS == 1 && ep.c_next &&
+                        (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(ep.c_next) & 15) == 0 && ep.ldo % 4 == 0 &&
+                        ep.ld_state % 4 == 0 && ep.state_stride % 4 == 0 && N % 2 == 0 && N / 2 <= ep.ld_state &&
+                        (!ep.step || ep.state_stride >= (long long)M * ep.ld_state) && Na <= 256;
+  const int tma_out = ssru_tma ? 2
+                               : (ep.kind != SKB_EPI_SSRU && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
+                                  ((long)ep.ldo * es) % 16 == 0);
   const int rows_box = CS == 1 ? Na : Na / CS;
   const int part_bytes = CS > 1 ? 2 * Na * 512 : 0;  // partial + receive slots
   const int stg_off = (part_bytes + 1023) & ~1023;
-  const int need = tma_out ? stg_off + ((rows_box + 15) / 16 * 16) * 128 * es : part_bytes;
+  const int need = ssru_tma ? Na * 512
+                            : (tma_out ? stg_off + ((rows_box + 15) / 16 * 16) * 128 * es : part_bytes);
   // Ring budget: half the SM by default, so the next kernel's CTA (PDL)
   // can become resident beside this one and prefetch its weights while this
   // one drains; the per-SM TMA ingest (~80-120 GB/s) is already reached
@@ -1864,12 +1944,16 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
   if (stages < 1 || stages * SB + fixed > SMEM_MAX)
     return fail(SKB_ERR_UNSUPPORTED, "gemm_sw: Na=%d CS=%d does not fit", Na, CS);
   const size_t smem = (size_t)stages * SB + fixed;
-  CUtensorMap mo;
-  if (tma_out) {
-    rc = make_map_out(&mo, ep.out, M, N, ep.ldo, f32o, rows_box);
+  OutMaps mo;
+  mo.a = mo.b = mw;  // (unused unless set below)
+  if (ssru_tma) {
+    rc = make_map_ssru(&mo.a, ep.out, M, N / 2, ep.ldo, 1, 0, Na);
     if (rc) return rc;
-  } else {
-    mo = mw;  // unused
+    rc = make_map_ssru(&mo.b, ep.c_next, M, N / 2, ep.ld_state, ep.step ? 2 : 1, ep.state_stride, Na);
+    if (rc) return rc;
+  } else if (tma_out) {
+    rc = make_map_out(&mo.a, ep.out, M, N, ep.ldo, f32o, rows_box);
+    if (rc) return rc;
   }
   if (i8) {
     if (ep.kind == SKB_EPI_RELU)
