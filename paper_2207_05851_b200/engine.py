@@ -373,6 +373,7 @@ class DecodeWorkspace:
         self.st_f64.copy_(self.init_f64, non_blocking=True)
 
     def _capture(self, fn, launches_attr):
+        STATS["captures"] += 1
         g = torch.cuda.CUDAGraph()
         before = kern.launches
         with torch.cuda.graph(g):
@@ -480,6 +481,7 @@ def _poll_stream(main: torch.cuda.Stream) -> torch.cuda.Stream:
     return _POLL_STREAMS[key]
 
 
+STATS = {"workspaces": 0, "captures": 0}  # cache misses (diagnostics: tools/e2e_var.py)
 HOST_TRACE = os.environ.get("SKB_HOST_TRACE", "0") == "1"
 HOST_MARKS: list = []  # (label, perf_counter) when SKB_HOST_TRACE=1 (tools/host_timeline.py)
 
@@ -517,6 +519,7 @@ def _workspace(model, key, *args):
         per.move_to_end(key)
         return ws
     ws = DecodeWorkspace(model, *args)
+    STATS["workspaces"] += 1
     ws.nbytes = _ws_bytes(ws)
     per[key] = ws
     total = sum(w.nbytes for p in _WS_CACHE.values() for w in p.values())
@@ -761,6 +764,7 @@ def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_
     results: list[ChunkResult | None] = [None] * len(jobs)
 
     def take(idx, bb):
+        _mark("finish: wait")
         for i, r in zip(idx, bb.finish()):
             results[i] = r
             if on_done is not None:

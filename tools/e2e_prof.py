@@ -15,7 +15,7 @@ from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translat
 model, vocabs, _ = bench.build_model("big")
 inputs = [SentenceInput(tokens=s) for k in range(9) for s in bench.synth_sentences(128, 30, 32000, seed=500 + k)]
 settings = SearchSettings(beam=5, length_alpha=1.0)
-engine.DECODE_STREAMS = 3
+engine.DECODE_STREAMS = 5
 translate(model, vocabs, inputs, settings, max_rows=640)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
