@@ -1996,6 +1996,15 @@ static int pick_cs(int N, int K) {
     long_k = e ? atoi(e) : 2;
   }
   if (nk >= 48 && n_wt <= 16) return long_k;
+  // K = 2048-class shapes of narrow N (base FFN2: N 512, K 2048) split in
+  // 2 as well: base beam-5 b64 +0.9 % at 5 streams, +3 % single stream
+  // (profiles/r2_103_var.txt).  SKB_CS_MIDK overrides.
+  static int mid_k = -1;
+  if (mid_k < 0) {
+    const char *e = getenv("SKB_CS_MIDK");
+    mid_k = e ? atoi(e) : 2;
+  }
+  if (mid_k > 1 && nk >= 32 && n_wt <= 8) return mid_k;
   // SKB_CS_SMALLN=2|4 also splits the narrow K = 1024 shapes (wo, wo_c):
   // still a function of (N, K) only, a latency / throughput trade-off —
   // measured on B200: 4 gives batch-1 greedy 21.4 ms (from 23.5) but costs
