@@ -2816,7 +2816,12 @@ static int gemm_impl(int in_dtype, int M, int N, int K, const void *A, int lda, 
     // automatic: wide plain GEMMs of large M (the cross-attention K/V
     // projection of a batch, N = 2 d D); the LOGITS epilogue measured slower
     // on the pair kernel (126.6 vs 116.1 us at M = 1280, profiles/r2_05_*)
-    const bool pc_auto = M >= pc::g_min_m && N >= 8192 && epi->kind != SKB_EPI_LOGITS;
+    static int pc_min_n = -1;  // SKB_PC_MIN_N: narrowest N the automatic choice sends here
+    if (pc_min_n < 0) {
+      const char *e = getenv("SKB_PC_MIN_N");
+      pc_min_n = e ? atoi(e) : 8192;
+    }
+    const bool pc_auto = M >= pc::g_min_m && N >= pc_min_n && epi->kind != SKB_EPI_LOGITS;
     if (pc_ok && (pc::g_mode == 2 || (pc::g_mode == 0 && pc_auto))) {
       if (epi->ln_in) {
         rc = ln_before(in_dtype, M, K, A, lda, epi, stream);
