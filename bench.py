@@ -326,6 +326,73 @@ def topk_roofline(bb, hbm_peak, reps=20):
             "algorithmic_bytes_per_launch": nbytes, "traffic": _beam_traffic()}
 
 
+def attention_roofline(bb, model, hbm_peak, t=35, reps=10):
+    """The decode step's attention kernels at step t of the benchmark batch,
+    all decoder layers back to back on their stream (CUDA events):
+    self-attention over the KV cache (k_self_attn_tc over the step plan;
+    algorithmic bytes = the distinct cached (slot, position) entries the
+    sentences' beam rows read, K and V of every head, bf16) and
+    cross-attention (k_cross_tc; bytes = every sentence's encoder K and V
+    rows up to its length, once per layer).  achieved = bytes per layer / time per layer."""
+    import numpy as np
+    import torch
+    from paper_2207_05851_b200 import kern
+    c = model.config
+    if c.decoder_kind == "ssru":
+        return None
+    sb, K, B = bb.sb, bb.K, bb.B
+    R, H, dh, d = B * K, c.heads, c.head_dim, c.d_model
+    D = len(model.dec)
+    sb.step.fill_(t)
+    if sb.plan is not None:
+        kern.attn_plan(sb.anc, sb.step, sb.plan, R, sb.S_max, sb.group)
+    anc = sb.anc[t & 1, :, :t].cpu().numpy()
+    entries = sum(len({(int(anc[r, p]), p) for r in range(b * K, b * K + K) for p in range(t)}) + K
+                  for b in range(B))
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(3):
+            e0.record(st)
+            for _ in range(reps):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / (reps * D))
+        return best * 1e3  # us per layer
+
+    def self_all():
+        for li in range(D):
+            kern.self_attention_step(sb.qkv, sb.kc[li], sb.vc[li], sb.anc, sb.step, sb.ctx, R, H, dh,
+                                     sb.S_max, sb.group, plan=sb.plan)
+
+    def cross_all():
+        for li in range(D):
+            kern.cross_attention_step(sb.q, sb.ckv, li * 2 * d, li * 2 * d + d, sb.L, sb.row_sent,
+                                      sb.lengths, sb.ctx, R, H, dh, sb.group)
+
+    us_self, us_cross = timed(self_all), timed(cross_all)
+    b_self = entries * H * dh * 2 * 2
+    b_cross = int(sb.lengths.sum().item()) * 2 * d * 2  # encoder K,V rows within each length
+    out = {}
+    for name, us, nb, kern_name in (("self", us_self, b_self, "k_self_attn_tc (step plan)"),
+                                    ("cross", us_cross, b_cross, "k_cross_tc")):
+        ach = nb / (us / 1e6) / 1e9
+        out[name] = {"kernel": kern_name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "us_per_layer": round(us, 2),
+                     "algorithmic_bytes_per_layer": int(nb)}
+    out["self"]["distinct_entries"] = int(entries)
+    out["step"] = t
+    out["how"] = ("all decoder layers back to back at step %d of the benchmark batch, CUDA events; "
+                  "the kernels stage cached entries before griddepcontrol.wait, which these "
+                  "back-to-back launches overlap as in the decode graph" % t)
+    return out
+
+
 def _beam_traffic():
     """DRAM bytes per k_beam_step launch from the committed ncu capture
     (profiles/r1_beam_step_traffic.json), or None."""
@@ -717,6 +784,7 @@ def run_ours(args):
     breakdown = step_breakdown(bb)
     topk = topk_roofline(bb, hbm)
     topk["peak_source"] = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback"
+    attn_roof = attention_roofline(bb, model, hbm)
     floor = ideal_floor(model, B, K, L, S, peaks.get("bf16_tflops_sustained", 1422.5), hbm, U=U,
                         distinct=distinct)
     floor["frac"] = round(value / world / floor["sentences_per_s"], 4)
@@ -732,7 +800,7 @@ def run_ours(args):
                    "ms_per_batch_single_stream": round(r["ms_single"] / args.steps, 3),
                    "union_columns": int(U),
                    "l2": "working set > L2 (weights 0.48 GB + KV cache 1.1 GB per batch)"},
-        "e2e": e2e, "batch1_latency": lat, "roofline": roof, "roofline_topk": topk,
+        "e2e": e2e, "batch1_latency": lat, "roofline": roof, "roofline_topk": topk, "roofline_attention": attn_roof,
         "floor": floor, "gpu_launches": launches,
         "clocks": clk,
         "decode": {"mean_steps_per_sentence": round(steps_per_sent, 2),
