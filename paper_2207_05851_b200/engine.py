@@ -740,17 +740,40 @@ class BeamBatch:
         return out
 
 
-def decode_jobs(model: Model, jobs: list[ChunkJob], beam: int, alpha: float,
+class LazyJobs:
+    """Chunk jobs built on first access, with their source lengths known up
+    front for the length sort: decode_jobs builds a batch's jobs (the host's
+    vocabulary encoding) right before launching it, so only the first batch
+    waits for host preprocessing and the rest overlaps the GPU work of the
+    batches launched before it."""
+
+    def __init__(self, lengths: list[int], make):
+        self.lengths = lengths
+        self._make = make
+        self._jobs: list = [None] * len(lengths)
+
+    def __len__(self) -> int:
+        return len(self.lengths)
+
+    def __getitem__(self, i: int) -> ChunkJob:
+        j = self._jobs[i]
+        if j is None:
+            j = self._jobs[i] = self._make(i)
+        return j
+
+
+def decode_jobs(model: Model, jobs, beam: int, alpha: float,
                 nvs_threshold: float | None = None, max_rows: int = 2560,
                 use_graph: bool = True, on_done=None) -> list[ChunkResult]:
-    """Decode chunks in length-sorted device batches of <= max_rows rows.
-    Results are independent of batch composition (row-wise kernels with a
+    """Decode chunks (a list of ChunkJob, or LazyJobs) in length-sorted
+    device batches of <= max_rows rows.  Results are independent of batch composition (row-wise kernels with a
     fixed reduction order), so sorting never changes outputs.  on_done(i, r)
     is called for every chunk as soon as its batch is read back, while the
     later batches still decode (host post-processing overlaps the GPU)."""
     if not jobs:
         return []
-    order = sorted(range(len(jobs)), key=lambda i: -len(jobs[i].src_ids))
+    lens = jobs.lengths if isinstance(jobs, LazyJobs) else [len(j.src_ids) for j in jobs]
+    order = sorted(range(len(jobs)), key=lambda i: -lens[i])
     per_batch = max(1, max_rows // beam)
     # Batches run concurrently on DECODE_STREAMS CUDA streams (batch n on
     # stream n % S); on each stream batch n+S is prepared and launched before
@@ -765,7 +788,9 @@ def _decode_jobs(model, jobs, beam, alpha, nvs_threshold, order, per_batch, use_
 
     def take(idx, bb):
         _mark("finish: wait")
-        for i, r in zip(idx, bb.finish()):
+        rs = bb.finish()
+        _mark("finish: done")
+        for i, r in zip(idx, rs):
             results[i] = r
             if on_done is not None:
                 on_done(i, r)

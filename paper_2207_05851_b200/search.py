@@ -29,7 +29,7 @@ import torch
 from . import kern
 from . import _native as N
 from .checkpoint import Vocabulary
-from .engine import ChunkJob, ChunkResult, decode_jobs
+from .engine import ChunkJob, ChunkResult, LazyJobs, decode_jobs
 from .errors import ConfigError, InputError
 from .shortlist import sorted_union
 from .model import (BOS_ID, EOS_ID, PAD_ID, SHIFT_ID, UNK_ID, Model, validate_active_ids)
@@ -159,6 +159,8 @@ def chunk_input(inp: SentenceInput, max_seq_len: int) -> list[SentenceInput]:
         raise InputError(f"source prefix ({plen} tokens) leaves no room in a window of "
                          f"{max_seq_len}")
     budget = max_seq_len - plen
+    if len(inp.tokens) <= budget:
+        return [inp]  # one window: the chunk is the input itself (never mutated)
     out = []
     for start in range(0, len(inp.tokens), budget):
         with_target = start == 0 or inp.prefix_all_chunks
@@ -276,8 +278,9 @@ def translate(model, vocabs, inputs, settings: SearchSettings | None = None,
     cfg = model.config
     nf = len(cfg.target_factor_specs)
     plans: list = []
-    jobs: list[ChunkJob] = []
-    nvs_thr = None
+    all_chunks: list[SentenceInput] = []
+    lens: list[int] = []
+    nvs_thr = settings.restriction.threshold if isinstance(settings.restriction, NvsRestriction) else None
     for inp in inputs:
         try:
             inp.validate()
@@ -288,17 +291,17 @@ def translate(model, vocabs, inputs, settings: SearchSettings | None = None,
                 raise InputError(f"model has {nf} target factor streams, prefix factors name "
                                  f"{len(inp.target_prefix_factors)}")
             chunks = chunk_input(inp, cfg.max_seq_len)
-            first = len(jobs)
-            built = []
-            for ch in chunks:
-                job, nvs = _chunk_job(model, ch, vocabs, settings.restriction)
-                built.append(job)
-                nvs_thr = nvs
-            jobs.extend(built)
-            plans.append((inp, chunks, first))
+            n_src = [len(ch.source_prefix) + len(ch.tokens) for ch in chunks]
+            for ch, n in zip(chunks, n_src):  # _chunk_job's only input check, from lengths
+                _check_prefix_budget(ch.target_prefix, _max_output_len(n))
+            plans.append((inp, chunks, len(all_chunks)))
+            all_chunks.extend(chunks)
+            lens.extend(n_src)
         except InputError as e:
             logger.warning("input skipped: %s", e)
             plans.append(str(e))
+    # the chunks' ids are encoded when their device batch is launched
+    jobs = LazyJobs(lens, lambda i: _chunk_job(model, all_chunks[i], vocabs, settings.restriction)[0])
     texts: dict = {}  # chunk index -> (surface tokens, factor tokens), built while the GPU decodes
 
     def detok(i, r):
@@ -311,8 +314,8 @@ def translate(model, vocabs, inputs, settings: SearchSettings | None = None,
             results = [_hyp(r) for r in decode_jobs(model, jobs, K, settings.length_alpha,
                                                     nvs_thr, max_rows, on_done=detok)]
         else:
-            results = [ProtocolSearch.from_job(model, j, K, settings.restriction,
-                                               settings.length_alpha).run() for j in jobs]
+            results = [ProtocolSearch.from_job(model, jobs[i], K, settings.restriction,
+                                               settings.length_alpha).run() for i in range(len(jobs))]
     records = []
     for plan in plans:
         if isinstance(plan, str):
