@@ -985,20 +985,39 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
   if constexpr (PLAN) {
     const int nb = (R + G - 1) / G, emax = G * S_max;
     const AttnPlanView pv = plan_view(plan, nb, emax);
-    E = __ldcg(pv.E + blockIdx.x);
     const size_t o = (size_t)blockIdx.x * emax;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    // One L2 round trip: E and, speculatively, the first pass's entries
+    // (lane k of warp w holds entry w + HG*k, the k-th this warp stages) are
+    // loaded together into registers; the warps stage from their registers
+    // (warp broadcast) without a shared-memory round trip or block barrier.
+    E = __ldcg(pv.E + blockIdx.x);
+    const int my_e = warp + HG * lane;
+    int r_src = 0, r_pos = 0;
+    if (my_e < min(cap, emax)) {
+      r_src = __ldcg(pv.src + o + my_e);
+      r_pos = __ldcg(pv.pos + o + my_e);
+      emask[my_e] = __ldcg(pv.mask + o + my_e);
+      esrc[my_e] = (short)r_src;
+      epos[my_e] = (short)r_pos;
+    }
+    const int n1 = min(E, cap);
+    // entries of later passes (E > cap) through shared memory, read after the
+    // block barrier that precedes the first pass's attention
+    for (int e = cap + threadIdx.x; e < E; e += blockDim.x) {
       esrc[e] = __ldcg(pv.src + o + e);
       epos[e] = __ldcg(pv.pos + o + e);
       emask[e] = __ldcg(pv.mask + o + e);
     }
-    __syncthreads();
     // first pass, cached entries (earlier steps) before the dependency wait
-    for (int e = warp; e < min(E, cap); e += HG)
-      if (esrc[e] >= 0) stage(e, esrc[e], epos[e]);
+    for (int k = 0; warp + HG * k < n1; ++k) {
+      const int sl = __shfl_sync(0xffffffffu, r_src, k), p = __shfl_sync(0xffffffffu, r_pos, k);
+      if (sl >= 0) stage(warp + HG * k, sl, p);
+    }
     PDL_ENTRY();
-    for (int e = warp; e < min(E, cap); e += HG)
-      if (esrc[e] < 0) stage(e, esrc[e], epos[e]);
+    for (int k = 0; warp + HG * k < n1; ++k) {
+      const int sl = __shfl_sync(0xffffffffu, r_src, k), p = __shfl_sync(0xffffffffu, r_pos, k);
+      if (sl < 0) stage(warp + HG * k, sl, p);
+    }
   } else {
     // ---- walk, sweep 1: one 32-position block per warp (one position per
     // lane): ancestor slots of the G rows, distinct slots per position (first
@@ -1068,8 +1087,8 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
   asm volatile("cp.async.commit_group;" ::: "memory");
   AT_STAMP(2);
   // this step's k/v of my heads, for slot (row, t): loaded now (overlapping
-  // the staging copies), stored after the attention (only later steps read
-  // them; this step's copies source position t from qkv)
+  // the staging copies) and stored once the Q fragments are loaded (only
+  // later steps read them; this step's copies source position t from qkv)
   constexpr int KVC = (GW * RUN / 16 + 32 * HG - 1) / (32 * HG);  // chunks per thread, G <= GW
   uint4 kvk[KVC], kvv[KVC];
 #pragma unroll
@@ -1098,6 +1117,18 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
       qa[ks][1] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0) : 0u;
       qa[ks][2] = va ? *reinterpret_cast<const uint32_t *>(qa_p + c0 + 8) : 0u;
       qa[ks][3] = vb ? *reinterpret_cast<const uint32_t *>(qb_p + c0 + 8) : 0u;
+    }
+  }
+  // this step's k/v into the cache slot (row, t) now (the loads above have
+  // had the Q loads' time to land; nothing in this launch reads the slot)
+#pragma unroll
+  for (int q = 0; q < KVC; ++q) {
+    const int c = threadIdx.x + q * 32 * HG;
+    if (c < nr * (RUN / 16)) {
+      const int i = c / (RUN / 16), u = c % (RUN / 16);
+      const size_t cs = (((size_t)(r0 + i) * S_max + t) * H + h0) * DH + u * 8;
+      *reinterpret_cast<uint4 *>(kc + cs) = kvk[q];
+      *reinterpret_cast<uint4 *>(vc + cs) = kvv[q];
     }
   }
   const bool rva = gq < nr, rvb = gq + 8 < nr;
@@ -1140,6 +1171,9 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
         }
       }
     }
+    // rows gq + 8 exist only for groups of more than 8 rows (beam > 8):
+    // otherwise their scores are never used and the softmax skips them
+    const bool hb = nr > 8;
     float cm_a = -INFINITY, cm_b = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -1155,7 +1189,7 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
           } else {
             const int pe = epos[eb + ej], ke = ek[eb + ej];
             oka = rva && pla[pe] == ke;
-            okb = rvb && plb[pe] == ke;
+            okb = hb && rvb && plb[pe] == ke;
           }
         }
         sc[nt][e] = oka ? sc[nt][e] * scale : -INFINITY;
@@ -1166,7 +1200,7 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
 #pragma unroll
     for (int o2 = 1; o2 < 4; o2 <<= 1) {
       cm_a = fmaxf(cm_a, __shfl_xor_sync(0xffffffffu, cm_a, o2));
-      cm_b = fmaxf(cm_b, __shfl_xor_sync(0xffffffffu, cm_b, o2));
+      if (hb) cm_b = fmaxf(cm_b, __shfl_xor_sync(0xffffffffu, cm_b, o2));
     }
     const float mn_a = fmaxf(m_a, cm_a), mn_b = fmaxf(m_b, cm_b);
     const float cr_a = mn_a == -INFINITY ? 1.f : (m_a == -INFINITY ? 0.f : __expf(m_a - mn_a));
@@ -1177,14 +1211,24 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         sc[nt][e] = sc[nt][e] == -INFINITY ? 0.f : __expf(sc[nt][e] - mn_a);
-        sc[nt][2 + e] = sc[nt][2 + e] == -INFINITY ? 0.f : __expf(sc[nt][2 + e] - mn_b);
         ps_a += sc[nt][e];
-        ps_b += sc[nt][2 + e];
       }
+    if (hb) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          sc[nt][2 + e] = sc[nt][2 + e] == -INFINITY ? 0.f : __expf(sc[nt][2 + e] - mn_b);
+          ps_b += sc[nt][2 + e];
+        }
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) sc[nt][2] = sc[nt][3] = 0.f;
+    }
 #pragma unroll
     for (int o2 = 1; o2 < 4; o2 <<= 1) {
       ps_a += __shfl_xor_sync(0xffffffffu, ps_a, o2);
-      ps_b += __shfl_xor_sync(0xffffffffu, ps_b, o2);
+      if (hb) ps_b += __shfl_xor_sync(0xffffffffu, ps_b, o2);
     }
     l_a = l_a * cr_a + ps_a;
     l_b = l_b * cr_b + ps_b;
@@ -1193,7 +1237,7 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
 #pragma unroll
     for (int nn = 0; nn < DH / 8; ++nn) {
       o[nn][0] *= cr_a; o[nn][1] *= cr_a;
-      o[nn][2] *= cr_b; o[nn][3] *= cr_b;
+      if (hb) { o[nn][2] *= cr_b; o[nn][3] *= cr_b; }
     }
     // ---- O += P V, 16 entries per k-step
 #pragma unroll
@@ -1218,16 +1262,6 @@ __global__ void __launch_bounds__(32 * HG, 16 / HG) k_self_attn_tc(
     __syncthreads();  // the staging area is reused by the next pass
   }
   AT_STAMP(5);
-#pragma unroll
-  for (int q = 0; q < KVC; ++q) {
-    const int c = threadIdx.x + q * 32 * HG;
-    if (c < nr * (RUN / 16)) {
-      const int i = c / (RUN / 16), u = c % (RUN / 16);
-      const size_t cs = (((size_t)(r0 + i) * S_max + t) * H + h0) * DH + u * 8;
-      *reinterpret_cast<uint4 *>(kc + cs) = kvk[q];
-      *reinterpret_cast<uint4 *>(vc + cs) = kvv[q];
-    }
-  }
   // ---- normalise and store rows gq, gq+8
   const float ia = 1.0f / l_a, ib = 1.0f / l_b;
 #pragma unroll
