@@ -12,7 +12,9 @@ import torch
 sys.path.insert(0, ".")
 from paper_2207_05851_b200 import kern  # noqa: E402
 
-B, K, H, dh, S = 128, 5, 16, 64, 70
+import os
+B, K = int(os.environ.get("B", "128")), int(os.environ.get("K", "5"))
+H, dh, S = 16, 64, 70
 R, D = B * K, H * dh
 dev = "cuda"
 rng = np.random.default_rng(0)
