@@ -241,12 +241,22 @@ class DecodeWorkspace:
 
     CHUNK = int(os.environ.get("SKB_GRAPH_CHUNK", "8"))  # decode steps per captured graph
 
+    @property
+    def model(self) -> Model:
+        m = self._model()
+        if m is None:
+            raise RuntimeError("the workspace's model was released")
+        return m
+
     def __init__(self, model: Model, B: int, L: int, S_max: int, K: int, P: int, U: int,
                  alpha: float, restricted: bool):
         c = model.config
         dev = model.device
         nf, nsf = len(c.target_factor_specs), len(c.source_factor_specs)
-        self.model, self.B, self.L, self.S_max, self.K, self.P, self.U = model, B, L, S_max, K, P, U
+        # weak: the per-model workspace cache is a WeakKeyDictionary, whose
+        # values must not keep their key (the model) alive
+        self._model = weakref.ref(model)
+        self.B, self.L, self.S_max, self.K, self.P, self.U = B, L, S_max, K, P, U
         self.nf, self.nsf, self.restricted = nf, nsf, restricted
         R = B * K
         self.R = R

@@ -181,3 +181,28 @@ def test_translate_from_reference_written_model_dir(name):
         assert r.text == g["text"] and r.factors == g["factors"] and r.chunks == g["chunks"]
         if g["error"] is None:
             assert abs(r.score - g["score"]) < 1e-4
+
+
+def test_workspaces_released_with_model():
+    """A released Model takes its cached decode workspaces (KV cache, graphs)
+    with it: the per-model cache is weak in the model, and the workspaces
+    hold only a weak reference back (cached workspaces kept old
+    models alive)."""
+    import gc
+    import weakref
+
+    from fixture_models import oracle_model, product_config
+    from paper_2207_05851_b200 import engine
+    from paper_2207_05851_b200.model import Model
+    from paper_2207_05851_b200.search import SearchSettings, SentenceInput, translate
+    case = next(c for c in SEARCH_CASES if c["name"] == "toy_beam3")
+    m = Model(product_config("toy"), params=oracle_model("toy").p, precision="bf16")
+    translate(m, product_vocabs("toy"), [SentenceInput(**i) for i in case["inputs"]],
+              SearchSettings(beam=3))
+    assert m in engine._WS_CACHE and len(engine._WS_CACHE[m]) > 0
+    ref = weakref.ref(m)
+    del m
+    gc.collect()
+    assert ref() is None
+    assert all(k is not None for k in engine._WS_CACHE.keys())
+    assert not any(ref() is k for k in engine._WS_CACHE.keys())
