@@ -88,16 +88,17 @@ for name, (Nn, K) in SHAPES.items():
     if os.environ.get("SW_SWEEP"):
         cfgs.insert(1, ("tc auto", 1, 0, 0))
         for na in (32, 48, 64, 80, 96, 128, 160, 256):
-            for cs in ((1, 2, 4) if K >= 4096 else (1,)):
+            for cs in ((1, 2, 4) if K >= 4096 else tuple(int(x) for x in os.environ.get("SW_CS", "1").split(","))):
                 if cs > 1 and na % (4 * cs):
                     continue
                 cfgs.append((f"sw na{na} cs{cs}", 2, na, cs))
     # persistent CTA-pair kernel (mode 2 = forced), its tile and grid choices
-    cfgs.append(("pc auto", -2, 0, 0))
-    for na in (64, 96, 128, 160, 192, 224, 256):
-        cfgs.append((f"pc na{na}", -2, na, 0))
-    for pairs in (32, 48, 64):
-        cfgs.append((f"pc pairs{pairs}", -2, 0, pairs))
+    if not os.environ.get("NO_PC"):
+        cfgs.append(("pc auto", -2, 0, 0))
+        for na in (64, 96, 128, 160, 192, 224, 256):
+            cfgs.append((f"pc na{na}", -2, na, 0))
+        for pairs in (32, 48, 64):
+            cfgs.append((f"pc pairs{pairs}", -2, 0, pairs))
     for label, mode, na, cs in cfgs:
         if mode == -2:
             lib.skb_gemm_force_sw(0, 0, 0)
@@ -113,7 +114,7 @@ for name, (Nn, K) in SHAPES.items():
             us = time_graph(ours, REPS)
         except Exception as e:  # noqa: BLE001
             print(json.dumps(dict(shape=name, cfg=label, error=str(e)[:80])))
-            break
+            continue
         out_rows.append(dict(shape=name, M=M, cfg=label, us=round(us, 2),
                              tflops=round(flops / us / 1e6, 1), err=round(err, 4)))
         print(json.dumps(out_rows[-1]), flush=True)
