@@ -55,7 +55,12 @@ for name, (Nn, K) in shapes.items():
             xin.data_ptr(), K, gin.data_ptr(), bin_.data_ptr(), 1e-5)
     epi.k_split = int(os.environ.get("KSPLIT", "0"))
     for na, cs in cfgs:
-        N.call("skb_gemm_force_sw", 2, na, cs)
+        pc = bool(os.environ.get("PC"))  # the persistent CTA-pair kernel (cs = pairs)
+        if pc:
+            N.call("skb_gemm_force_sw", 0, 0, 0)
+            N.call("skb_gemm_force_pc", 2, na, cs)
+        else:
+            N.call("skb_gemm_force_sw", 2, na, cs)
         buf = (C.c_ulonglong * (1024 * 16))()
         for i in range(8):  # warm; the last launch is traced (its weights cold)
             if i == 7:
@@ -69,9 +74,13 @@ for name, (Nn, K) in shapes.items():
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         cols = [0, 2, 3, 5, 1, 8, 9, 10, 4, 11, 12, 13, 14, 6]
-        rel = (t[:, cols] - t0) / 1e3
         labels = ["entry", "postwait", "stage0", "accready", "epi/partial", "csync", "recv",
                   "summed", "stored", "flushed", "stats", "ln_ticket/ln_in_done", "ln_rows/mma_xready", "exit"]
+        if pc:  # k_gemm_pc's PC_STAMP slots
+            cols = [0, 1, 2, 3, 4, 5, 6, 8, 9]
+            labels = ["entry", "alloc+csync", "postwait", "stage0", "mma0 issued", "accready0",
+                      "epi0 done", "stores drained", "exit"]
+        rel = (t[:, cols] - t0) / 1e3
         print(f"{name} na={na} cs={cs} ctas={len(t)} sms={len(set(t[:, 7]))}")
         for j, lab in enumerate(labels):
             col = rel[:, j]
@@ -80,3 +89,4 @@ for name, (Nn, K) in shapes.items():
                 continue
             print(f"   {lab:9s} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
 N.call("skb_gemm_force_sw", 0, 0, 0)
+N.call("skb_gemm_force_pc", 0, 0, 0)
