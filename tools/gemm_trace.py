@@ -14,14 +14,16 @@ from paper_2207_05851_b200 import _native as N  # noqa: E402
 import os
 M = int(os.environ.get("M", "640"))
 shapes = {"wo": (1024, 1024), "ffn2": (1024, 4096), "qkv": (3072, 1024), "ffn1": (4096, 1024),
-          "out_proj": (32000, 1024), "ssru": (2048, 1024)}
+          "out_proj": (32000, 1024), "ssru": (2048, 1024),
+          "wide": (20480, 1024)}  # wide: with M = Na every weight tile has exactly one reader
 import os
 if os.environ.get("SHAPES"):
     shapes = {k: shapes[k] for k in os.environ["SHAPES"].split(",")}
 cfgs = [(int(a), int(b)) for a, b in (x.split(",") for x in sys.argv[1:])] or [(0, 0)]
 for name, (Nn, K) in shapes.items():
     A = torch.randn(M, K, device="cuda").bfloat16()
-    Ws = [torch.randn(Nn, K, device="cuda").bfloat16() for _ in range(8 if Nn * K < 1e8 / 2 else 2)]
+    ncopy = int(os.environ.get("COPIES", "0")) or (8 if Nn * K < 1e8 / 2 else 2)
+    Ws = [torch.randn(Nn, K, device="cuda").bfloat16() for _ in range(ncopy)]
     if os.environ.get("RESIDLN"):
         out = torch.zeros(M, Nn, device="cuda")
         hln = torch.zeros(M, Nn, device="cuda", dtype=torch.bfloat16)
