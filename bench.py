@@ -215,10 +215,11 @@ def batch1_latency(model, vocabs, L, V, n=21, restriction=None, which=(("greedy"
 
 def _gemm_traffic():
     """DRAM bytes (read + write) of one decode step's GEMM launches from the
-    committed ncu --set full capture (profiles/r1_gemm_step_traffic.json,
+    committed ncu --set full capture (profiles/r2_gemm_step_traffic.json,
     made by tools/ncu_step.sh; cold-L2 serialised replay), or None."""
-    p = ROOT / "profiles" / "r1_gemm_step_traffic.json"
-    if not p.exists():
+    p = next((q for q in (ROOT / "profiles" / f"{r}_gemm_step_traffic.json" for r in ("r2", "r1"))
+              if q.exists()), None)
+    if p is None:
         return None
     d = json.loads(p.read_text())
     return {"bytes_per_step": d["dram_bytes_per_step"], "source": d["source"]}
@@ -395,9 +396,10 @@ def attention_roofline(bb, model, hbm_peak, t=35, reps=10):
 
 def _beam_traffic():
     """DRAM bytes per k_beam_step launch from the committed ncu capture
-    (profiles/r1_beam_step_traffic.json), or None."""
-    p = ROOT / "profiles" / "r1_beam_step_traffic.json"
-    if not p.exists():
+    (profiles/r2_beam_step_traffic.json), or None."""
+    p = next((q for q in (ROOT / "profiles" / f"{r}_beam_step_traffic.json" for r in ("r2", "r1"))
+              if q.exists()), None)
+    if p is None:
         return None
     d = json.loads(p.read_text())
     return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": d["source"]}
