@@ -1347,23 +1347,23 @@ __global__ void __launch_bounds__(192, 1)
       // weights first: independent of the previous kernel (PDL prologue)
       const int pre = nkc < stages ? nkc : stages;
 #ifdef SKB_GEMM_TRACE
-      // timing experiments: 4 = skip the activation loads, 5 = skip weights
+      // timing experiments: 4 = skip the activation loads, 5 = skip weights, 6 = both
       const int ldbg = g_dbg;
 #else
       constexpr int ldbg = 0;
 #endif
-      const int sbx = lnx ? W_BYTES : (ldbg == 4 ? W_BYTES : (ldbg == 5 ? SB - W_BYTES : SB));
+      const int sbx = ldbg == 6 ? 0 : (lnx ? W_BYTES : (ldbg == 4 ? W_BYTES : (ldbg == 5 ? SB - W_BYTES : SB)));
 #pragma unroll 1
       for (int q = 0; q < pre; ++q) {
         mbar_expect_tx(&full[q], sbx);
-        if (ldbg != 5) tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * KBE, n0, &full[q]);
+        if (ldbg != 5 && ldbg != 6) tma_load_2d(smem + q * SB, &tmW, (kb0 + q) * KBE, n0, &full[q]);
       }
       pdl_wait();
       if (!ep.late_trigger) pdl_trigger();
       SW_STAMP(2);
 #pragma unroll 1
       for (int q = 0; q < pre; ++q)
-        if (ldbg != 4 && !lnx) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * KBE, m0, &full[q]);
+        if (ldbg != 4 && ldbg != 6 && !lnx) tma_load_2d(smem + q * SB + W_BYTES, &tmX, (kb0 + q) * KBE, m0, &full[q]);
 #pragma unroll 1
       for (int it = pre; it < nkc; ++it) {
         const int s = it % stages;
@@ -1371,8 +1371,8 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t *st = smem + s * SB;
         mbar_expect_tx(&full[s], sbx);
-        if (ldbg != 5) tma_load_2d(st, &tmW, (kb0 + it) * KBE, n0, &full[s]);
-        if (ldbg != 4 && !lnx) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * KBE, m0, &full[s]);
+        if (ldbg != 5 && ldbg != 6) tma_load_2d(st, &tmW, (kb0 + it) * KBE, n0, &full[s]);
+        if (ldbg != 4 && ldbg != 6 && !lnx) tma_load_2d(st + W_BYTES, &tmX, (kb0 + it) * KBE, m0, &full[s]);
       }
     } else {
       pdl_wait();
