@@ -630,18 +630,28 @@ def e2e_translate(model, vocabs, restriction, B, K, L, alpha, steps, n_streams, 
     flat = sum(host_inputs, [])
     per_call = int(os.environ.get("SKB_E2E_CALL_SENTS", "0")) or len(flat)
     groups = [flat[g:g + per_call] for g in range(0, len(flat), per_call)]
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # REPS timed passes over the same host inputs (each one complete: H2D,
+    # decode, D2H, records); the median is reported, every pass listed — a
+    # single pass of ~0.2 s varies with the device's power-capped clocks
+    reps = max(1, int(os.environ.get("SKB_E2E_REPS", "3")))
     s0 = dict(_eng.STATS)
-    e0.record()
-    for inp in groups:
-        recs = translate(model, vocabs, inp, settings, max_rows=B * K)
-    e1.record()
+    samples = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for inp in groups:
+            recs = translate(model, vocabs, inp, settings, max_rows=B * K)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        samples.append(float(t.item()))
     misses = {k: _eng.STATS[k] - s0[k] for k in s0}
-    torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = statistics.median(samples)
     S = 2 * L + 10
     h2d = B * L * 4 + B * 4 * 4 + B * 8          # ids, lengths/limits/prefix, step tables
     d2h = B * S * 4 + B * (8 + 4 + 4) + B * S * 4  # tokens, best score/steps/forced, factors
@@ -649,6 +659,7 @@ def e2e_translate(model, vocabs, restriction, B, K, L, alpha, steps, n_streams, 
     return {"value": round(world * B * steps / (e2e_ms / 1e3), 2), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": "paper_2207_05851_b200.search.translate",
+            "passes_sentences_per_s": [round(world * B * steps / (m / 1e3), 2) for m in samples],
             "cache_misses_in_timed_call": misses}
 
 
