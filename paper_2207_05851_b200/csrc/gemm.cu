@@ -2030,11 +2030,23 @@ static int pick_na(int M, int N, int CS, int conc) {
   const int slots = 2 * tc::num_sms() / (conc > 0 ? conc : 1);
   const int n_wt = (N + 127) / 128;
   const int na_max = CS > 1 ? 80 : 160;  // split-K partial + receive slots fit the ring
-  static int na_floor = -1;
-  if (na_floor < 0) {
+  // Smallest tile worth issuing: a 128 x Na x 16 tcgen05.mma costs the same
+  // ~71 cycles for every Na <= 128 (profiles/r2_136_gemm_mainloop_findings.txt),
+  // so with several decode streams sharing the SMs (total tensor work, not
+  // one GEMM's latency, is what counts) tiles of >= 128 rows issue 2-8x
+  // fewer instructions for the same work: big 6-6 at 5 streams (M = 640)
+  // 5703 -> 5791 sentences/s (r2_140).  One stream keeps the one-wave small
+  // tiles (3160 vs 2893), and so do GEMMs of < 512 rows, whose few tiles
+  // leave SMs idle (base b64 at M = 320 8096 -> 7943, SSRU greedy at
+  // M = 128 20292 -> 19636 with the floor, r2_141).  Numerics do not depend
+  // on Na.  SKB_SW_NA_MIN overrides.
+  static int na_env = -2;
+  if (na_env == -2) {
     const char *e = getenv("SKB_SW_NA_MIN");
-    na_floor = e ? atoi(e) : 16;
+    na_env = e ? atoi(e) : -1;
   }
+  int na_floor = na_env >= 0 ? na_env : (conc > 1 && M >= 512 ? 128 : 16);
+  if (na_floor > (M + 15) / 16 * 16) na_floor = (M + 15) / 16 * 16;
   int best = 16;
   double best_c = 1e30;
   for (int na = 16; na <= na_max; na += 16) {
