@@ -1986,14 +1986,18 @@ static int launch(int M, int N, int K, const void *X, int ldx, const void *W, in
 static int pick_cs(int N, int K) {
   const int nk = (K + tc::BK - 1) / tc::BK;
   const int n_wt = (N + 127) / 128;
-  // Long-K shapes (FFN2, K = 4096) split in 2: measured on B200 (bench, 3
-  // decode streams, profiles/r2_55_exp.txt, r2_56_exp.txt): split 4 -> 5070,
-  // 2 -> 5400, 1 -> 5476 sentences/s, single stream 3131 / 3121 / 2914.
-  // SKB_CS_LONGK overrides.
+  // Long-K shapes (FFN2, K = 4096): whole-K tiles.  Measured on B200
+  // (bench, 3 decode streams, profiles/r2_55_exp.txt, r2_56_exp.txt): split
+  // 4 -> 5070, 2 -> 5400, 1 -> 5476 sentences/s, single stream 3131 / 3121 /
+  // 2914; with the >= 128-row tiles under concurrency (pick_na), which a
+  // cluster split cannot use (its partial buffers cap Na at 80), 5 streams
+  // 5898 (split 2) -> 6190 (split 1), single stream 3160 -> 2944
+  // (profiles/r2_149_longk_split_ab.txt).  A function of (N, K) only, as
+  // batch invariance requires.  SKB_CS_LONGK overrides.
   static int long_k = -1;
   if (long_k < 0) {
     const char *e = getenv("SKB_CS_LONGK");
-    long_k = e ? atoi(e) : 2;
+    long_k = e ? atoi(e) : 1;
   }
   if (nk >= 48 && n_wt <= 16) return long_k;
   // K = 2048-class shapes of narrow N (base FFN2: N 512, K 2048) split in
